@@ -1,0 +1,176 @@
+// gconv.cu — grouped convolution with the reference's sequential bias
+// update (proj/kernels/gconv.tc:2-7):
+//   O(n,g,o,h,w) +=! I(n,g,i,h+kh,w+kw) * W1(g,o,i,kh,kw)
+//   O(n,g,o,h,w)  =  O(n,g,o,h,w) + B(m)      for m = 0..M-1, one by one
+//
+// Direct (implicit-GEMM-shaped) convolution on the FFMA pipe. A CTA owns
+// one (image n, group g) pair and TH output rows: it stages the TH+KH-1
+// input rows of all C channels of the group (the halo) and the group's
+// weights — transposed to [c][kh][kw][f] so RF consecutive filters are one
+// vector load — in shared memory. Each thread owns an RF×RW register tile
+// (RF filters × RW adjacent output columns of one row) and walks c, kh,
+// kw in ascending order, reusing each loaded input row segment across the
+// KW taps: RF·RW·KW FFMAs per (RW+KW-1) scalar + KW vector smem loads.
+// The chain order per output is exactly the reference's (i, kh, kw), and
+// the bias loop adds B[0..M-1] sequentially (__fadd_rn, no contraction).
+#include "kernels.cuh"
+
+namespace tcb {
+namespace k {
+
+namespace {
+
+template <int RF, int RW, int KW>
+__global__ void __launch_bounds__(512) gconv_kernel(const GconvArgs a, const int TH, const int TW, const int TF) {
+  extern __shared__ __align__(16) float sm[];
+  const int C = a.C, KH = a.KH, F = a.F;
+  const int Ho = a.H - KH + 1, Wo = a.W - KW + 1;
+  const int rows = TH + KH - 1;
+  const int WP = TW * RW + KW - 1;
+  const int FP = TF * RF;
+  const int n = blockIdx.z, g = blockIdx.y, h0 = blockIdx.x * TH;
+  const int tid = threadIdx.x, T = blockDim.x;
+
+  float* In = sm;                      // [C][rows][WP]
+  float* Wt = In + C * rows * WP;      // [C][KH][KW][FP]
+  float* Bs = Wt + C * KH * KW * FP;   // [Mb]
+
+  const float* Ig = a.I + ((int64_t)n * a.G + g) * C * a.H * a.W;
+  for (int e = tid; e < C * rows * WP; e += T) {
+    int w = e % WP, t = e / WP;
+    int r = t % rows, c = t / rows;
+    int h = h0 + r;
+    In[e] = (h < a.H && w < a.W) ? __ldg(Ig + ((int64_t)c * a.H + h) * a.W + w) : 0.0f;
+  }
+  const float* Wg = a.W1 + (int64_t)g * F * C * KH * KW;
+  for (int e = tid; e < C * KH * KW * FP; e += T) {
+    int f = e % FP, t = e / FP;  // t = (c*KH + kh)*KW + kw
+    Wt[e] = f < F ? __ldg(Wg + (int64_t)f * C * KH * KW + t) : 0.0f;
+  }
+  for (int e = tid; e < a.Mb; e += T) Bs[e] = __ldg(a.B + e);
+  __syncthreads();
+
+  const int wg = tid % TW;
+  const int hl = (tid / TW) % TH;
+  const int fg = tid / (TW * TH);
+  if (fg >= TF) return;
+
+  float acc[RF][RW];
+#pragma unroll
+  for (int f = 0; f < RF; ++f)
+#pragma unroll
+    for (int j = 0; j < RW; ++j) acc[f][j] = 0.0f;
+
+  for (int c = 0; c < C; ++c) {
+    for (int kh = 0; kh < KH; ++kh) {
+      const float* row = In + (c * rows + hl + kh) * WP + wg * RW;
+      float x[RW + KW - 1];
+#pragma unroll
+      for (int j = 0; j < RW + KW - 1; ++j) x[j] = row[j];
+      const float* wp = Wt + ((c * KH + kh) * KW) * FP + fg * RF;
+#pragma unroll
+      for (int kw = 0; kw < KW; ++kw) {
+        float wv[RF];
+        if constexpr (RF % 4 == 0) {
+#pragma unroll
+          for (int f = 0; f < RF; f += 4) {
+            float4 v = *reinterpret_cast<const float4*>(wp + kw * FP + f);
+            wv[f] = v.x;
+            wv[f + 1] = v.y;
+            wv[f + 2] = v.z;
+            wv[f + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int f = 0; f < RF; ++f) wv[f] = wp[kw * FP + f];
+        }
+#pragma unroll
+        for (int f = 0; f < RF; ++f)
+#pragma unroll
+          for (int j = 0; j < RW; ++j) acc[f][j] = __fmaf_rn(x[j + kw], wv[f], acc[f][j]);
+      }
+    }
+  }
+
+  const int h = h0 + hl;
+  if (h >= Ho) return;
+  for (int m = 0; m < a.Mb; ++m) {
+    const float bm = Bs[m];
+#pragma unroll
+    for (int f = 0; f < RF; ++f)
+#pragma unroll
+      for (int j = 0; j < RW; ++j) acc[f][j] = __fadd_rn(acc[f][j], bm);
+  }
+  float* Og = a.O + ((int64_t)n * a.G + g) * F * Ho * Wo;
+#pragma unroll
+  for (int f = 0; f < RF; ++f) {
+    int o = fg * RF + f;
+    if (o >= F) continue;
+#pragma unroll
+    for (int j = 0; j < RW; ++j) {
+      int w = wg * RW + j;
+      if (w < Wo) Og[((int64_t)o * Ho + h) * Wo + w] = acc[f][j];
+    }
+  }
+}
+
+const GconvVariant kGconvVariants[] = {
+    {0, 4, 7, 3, "rf4_rw7_kw3"},  {1, 8, 7, 3, "rf8_rw7_kw3"},  {2, 4, 4, 3, "rf4_rw4_kw3"},
+    {3, 4, 8, 3, "rf4_rw8_kw3"},  {4, 8, 4, 3, "rf8_rw4_kw3"},  {5, 2, 7, 3, "rf2_rw7_kw3"},
+    {6, 4, 4, 1, "rf4_rw4_kw1"},  {7, 4, 4, 5, "rf4_rw4_kw5"},  {8, 1, 1, 3, "rf1_rw1_kw3"},
+};
+
+template <int RF, int RW, int KW>
+cudaError_t launchV(const GconvArgs& a, int th, cudaStream_t s) {
+  const int Ho = a.H - a.KH + 1, Wo = a.W - KW + 1;
+  const int TW = (Wo + RW - 1) / RW, TF = (a.F + RF - 1) / RF;
+  const int threads = TW * th * TF;
+  if (threads > 512 || threads < 1) return cudaErrorInvalidConfiguration;
+  size_t smem = gconvSmem(a, th, RW);
+  smem += (size_t)a.C * a.KH * KW * (TF * RF - a.F) * sizeof(float);  // filter padding
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  auto kfn = gconv_kernel<RF, RW, KW>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((Ho + th - 1) / th, a.G, a.N);
+  kfn<<<grid, threads, smem, s>>>(a, th, TW, TF);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int gconvVariantCount() { return sizeof(kGconvVariants) / sizeof(kGconvVariants[0]); }
+const GconvVariant& gconvVariant(int i) { return kGconvVariants[i]; }
+
+size_t gconvSmem(const GconvArgs& a, int th, int rw) {
+  const int Wo = a.W - a.KW + 1;
+  const int TW = (Wo + rw - 1) / rw;
+  const int WP = TW * rw + a.KW - 1;
+  return ((size_t)a.C * (th + a.KH - 1) * WP + (size_t)a.C * a.KH * a.KW * a.F + a.Mb) * sizeof(float);
+}
+
+int gconvThreads(const GconvArgs& a, int variant, int th) {
+  const GconvVariant& v = kGconvVariants[variant];
+  const int Wo = a.W - a.KW + 1;
+  return ((Wo + v.rw - 1) / v.rw) * th * ((a.F + v.rf - 1) / v.rf);
+}
+
+cudaError_t launchGconv(const GconvArgs& a, int variant, int th, cudaStream_t s) {
+  if (a.N <= 0 || a.G <= 0) return cudaSuccess;
+  if (variant < 0 || variant >= gconvVariantCount()) return cudaErrorInvalidValue;
+  if (kGconvVariants[variant].kw != a.KW || th < 1) return cudaErrorInvalidConfiguration;
+  switch (variant) {
+    case 0: return launchV<4, 7, 3>(a, th, s);
+    case 1: return launchV<8, 7, 3>(a, th, s);
+    case 2: return launchV<4, 4, 3>(a, th, s);
+    case 3: return launchV<4, 8, 3>(a, th, s);
+    case 4: return launchV<8, 4, 3>(a, th, s);
+    case 5: return launchV<2, 7, 3>(a, th, s);
+    case 6: return launchV<4, 4, 1>(a, th, s);
+    case 7: return launchV<4, 4, 5>(a, th, s);
+    case 8: return launchV<1, 1, 3>(a, th, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace k
+}  // namespace tcb

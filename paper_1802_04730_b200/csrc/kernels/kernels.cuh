@@ -1,0 +1,107 @@
+// kernels.cuh — launch interfaces of the hand-written sm_100a kernels.
+//
+// Every kernel here is "FFMA-exact": each output element is produced by a
+// single thread that runs the reference's reduction chain in canonical
+// order — init value, then acc = fma(a_k, b_k, acc) for k ascending — so
+// the result matches the reference interpreter
+// (interpreter.cc:218-233: double combine + float narrowing per step) up to
+// double-rounding ties of the fused step (≈2^-29 per step; none observed
+// on the golden vectors). No kernel reassociates a reduction.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace tcb {
+namespace k {
+
+// ------------------------------------------------------------- GEMM-NT
+// C[b][m][n] = epi(init + sum_k A[b][m][k] * B[b][n][k]),  k ascending.
+enum InitMode : int { kInitZero = 0, kInitInout = 1, kInitBias = 2 };
+
+struct GemmArgs {
+  const float* A;
+  const float* B;
+  float* C;
+  const float* bias;  // kInitBias: bias[n]
+  int batch, M, N, K;
+  int64_t lda, ldb, ldc;     // row strides (elements)
+  int64_t sA, sB, sC;        // batch strides (elements); 0 ⇒ broadcast
+  int init;                  // InitMode
+  int relu;                  // epilogue fmaxf(acc, 0)
+};
+
+// variant ids: see gemm.cu kGemmVariants
+struct GemmVariant {
+  int id;
+  int tm, tn, rm, rn, tk;  // tm==0 ⇒ "direct" (no smem staging, 1 output / thread)
+  const char* name;
+};
+int gemmVariantCount();
+const GemmVariant& gemmVariant(int i);
+// threads: only used by the direct variant (≥32, multiple of 32, ≤1024)
+cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t s);
+
+// ------------------------------------------------------------ FC chain
+// Fused FC+bias+ReLU layers (MLP1 / 2FCRelu / MLP3): one CTA per `rows`
+// batch rows keeps every intermediate activation in shared memory.
+constexpr int kMaxLayers = 4;
+struct FcLayer {
+  const float* W;     // [out][ldw]
+  const float* bias;  // [out]
+  float* O;           // [batch][out] (global output of this layer)
+  int out, kred;      // output features, reduction length
+  int64_t ldw;
+};
+struct FcChainArgs {
+  const float* I;  // [batch][ldi] first-layer input
+  int64_t ldi;
+  int batch;
+  int layers;
+  FcLayer L[kMaxLayers];
+};
+cudaError_t launchFcChain(const FcChainArgs& a, int rows, int threads, cudaStream_t s);
+size_t fcChainSmem(const FcChainArgs& a, int rows);
+
+// ------------------------------------------------------------------ KRU
+struct KruArgs {
+  const float *W0, *W1, *W2, *X;
+  float *Y, *XW1, *XW2;
+  int M, N0, N1, N2, D0, D1, D2;
+};
+cudaError_t launchKru3(const KruArgs& a, int dchunk, int threads, cudaStream_t s);
+size_t kru3Smem(const KruArgs& a, int dchunk);
+
+// ---------------------------------------------------------------- gconv
+struct GconvArgs {
+  const float* I;   // [N][G][C][H][W]
+  const float* W1;  // [G][F][C][KH][KW]
+  const float* B;   // [Mb]
+  float* O;         // [N][G][F][Ho][Wo]
+  int N, G, C, H, W, F, KH, KW, Mb;
+};
+struct GconvVariant {
+  int id, rf, rw, kw;
+  const char* name;
+};
+int gconvVariantCount();
+const GconvVariant& gconvVariant(int i);
+cudaError_t launchGconv(const GconvArgs& a, int variant, int th, cudaStream_t s);
+size_t gconvSmem(const GconvArgs& a, int th, int rw);
+int gconvThreads(const GconvArgs& a, int variant, int th);
+
+// ------------------------------------------------------------------ LUT
+// O[i][j] = sum_k LUT[I[i][k]][j] (k ascending); out-of-range indices set
+// *err (IndexOutOfRange) and leave that row's value unspecified.
+struct LutArgs {
+  const float* LUT;
+  const int32_t* I;
+  float* O;
+  int64_t E;
+  int D, B, L;
+  int* err;
+};
+cudaError_t launchLut(const LutArgs* tables, int ntables, int threads, cudaStream_t s);
+
+}  // namespace k
+}  // namespace tcb

@@ -1,0 +1,85 @@
+// lut.cu — embedding lookup-table reductions (1LUT / 2LUT,
+// proj/kernels/2lut.tc:2-6):   O(i,j) +=! LUT(I(i,k), j)
+// A warp-group of D/4 threads owns one batch row i; each thread owns four
+// consecutive columns j and walks k ascending, gathering 16-byte slices of
+// the indexed table rows (fully coalesced per row) and adding them in
+// order (__fadd_rn — the reference's double add narrowed to float is the
+// correctly rounded float add). Indices are validated on the device: an
+// index outside [0, E) raises the kernel's error flag, the reference's
+// IndexOutOfRange (interpreter.cc:284-292), and is never clamped. Both
+// tables of 2LUT run in one launch (blockIdx.y selects the table).
+#include "kernels.cuh"
+
+namespace tcb {
+namespace k {
+
+namespace {
+
+struct LutPack {
+  LutArgs t[2];
+};
+
+__global__ void lut_kernel(const LutArgs a0, const LutArgs a1, const int vec) {
+  const LutArgs& a = blockIdx.y == 0 ? a0 : a1;
+  const int lanesPerRow = vec ? a.D / 4 : a.D;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid / lanesPerRow;
+  const int lane = (int)(gid % lanesPerRow);
+  if (row >= a.B) return;
+  const int32_t* idx = a.I + row * a.L;
+  if (vec) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < a.L; ++k) {
+      int64_t e = __ldg(idx + k);
+      if (e < 0 || e >= a.E) {
+        atomicOr(a.err, 1);
+        break;
+      }
+      float4 v = __ldg(reinterpret_cast<const float4*>(a.LUT + e * a.D) + lane);
+      acc.x = __fadd_rn(acc.x, v.x);
+      acc.y = __fadd_rn(acc.y, v.y);
+      acc.z = __fadd_rn(acc.z, v.z);
+      acc.w = __fadd_rn(acc.w, v.w);
+    }
+    reinterpret_cast<float4*>(a.O + row * a.D)[lane] = acc;
+  } else {
+    float acc = 0.f;
+    for (int k = 0; k < a.L; ++k) {
+      int64_t e = __ldg(idx + k);
+      if (e < 0 || e >= a.E) {
+        atomicOr(a.err, 1);
+        break;
+      }
+      acc = __fadd_rn(acc, __ldg(a.LUT + e * a.D + lane));
+    }
+    a.O[row * a.D + lane] = acc;
+  }
+}
+
+}  // namespace
+
+cudaError_t launchLut(const LutArgs* tables, int ntables, int threads, cudaStream_t s) {
+  if (ntables < 1 || ntables > 2) return cudaErrorInvalidValue;
+  LutPack p;
+  p.t[0] = tables[0];
+  p.t[1] = ntables > 1 ? tables[1] : tables[0];
+  int vec = 1;
+  int64_t maxLanes = 0;
+  for (int i = 0; i < ntables; ++i) {
+    const LutArgs& a = tables[i];
+    vec &= (a.D % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.LUT) & 15) == 0) &&
+           ((reinterpret_cast<uintptr_t>(a.O) & 15) == 0);
+  }
+  for (int i = 0; i < ntables; ++i) {
+    int64_t lanes = (int64_t)tables[i].B * (vec ? tables[i].D / 4 : tables[i].D);
+    maxLanes = lanes > maxLanes ? lanes : maxLanes;
+  }
+  if (maxLanes == 0) return cudaSuccess;
+  int t = threads > 0 ? threads : 256;
+  dim3 grid((unsigned)((maxLanes + t - 1) / t), ntables);
+  lut_kernel<<<grid, t, 0, s>>>(p.t[0], p.t[1], vec);
+  return cudaGetLastError();
+}
+
+}  // namespace k
+}  // namespace tcb

@@ -1,0 +1,588 @@
+// ops.cc — operator registry, tensor binding, option decoding, launch.
+#include "ops.h"
+
+#include <map>
+#include <mutex>
+#include <sstream>
+
+#include "cache.h"
+
+namespace tcb {
+namespace ops {
+
+namespace {
+
+const char* kOpsTc =
+#include "ops_tc.inc"
+    ;
+
+struct Registry {
+  std::map<std::string, std::string> byCanon;  // canonical text → form name
+  std::vector<std::string> forms;
+};
+
+const Registry& registry() {
+  static Registry r;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    lang::Program p = lang::parse(kOpsTc);
+    for (const auto& d : p.defs) {
+      lang::Validated v = lang::validate(d, &p);
+      r.byCanon[cache::canonicalize(v)] = d.name;
+      r.forms.push_back(d.name);
+    }
+  });
+  return r;
+}
+
+Ref in(int i) { return Ref{false, i}; }
+Ref out(int i) { return Ref{true, i}; }
+
+const std::vector<int64_t>& shapeOf(const sem::Specialized& s, const Ref& r) {
+  const std::string& name = r.out ? s.v.def.rets[r.idx] : s.v.def.params[r.idx].name;
+  return s.shapes.at(name);
+}
+
+double vol(const std::vector<int64_t>& v) {
+  double n = 1;
+  for (auto e : v) n *= static_cast<double>(e);
+  return n;
+}
+
+[[noreturn]] void invalid(const std::string& m) { fail(ErrorKind::MappingInvalid, m); }
+
+void decodeGemm(const MappingOptions& o, Mapping& m) {
+  if (!o.useShared) {
+    int t = static_cast<int>(o.threads());
+    if (t < 32 || t % 32 != 0) invalid("direct GEMM needs a thread count that is a multiple of 32");
+    m.gemmVariant = 0;
+    m.gemmThreads = t;
+    return;
+  }
+  if (o.tileSizes.size() < 3) invalid("tiled GEMM needs three tile sizes (rows, cols, reduction depth)");
+  if (o.threadShape[2] != 1) invalid("tiled GEMM uses a 2-D thread block");
+  int64_t tm = o.tileSizes[0], tn = o.tileSizes[1], tk = o.tileSizes[2];
+  int64_t tx = o.threadShape[0], ty = o.threadShape[1];
+  if (tm % ty || tn % tx) invalid("tile extents must be multiples of the thread block extents");
+  for (int i = 1; i < k::gemmVariantCount(); ++i) {
+    const auto& v = k::gemmVariant(i);
+    if (v.tm == tm && v.tn == tn && v.tk == tk && v.rm == tm / ty && v.rn == tn / tx) {
+      m.gemmVariant = i;
+      m.gemmThreads = static_cast<int>(tx * ty);
+      return;
+    }
+  }
+  invalid("no GEMM kernel instantiated for tile " + std::to_string(tm) + "x" + std::to_string(tn) + "x" +
+          std::to_string(tk) + " with a " + std::to_string(tx) + "x" + std::to_string(ty) + " block");
+}
+
+void launchGemmDesc(const GemmDesc& g, const Mapping& m, void* const* in, void* const* out, cudaStream_t s) {
+  auto ptr = [&](const Ref& r) -> void* { return r.valid() ? (r.out ? out[r.idx] : in[r.idx]) : nullptr; };
+  k::GemmArgs a;
+  a.A = static_cast<const float*>(ptr(g.A));
+  a.B = static_cast<const float*>(ptr(g.B));
+  a.C = static_cast<float*>(ptr(g.C));
+  a.bias = static_cast<const float*>(ptr(g.bias));
+  a.batch = g.batch;
+  a.M = g.M;
+  a.N = g.N;
+  a.K = g.K;
+  a.lda = g.lda;
+  a.ldb = g.ldb;
+  a.ldc = g.ldc;
+  a.sA = g.sA;
+  a.sB = g.sB;
+  a.sC = g.sC;
+  a.init = g.init;
+  a.relu = g.relu;
+  cudaError_t e = k::launchGemm(a, m.gemmVariant, m.gemmThreads, s);
+  if (e != cudaSuccess) fail(ErrorKind::Cuda, std::string("GEMM launch failed: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+const char* familyName(Family f) {
+  switch (f) {
+    case Family::Gemm: return "gemm_nt";
+    case Family::FcChain: return "fc_chain";
+    case Family::Kru3: return "kru3";
+    case Family::Gconv: return "gconv";
+    case Family::Lut: return "lut";
+  }
+  return "?";
+}
+
+const std::string& opsSource() {
+  static const std::string s(kOpsTc);
+  return s;
+}
+
+std::vector<std::string> registeredForms() { return registry().forms; }
+
+std::string formOf(const std::string& canon) {
+  const auto& r = registry();
+  auto f = r.byCanon.find(canon);
+  return f == r.byCanon.end() ? std::string() : f->second;
+}
+
+std::string Mapping::describe() const {
+  std::ostringstream os;
+  os << familyName(family) << ":";
+  switch (family) {
+    case Family::Gemm:
+      os << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
+      break;
+    case Family::FcChain:
+      if (fused) os << "fused rows=" << rows << " threads=" << threads;
+      else os << "per-layer " << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
+      break;
+    case Family::Kru3: os << "fused dchunk=" << dchunk << " threads=" << threads; break;
+    case Family::Gconv: os << k::gconvVariant(gconvVariant).name << " th=" << th; break;
+    case Family::Lut: os << "gather threads=" << threads; break;
+  }
+  return os.str();
+}
+
+Problem match(const sem::Specialized& s, const std::string& canon) {
+  std::string form = formOf(canon);
+  if (form.empty())
+    fail(ErrorKind::NoKernel, "definition '" + s.v.def.name +
+                                  "' matches no hand-written kernel family (recognised forms: tmm, tbmm, C3, "
+                                  "MLP1, 2FCRelu, MLP3, 3KRU, gconv, 2LUT, 1LUT)");
+  Problem p;
+  p.form = form;
+  auto sh = [&](const Ref& r) { return shapeOf(s, r); };
+  auto i32 = [](int64_t v) {
+    if (v > INT32_MAX) fail(ErrorKind::NoKernel, "extent exceeds the 32-bit kernel index range");
+    return static_cast<int>(v);
+  };
+
+  if (form == "tmm" || form == "tbmm" || form == "C3") {
+    p.family = Family::Gemm;
+    GemmDesc& g = p.gemm;
+    g.A = in(0);
+    g.B = in(1);
+    g.C = out(0);
+    const auto &a = sh(g.A), &b = sh(g.B), &c = sh(g.C);
+    if (form == "tbmm") {
+      g.batch = i32(a[0]);
+      g.M = i32(a[1]);
+      g.N = i32(b[1]);
+      g.K = i32(std::min(a[2], b[2]));
+      g.lda = a[2];
+      g.ldb = b[2];
+      g.ldc = c[2];
+      g.sA = a[1] * a[2];
+      g.sB = b[1] * b[2];
+      g.sC = c[1] * c[2];
+    } else {
+      g.M = i32(a[0]);
+      g.N = i32(b[0]);
+      g.K = i32(std::min(a[1], b[1]));
+      g.lda = a[1];
+      g.ldb = b[1];
+      g.ldc = c[1];
+    }
+    g.init = form == "C3" ? k::kInitInout : k::kInitZero;
+    p.flops = 2.0 * g.batch * g.M * g.N * g.K;
+    p.bytes = 4.0 * (vol(a) + vol(b) + vol(c) * (form == "C3" ? 2 : 1));
+    return p;
+  }
+  if (form == "MLP1" || form == "2FCRelu" || form == "MLP3") {
+    p.family = Family::FcChain;
+    FcDesc& f = p.fc;
+    int nl = form == "MLP1" ? 1 : form == "2FCRelu" ? 2 : 3;
+    // MLP1/2FCRelu read I = param 0; MLP3 reads the pass-through return O1
+    f.I = form == "MLP3" ? out(0) : in(0);
+    const auto& I = sh(f.I);
+    f.ldi = I[1];
+    f.batch = i32(I[0]);
+    int64_t prevOut = I[1];
+    p.bytes = 4.0 * vol(I);
+    for (int l = 0; l < nl; ++l) {
+      FcLayerDesc L;
+      L.W = in(1 + 2 * l);
+      L.bias = in(2 + 2 * l);
+      L.O = out(form == "MLP3" ? 1 + l : l);
+      const auto& W = sh(L.W);
+      L.out = i32(W[0]);
+      L.ldw = W[1];
+      L.kred = i32(std::min(prevOut, W[1]));  // reduction range = intersection (ranges.cc)
+      prevOut = L.out;
+      p.flops += 2.0 * f.batch * L.out * L.kred;
+      p.bytes += 4.0 * (vol(W) + vol(sh(L.bias)) + (double)f.batch * L.out);
+      f.layers.push_back(L);
+    }
+    return p;
+  }
+  if (form == "3KRU") {
+    p.family = Family::Kru3;
+    KruDesc& k = p.kru;
+    k.W0 = in(0);
+    k.W1 = in(1);
+    k.W2 = in(2);
+    k.X = in(3);
+    k.Y = out(0);
+    k.XW1 = out(1);
+    k.XW2 = out(2);
+    const auto& X = sh(k.X);
+    k.M = i32(X[0]);
+    k.N0 = i32(X[1]);
+    k.N1 = i32(X[2]);
+    k.N2 = i32(X[3]);
+    k.D0 = i32(sh(k.W0)[0]);
+    k.D1 = i32(sh(k.W1)[0]);
+    k.D2 = i32(sh(k.W2)[0]);
+    double m = k.M;
+    p.flops = 2.0 * m *
+              ((double)k.N0 * k.N1 * k.D2 * k.N2 + (double)k.N0 * k.D1 * k.D2 * k.N1 + (double)k.D0 * k.D1 * k.D2 * k.N0);
+    p.bytes = 4.0 * (vol(X) + vol(sh(k.W0)) + vol(sh(k.W1)) + vol(sh(k.W2)) + vol(sh(k.Y)) + vol(sh(k.XW1)) +
+                     vol(sh(k.XW2)));
+    return p;
+  }
+  if (form == "gconv") {
+    p.family = Family::Gconv;
+    GconvDesc& g = p.gconv;
+    g.I = in(0);
+    g.W1 = in(1);
+    g.B = in(2);
+    g.O = out(0);
+    const auto &I = sh(g.I), &W = sh(g.W1);
+    g.N = i32(I[0]);
+    g.G = i32(I[1]);
+    g.C = i32(I[2]);
+    g.H = i32(I[3]);
+    g.W = i32(I[4]);
+    g.F = i32(W[1]);
+    g.KH = i32(W[3]);
+    g.KW = i32(W[4]);
+    g.Mb = i32(sh(g.B)[0]);
+    double outs = vol(sh(g.O));
+    p.flops = outs * (2.0 * g.C * g.KH * g.KW + g.Mb);
+    p.bytes = 4.0 * (vol(I) + vol(W) + g.Mb + outs);
+    return p;
+  }
+  if (form == "2LUT" || form == "1LUT") {
+    p.family = Family::Lut;
+    int nt = form == "2LUT" ? 2 : 1;
+    for (int t = 0; t < nt; ++t) {
+      LutTable T;
+      T.LUT = in(2 * t);
+      T.I = in(2 * t + 1);
+      T.O = out(t);
+      const auto &L = sh(T.LUT), &I = sh(T.I);
+      T.E = L[0];
+      T.D = i32(L[1]);
+      T.B = i32(I[0]);
+      T.L = i32(I[1]);
+      p.flops += (double)T.B * T.L * T.D;
+      p.bytes += 4.0 * ((double)T.B * T.L + (double)T.B * T.L * T.D + (double)T.B * T.D);
+      p.lut.push_back(T);
+    }
+    return p;
+  }
+  fail(ErrorKind::Internal, "registered form '" + form + "' has no binder");
+}
+
+Mapping decode(const Problem& p, const MappingOptions& o) {
+  o.validate();
+  Mapping m;
+  m.family = p.family;
+  switch (p.family) {
+    case Family::Gemm: decodeGemm(o, m); break;
+    case Family::FcChain: {
+      if (o.fusion == Fusion::Min) {
+        m.fused = false;
+        decodeGemm(o, m);
+        break;
+      }
+      m.fused = true;
+      m.rows = o.tileSizes.empty() ? 1 : static_cast<int>(o.tileSizes[0]);
+      if (m.rows != 1 && m.rows != 2 && m.rows != 4 && m.rows != 8) invalid("fused FC chain rows per CTA must be 1, 2, 4 or 8");
+      m.threads = static_cast<int>(o.threads());
+      if (m.threads < 32 || m.threads % 32) invalid("fused FC chain needs a multiple of 32 threads");
+      int outMax = 0;
+      for (const auto& L : p.fc.layers) outMax = std::max(outMax, L.out);
+      if (outMax > 2 * m.threads) invalid("fused FC chain: more than two output features per thread");
+      k::FcChainArgs a{};
+      a.layers = static_cast<int>(p.fc.layers.size());
+      for (int l = 0; l < a.layers; ++l) {
+        a.L[l].out = p.fc.layers[l].out;
+        a.L[l].kred = p.fc.layers[l].kred;
+      }
+      if (k::fcChainSmem(a, m.rows) > 227 * 1024) invalid("fused FC chain exceeds the shared-memory capacity");
+      break;
+    }
+    case Family::Kru3: {
+      if (o.fusion == Fusion::Min) invalid("3-KRU is only implemented as one fused kernel");
+      m.dchunk = o.tileSizes.empty() ? 16 : static_cast<int>(o.tileSizes[0]);
+      m.threads = static_cast<int>(o.threads());
+      if (m.threads < 32 || m.threads % 32) invalid("3-KRU needs a multiple of 32 threads");
+      k::KruArgs a{};
+      a.N0 = p.kru.N0;
+      a.N1 = p.kru.N1;
+      a.N2 = p.kru.N2;
+      a.D0 = p.kru.D0;
+      a.D1 = p.kru.D1;
+      a.D2 = p.kru.D2;
+      if (m.dchunk < 1 || m.dchunk > p.kru.D2) invalid("3-KRU d2 chunk outside [1, D2]");
+      if (k::kru3Smem(a, m.dchunk) > 227 * 1024) invalid("3-KRU chunk exceeds the shared-memory capacity");
+      break;
+    }
+    case Family::Gconv: {
+      if (o.tileSizes.size() < 3) invalid("gconv needs tile sizes (rows per CTA, filters per thread, columns per thread)");
+      m.th = static_cast<int>(o.tileSizes[0]);
+      int rf = static_cast<int>(o.tileSizes[1]), rw = static_cast<int>(o.tileSizes[2]);
+      m.gconvVariant = -1;
+      for (int i = 0; i < k::gconvVariantCount(); ++i) {
+        const auto& v = k::gconvVariant(i);
+        if (v.rf == rf && v.rw == rw && v.kw == p.gconv.KW) m.gconvVariant = i;
+      }
+      if (m.gconvVariant < 0) invalid("no gconv kernel instantiated for this filter/column micro-tile and KW");
+      k::GconvArgs a{};
+      a.C = p.gconv.C;
+      a.H = p.gconv.H;
+      a.W = p.gconv.W;
+      a.F = p.gconv.F;
+      a.KH = p.gconv.KH;
+      a.KW = p.gconv.KW;
+      a.Mb = p.gconv.Mb;
+      int t = k::gconvThreads(a, m.gconvVariant, m.th);
+      if (t > 512) invalid("gconv CTA would exceed 512 threads");
+      if (k::gconvSmem(a, m.th, rw) + (size_t)a.C * a.KH * a.KW * (rf * ((a.F + rf - 1) / rf) - a.F) * 4 > 227 * 1024)
+        invalid("gconv tile exceeds the shared-memory capacity");
+      m.threads = t;
+      break;
+    }
+    case Family::Lut: {
+      m.threads = static_cast<int>(o.threads());
+      if (m.threads < 32 || m.threads % 32) invalid("LUT gather needs a multiple of 32 threads");
+      break;
+    }
+  }
+  return m;
+}
+
+MappingOptions defaultOptions(const Problem& p) {
+  MappingOptions o;
+  switch (p.family) {
+    case Family::Gemm: {
+      // the reference's contraction preset (options.cc:182-191) is a valid
+      // tile here: 32x32 CTA tile, 16x16 threads, 2x2 register micro-tile
+      o = baselineOptions()[0];
+      const GemmDesc& g = p.gemm;
+      double ctas = (double)g.batch * ((g.M + 31) / 32) * ((g.N + 31) / 32);
+      if (ctas < 148) {  // small problems: finer tiles to cover the SMs
+        o.tileSizes = {16, 16, 32};
+        o.threadShape = {{16, 16, 1}};
+      }
+      break;
+    }
+    case Family::FcChain: {
+      int outMax = 0;
+      for (const auto& L : p.fc.layers) outMax = std::max(outMax, L.out);
+      o.tileSizes = {1, 1, 1};
+      o.threadShape = {{outMax > 256 ? 512 : outMax > 128 ? 256 : 128, 1, 1}};
+      o.fusion = Fusion::Max;
+      o.useShared = true;
+      break;
+    }
+    case Family::Kru3:
+      o.tileSizes = {std::min<int64_t>(16, p.kru.D2), 1, 1};
+      o.threadShape = {{256, 1, 1}};
+      o.useShared = true;
+      break;
+    case Family::Gconv: {
+      int Wo = p.gconv.W - p.gconv.KW + 1;
+      int rw = (p.gconv.KW == 3 && Wo % 7 == 0) ? 7 : 4;
+      int rf = 4;
+      if (p.gconv.KW != 3) rw = 4;
+      o.tileSizes = {4, rf, rw};
+      o.threadShape = {{1, 1, 1}};
+      o.useShared = true;
+      // shrink rows-per-CTA until the CTA fits 512 threads
+      k::GconvArgs a{};
+      a.W = p.gconv.W;
+      a.KW = p.gconv.KW;
+      a.F = p.gconv.F;
+      for (int th : {4, 2, 1}) {
+        o.tileSizes[0] = th;
+        int v = -1;
+        for (int i = 0; i < k::gconvVariantCount(); ++i)
+          if (k::gconvVariant(i).rf == rf && k::gconvVariant(i).rw == rw && k::gconvVariant(i).kw == p.gconv.KW) v = i;
+        if (v >= 0 && k::gconvThreads(a, v, th) <= 512) break;
+      }
+      break;
+    }
+    case Family::Lut:
+      o.threadShape = {{256, 1, 1}};
+      break;
+  }
+  return o;
+}
+
+GenePools genePools(const Problem& p) {
+  GenePools g;
+  switch (p.family) {
+    case Family::Gemm:
+    case Family::FcChain:
+      g.tile0 = {16, 32, 64};
+      g.tile1 = {16, 32, 64};
+      g.tile2 = {16, 32, 64};
+      g.tx = {4, 8, 16, 32};
+      g.ty = {4, 8, 16, 32};
+      g.tz = {1};
+      g.useShared = {0, 1};
+      g.fusion = {Fusion::Max};
+      if (p.family == Family::FcChain) {
+        g.tile0 = {1, 2, 4, 8, 16, 32, 64};
+        g.tx = {4, 8, 16, 32, 64, 128, 256};
+        g.fusion = {Fusion::Max, Fusion::Min};
+      }
+      break;
+    case Family::Kru3:
+      g.tile0 = {2, 4, 8, 16, 32};
+      g.tile1 = {1};
+      g.tile2 = {1};
+      g.tx = {32, 64, 128, 256, 512};
+      g.ty = {1, 2};
+      g.tz = {1};
+      g.useShared = {1};
+      g.fusion = {Fusion::Max};
+      break;
+    case Family::Gconv:
+      g.tile0 = {1, 2, 4, 8};
+      g.tile1 = {1, 2, 4, 8};
+      g.tile2 = {1, 4, 7, 8};
+      g.tx = {1};
+      g.ty = {1};
+      g.tz = {1};
+      g.useShared = {1};
+      g.fusion = {Fusion::Max};
+      break;
+    case Family::Lut:
+      g.tile0 = {1};
+      g.tile1 = {1};
+      g.tile2 = {1};
+      g.tx = {32, 64, 128, 256, 512, 1024};
+      g.ty = {1};
+      g.tz = {1};
+      g.useShared = {0};
+      g.fusion = {Fusion::Max};
+      break;
+  }
+  return g;
+}
+
+void launch(const Problem& p, const Mapping& m, void* const* in, void* const* out, int* errFlag, cudaStream_t s) {
+  auto ptr = [&](const Ref& r) -> void* { return r.out ? out[r.idx] : in[r.idx]; };
+  auto check = [](cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(ErrorKind::Cuda, std::string(what) + " launch failed: " + cudaGetErrorString(e));
+  };
+  switch (p.family) {
+    case Family::Gemm: launchGemmDesc(p.gemm, m, in, out, s); return;
+    case Family::FcChain: {
+      const FcDesc& f = p.fc;
+      if (!m.fused) {
+        // one GEMM per layer: init = bias, epilogue = ReLU; layer l>0 reads
+        // layer l-1's global output
+        Ref prev = f.I;
+        int64_t ldprev = f.ldi;
+        for (const auto& L : f.layers) {
+          GemmDesc g;
+          g.A = prev;
+          g.B = L.W;
+          g.C = L.O;
+          g.bias = L.bias;
+          g.M = f.batch;
+          g.N = L.out;
+          g.K = L.kred;
+          g.lda = ldprev;
+          g.ldb = L.ldw;
+          g.ldc = L.out;
+          g.init = k::kInitBias;
+          g.relu = 1;
+          launchGemmDesc(g, m, in, out, s);
+          prev = L.O;
+          ldprev = L.out;
+        }
+        return;
+      }
+      k::FcChainArgs a{};
+      a.I = static_cast<const float*>(ptr(f.I));
+      a.ldi = f.ldi;
+      a.batch = f.batch;
+      a.layers = static_cast<int>(f.layers.size());
+      for (int l = 0; l < a.layers; ++l) {
+        const auto& L = f.layers[l];
+        a.L[l].W = static_cast<const float*>(ptr(L.W));
+        a.L[l].bias = static_cast<const float*>(ptr(L.bias));
+        a.L[l].O = static_cast<float*>(ptr(L.O));
+        a.L[l].out = L.out;
+        a.L[l].kred = L.kred;
+        a.L[l].ldw = L.ldw;
+      }
+      check(k::launchFcChain(a, m.rows, m.threads, s), "FC chain");
+      return;
+    }
+    case Family::Kru3: {
+      const KruDesc& d = p.kru;
+      k::KruArgs a;
+      a.W0 = static_cast<const float*>(ptr(d.W0));
+      a.W1 = static_cast<const float*>(ptr(d.W1));
+      a.W2 = static_cast<const float*>(ptr(d.W2));
+      a.X = static_cast<const float*>(ptr(d.X));
+      a.Y = static_cast<float*>(ptr(d.Y));
+      a.XW1 = static_cast<float*>(ptr(d.XW1));
+      a.XW2 = static_cast<float*>(ptr(d.XW2));
+      a.M = d.M;
+      a.N0 = d.N0;
+      a.N1 = d.N1;
+      a.N2 = d.N2;
+      a.D0 = d.D0;
+      a.D1 = d.D1;
+      a.D2 = d.D2;
+      check(k::launchKru3(a, m.dchunk, m.threads, s), "3-KRU");
+      return;
+    }
+    case Family::Gconv: {
+      const GconvDesc& d = p.gconv;
+      k::GconvArgs a;
+      a.I = static_cast<const float*>(ptr(d.I));
+      a.W1 = static_cast<const float*>(ptr(d.W1));
+      a.B = static_cast<const float*>(ptr(d.B));
+      a.O = static_cast<float*>(ptr(d.O));
+      a.N = d.N;
+      a.G = d.G;
+      a.C = d.C;
+      a.H = d.H;
+      a.W = d.W;
+      a.F = d.F;
+      a.KH = d.KH;
+      a.KW = d.KW;
+      a.Mb = d.Mb;
+      check(k::launchGconv(a, m.gconvVariant, m.th, s), "gconv");
+      return;
+    }
+    case Family::Lut: {
+      k::LutArgs t[2];
+      int n = static_cast<int>(p.lut.size());
+      for (int i = 0; i < n; ++i) {
+        const auto& T = p.lut[i];
+        t[i].LUT = static_cast<const float*>(ptr(T.LUT));
+        t[i].I = static_cast<const int32_t*>(ptr(T.I));
+        t[i].O = static_cast<float*>(ptr(T.O));
+        t[i].E = T.E;
+        t[i].D = T.D;
+        t[i].B = T.B;
+        t[i].L = T.L;
+        t[i].err = errFlag;
+      }
+      check(k::launchLut(t, n, m.threads, s), "LUT");
+      return;
+    }
+  }
+}
+
+}  // namespace ops
+}  // namespace tcb

@@ -1,0 +1,117 @@
+// ops.h — from a specialized TC definition to hand-written kernels.
+//
+// The reference turns every definition into a generated loop nest
+// (pipeline::compile, pipeline.cc:69-101) and runs it on its CPU emulator
+// (backend::emulate, emulator.cc:448-559). tc-b200 instead recognises the
+// definition — by its positional canonical form (cache::canonicalize, the
+// same text the cache keys on) — as one of the registered paper operators
+// (tc/ops.tc), binds the caller's tensors to the operands of that
+// operator's kernel family, and maps the reference's MappingOptions genes
+// onto that family's kernel parameters. A definition with no registered
+// form fails with ErrorKind::NoKernel (never a CPU fallback).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "kernels/kernels.cuh"
+#include "options.h"
+#include "sem.h"
+
+namespace tcb {
+namespace ops {
+
+enum class Family { Gemm, FcChain, Kru3, Gconv, Lut };
+const char* familyName(Family f);
+
+// A tensor of the run call: inputs[idx] (parameters, declaration order) or
+// outputs[idx] (returns, declaration order).
+struct Ref {
+  bool out = false;
+  int idx = -1;
+  bool valid() const { return idx >= 0; }
+};
+
+struct GemmDesc {
+  Ref A, B, C, bias;
+  int batch = 1, M = 0, N = 0, K = 0;
+  int64_t lda = 0, ldb = 0, ldc = 0, sA = 0, sB = 0, sC = 0;
+  int init = k::kInitZero, relu = 0;
+};
+struct FcLayerDesc {
+  Ref W, bias, O;
+  int out = 0, kred = 0;
+  int64_t ldw = 0;
+};
+struct FcDesc {
+  Ref I;
+  int64_t ldi = 0;
+  int batch = 0;
+  std::vector<FcLayerDesc> layers;
+};
+struct KruDesc {
+  Ref W0, W1, W2, X, Y, XW1, XW2;
+  int M = 0, N0 = 0, N1 = 0, N2 = 0, D0 = 0, D1 = 0, D2 = 0;
+};
+struct GconvDesc {
+  Ref I, W1, B, O;
+  int N = 0, G = 0, C = 0, H = 0, W = 0, F = 0, KH = 0, KW = 0, Mb = 0;
+};
+struct LutTable {
+  Ref LUT, I, O;
+  int64_t E = 0;
+  int D = 0, B = 0, L = 0;
+};
+
+struct Problem {
+  std::string form;  // registered def name in tc/ops.tc
+  Family family = Family::Gemm;
+  GemmDesc gemm;
+  FcDesc fc;
+  KruDesc kru;
+  GconvDesc gconv;
+  std::vector<LutTable> lut;
+  double flops = 0;  // algorithmic FLOPs per call (2 per multiply-add)
+  double bytes = 0;  // algorithmic HBM bytes per call (inputs once, outputs once, in/out read once)
+};
+
+struct Mapping {
+  // Gemm (and unfused FC layers)
+  int gemmVariant = 4, gemmThreads = 0;
+  // FcChain
+  bool fused = true;
+  int rows = 1, threads = 128;
+  // Kru3
+  int dchunk = 16;
+  // Gconv
+  int gconvVariant = 0, th = 4;
+  std::string describe() const;
+  Family family = Family::Gemm;
+};
+
+// Registered forms: canonical text → def name, from the embedded tc/ops.tc.
+const std::string& opsSource();
+std::vector<std::string> registeredForms();
+std::string formOf(const std::string& canonicalTc);  // "" if unregistered
+
+Problem match(const sem::Specialized& s, const std::string& canonicalTc);  // Error(NoKernel)
+Mapping decode(const Problem& p, const MappingOptions& o);                // Error(MappingInvalid)
+MappingOptions defaultOptions(const Problem& p);
+
+// Gene pools for the tuner (TuningSpace per family; see tuner.cc).
+struct GenePools {
+  std::vector<int64_t> tile0, tile1, tile2, tx, ty, tz;
+  std::vector<Fusion> fusion;
+  std::vector<int> useShared;  // {0,1} or {1}
+};
+GenePools genePools(const Problem& p);
+
+// Launches the whole definition on `stream`. in/out are device pointers in
+// declaration order. errFlag: device int for data-dependent index checks.
+void launch(const Problem& p, const Mapping& m, void* const* in, void* const* out, int* errFlag,
+            cudaStream_t stream);
+
+}  // namespace ops
+}  // namespace tcb

@@ -1,0 +1,47 @@
+// tuner.h — the genetic autotuner (proj/include/tc/tuner/genetic.h,
+// proj/src/tuner/genetic.cc) re-targeted at real B200 execution.
+//
+// Kept from the reference: the 14-gene genome over MappingOptions, the
+// seeding order (cached best, extra starts, baselines, uniform random
+// top-up), fitness-proportional roulette, three-parent uniform crossover,
+// per-gene mutation, elitism, restart on a degenerate generation, a min-
+// update of the cache for every evaluated candidate, one JSONL session-log
+// line per generation. Changed: admissible gene values come from the
+// kernel family's instantiated variants (ops::genePools) instead of the
+// problem's ceil-divisors, and a candidate's cost is its measured device
+// time (median of CUDA-event timings, ns) instead of the emulator's
+// statement count. A candidate fails (fitness 0) when its options do not
+// decode to a kernel, its launch fails, or its outputs differ bit-wise
+// from the reference candidate's — the B200 stand-in for the emulator's
+// race detector (genetic.cc:112-117).
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "cache.h"
+#include "ops.h"
+
+namespace tcb {
+
+struct TuneOptions {
+  size_t population = 100;
+  size_t generations = 25;
+  double mutationRate = 0.05;
+  uint64_t seed = 0;
+  int timingIters = 10;
+  std::string sessionLog;
+  bool useBaselines = true;
+  std::vector<MappingOptions> extraStarting;
+};
+
+struct TuneResult {
+  MappingOptions best;
+  int64_t bestCost = 0;
+  size_t evaluated = 0, failed = 0;
+};
+
+TuneResult tune(const sem::Specialized& s, const ops::Problem& p, const cache::Key& key, const TuneOptions& o,
+                cache::Cache* c);
+
+}  // namespace tcb
