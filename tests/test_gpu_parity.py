@@ -1,0 +1,265 @@
+"""GPU parity: the CUDA path, called through the C ABI, against the
+reference's own outputs (golden FNV hashes / vectors) and the pinned C
+restatement. Bar: bit-exact (the FFMA-exact kernels run the reference's
+reduction chain in order); every comparison also reports maxRelError
+(tensor_data.cc:221-234) so a double-rounding tie would show as <= 1e-5."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from cases import PARAM_ORDER, RETURN_ORDER, case_inputs, oracle_outputs
+from conftest import fnv_hex, max_rel
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+_G = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+CASES = sorted(_G["cases"])
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    torch.cuda.init()
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_on_gpu(engine, d, ins, seeded, options=None, host=False):
+    params = [ins[n] for n in PARAM_ORDER[d]]
+    given = [seeded[r].shape if r in seeded else None for r in RETURN_ORDER[d]]
+    shapes = engine.infer_output_tensor_info(d, params, given)
+    outs_np = [np.array(seeded[r], copy=True) if r in seeded else np.zeros(s, np.float32)
+               for r, s in zip(RETURN_ORDER[d], shapes)]
+    if host:
+        p, o = params, outs_np
+    else:
+        p, o = [to_dev(x) for x in params], [to_dev(x) for x in outs_np]
+    h = engine.compile(d, p, o, options)
+    engine.run(h, p, o)
+    if not host:
+        torch.cuda.synchronize()
+        o = [t.cpu().numpy() for t in o]
+    return dict(zip(RETURN_ORDER[d], o)), h
+
+
+def assert_exact(oracle, name, k, got, ref_fnv, ref_arr=None):
+    if fnv_hex(oracle, got) == ref_fnv:
+        return
+    msg = f"{name}:{k} not bit-exact"
+    if ref_arr is not None:
+        diff = int(np.sum(got.view(np.uint32) != ref_arr.view(np.uint32)))
+        msg += f" ({diff}/{got.size} elements differ, maxRel={max_rel(ref_arr, got):.3g})"
+    raise AssertionError(msg)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_golden_bit_exact(engine, oracle, golden, name):
+    case, ins, seeded = case_inputs(oracle, golden, name)
+    got, _ = run_on_gpu(engine, case["def"], ins, seeded)
+    ref = oracle_outputs(oracle, case, ins, seeded)
+    for k, rec in case["outputs"].items():
+        assert list(got[k].shape) == rec["shape"]
+        assert max_rel(ref[k], got[k]) <= TOL
+        assert_exact(oracle, name, k, got[k], rec["fnv"], ref[k])
+
+
+@pytest.mark.parametrize("name", ["tmm_small", "tbmm_small", "c3_small", "mlp1_ragged"])
+def test_every_gemm_variant_identical(engine, oracle, golden, name):
+    """All instantiated GEMM kernels (and the direct one) give the same bits."""
+    from paper_1802_04730_b200 import TcError
+    case, ins, seeded = case_inputs(oracle, golden, name)
+    ref = oracle_outputs(oracle, case, ins, seeded)
+    base = json.loads(
+        '{"block_shape":[1,1,1],"fusion_strategy":"max","rng_seed":0,"shared_memory_budget":49152,'
+        '"thread_shape":[1,1,1],"tile_sizes":[32,32,32],"unroll_copy_shared":false,"unroll_factor":1,'
+        '"use_private":true,"use_shared":true}')
+    variants = [(16, 16, 1, 1, 32), (16, 32, 1, 2, 32), (32, 16, 2, 1, 32), (32, 32, 2, 2, 32),
+                (32, 64, 2, 4, 32), (64, 32, 4, 2, 32), (64, 64, 4, 4, 32), (32, 32, 4, 4, 32),
+                (16, 32, 2, 2, 32), (32, 32, 2, 2, 64), (64, 64, 4, 4, 16), (16, 64, 2, 4, 32),
+                (32, 32, 2, 4, 32), (16, 16, 2, 2, 32), (32, 64, 4, 4, 32)]
+    ran = 0
+    for v in variants + [None]:
+        o = dict(base)
+        if v is None:
+            o["use_shared"] = False
+            o["thread_shape"] = [96, 1, 1]
+        else:
+            tm, tn, rm, rn, tk = v
+            o["tile_sizes"] = [tm, tn, tk]
+            o["thread_shape"] = [tn // rn, tm // rm, 1]
+        if case["def"] == "MLP1":
+            o["fusion_strategy"] = "min"
+        got, _ = run_on_gpu(engine, case["def"], ins, seeded, options=o)
+        for k in case["outputs"]:
+            assert_exact(oracle, f"{name}/{o['tile_sizes']}", k, got[k], case["outputs"][k]["fnv"], ref[k])
+        ran += 1
+    assert ran == len(variants) + 1
+
+
+@pytest.mark.parametrize("rows,threads", [(1, 64), (2, 128), (4, 128), (8, 256)])
+def test_fc_chain_fused_variants(engine, oracle, golden, rows, threads):
+    for name in ["2fcrelu_small", "mlp3_small", "mlp3_paper"]:
+        case, ins, seeded = case_inputs(oracle, golden, name)
+        o = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0,
+             "shared_memory_budget": 49152, "thread_shape": [threads, 1, 1], "tile_sizes": [rows, 1, 1],
+             "unroll_copy_shared": False, "unroll_factor": 1, "use_private": False, "use_shared": True}
+        got, _ = run_on_gpu(engine, case["def"], ins, seeded, options=o)
+        for k, rec in case["outputs"].items():
+            assert_exact(oracle, name, k, got[k], rec["fnv"])
+
+
+@pytest.mark.parametrize("dchunk,threads", [(1, 64), (3, 128), (8, 256), (16, 512)])
+def test_kru_chunks(engine, oracle, golden, dchunk, threads):
+    case, ins, seeded = case_inputs(oracle, golden, "kru_paper_m8")
+    o = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0, "shared_memory_budget": 49152,
+         "thread_shape": [threads, 1, 1], "tile_sizes": [dchunk, 1, 1], "unroll_copy_shared": False,
+         "unroll_factor": 1, "use_private": False, "use_shared": True}
+    got, _ = run_on_gpu(engine, "3KRU", ins, seeded, options=o)
+    for k, rec in case["outputs"].items():
+        assert_exact(oracle, "kru", k, got[k], rec["fnv"])
+
+
+@pytest.mark.parametrize("th,rf,rw", [(1, 4, 7), (4, 4, 7), (2, 8, 7), (4, 4, 4), (4, 4, 8), (2, 8, 4),
+                                      (8, 2, 7), (1, 1, 1)])
+def test_gconv_variants(engine, oracle, golden, th, rf, rw):
+    for name in ["gconv_small", "gconv_paper_n1g2"]:
+        case, ins, seeded = case_inputs(oracle, golden, name)
+        o = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0, "shared_memory_budget": 49152,
+             "thread_shape": [1, 1, 1], "tile_sizes": [th, rf, rw], "unroll_copy_shared": False,
+             "unroll_factor": 1, "use_private": False, "use_shared": True}
+        got, _ = run_on_gpu(engine, "gconv", ins, seeded, options=o)
+        assert_exact(oracle, name, "O", got["O"], case["outputs"]["O"]["fnv"])
+
+
+def test_kru_full_paper_shape(engine, oracle):
+    """3-KRU at M=256, N=16, D=32 against the restatement."""
+    rng = oracle.rng(7)
+    ins = {"W0": rng.f32((32, 16)), "W1": rng.f32((32, 16)), "W2": rng.f32((32, 16)),
+           "X": rng.f32((256, 16, 16, 16))}
+    got, _ = run_on_gpu(engine, "3KRU", ins, {})
+    y, xw1, xw2 = oracle.kru3(ins["W0"], ins["W1"], ins["W2"], ins["X"])
+    for k, ref in (("Y", y), ("XW1", xw1), ("XW2", xw2)):
+        assert max_rel(ref, got[k]) <= TOL
+        np.testing.assert_array_equal(got[k], ref)
+
+
+def test_gconv_full_paper_shape_sampled(engine, oracle):
+    """gconv at the BASELINE shape (N=32,G=32,C=F=16,58x58,3x3): the full
+    oracle takes minutes, so compare 200k random output points exactly."""
+    rng = oracle.rng(11)
+    ins = {"I": rng.f32((32, 32, 16, 58, 58)), "W1": rng.f32((32, 16, 16, 3, 3)), "B": rng.f32((16,))}
+    got, _ = run_on_gpu(engine, "gconv", ins, {})
+    O = got["O"]
+    assert O.shape == (32, 32, 16, 56, 56)
+    idx = np.random.default_rng(0).integers(0, O.size, 200_000)
+    ref = oracle.gconv_points(ins["I"], ins["W1"], ins["B"], idx)
+    np.testing.assert_array_equal(O.reshape(-1)[idx], ref)
+
+
+def test_c3_accumulates_in_place(engine, oracle, golden):
+    """C3 is `+=` (in/out): running twice accumulates twice."""
+    case, ins, seeded = case_inputs(oracle, golden, "c3_small")
+    p = [to_dev(ins["I3"]), to_dev(ins["W"])]
+    c3 = to_dev(seeded["C3"])
+    h = engine.compile("C3", p, [c3])
+    engine.run(h, p, [c3])
+    engine.run(h, p, [c3])
+    once = oracle.c3(ins["I3"], ins["W"], seeded["C3"])
+    twice = oracle.c3(ins["I3"], ins["W"], once)
+    np.testing.assert_array_equal(c3.cpu().numpy(), twice)
+
+
+@pytest.mark.parametrize("name", ["tbmm_small", "c3_small", "mlp3_small", "2lut_small", "gconv_small"])
+def test_host_buffers_equal_device(engine, oracle, golden, name):
+    """TCB_HOST tensors (library does H2D/D2H) give the device path's bits."""
+    case, ins, seeded = case_inputs(oracle, golden, name)
+    got_h, _ = run_on_gpu(engine, case["def"], ins, seeded, host=True)
+    for k, rec in case["outputs"].items():
+        assert_exact(oracle, name + "/host", k, got_h[k], rec["fnv"])
+
+
+def test_lut_index_out_of_range(engine):
+    from paper_1802_04730_b200 import TcError
+    lut = to_dev(np.ones((5, 8), np.float32))
+    idx = to_dev(np.array([[0, 1], [2, 9]], np.int32))
+    out = torch.zeros((2, 8), device="cuda")
+    h = engine.compile("1LUT", [lut, idx], [out])
+    with pytest.raises(TcError) as ei:
+        engine.run(h, [lut, idx], [out])
+    assert ei.value.kind == "IndexOutOfRange"
+
+
+def test_lut_paper_shape(engine, oracle):
+    """1LUT at E=1e6 (1e7 at the paper shape is 2.5 GB/table), D=64, B=128, L=50."""
+    rng = oracle.rng(3)
+    lut = rng.f32((1_000_000, 64))
+    idx = rng.i32((128, 50), 0, 1_000_000)
+    got, _ = run_on_gpu(engine, "1LUT", {"LUT": lut, "I": idx}, {})
+    np.testing.assert_array_equal(got["O"], oracle.lut(lut, idx))
+
+
+def test_cuda_graph_capture(engine, oracle, golden):
+    case, ins, seeded = case_inputs(oracle, golden, "tbmm_paper")
+    p = [to_dev(ins["X"]), to_dev(ins["Y"])]
+    z = torch.zeros((500, 26, 26), device="cuda")
+    h = engine.compile("tbmm", p, [z])
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        engine.run(h, p, [z])  # warm-up (lazy module load) outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    z.zero_()
+    with torch.cuda.graph(g):
+        engine.run(h, p, [z], check_errors=False)
+    g.replay()
+    torch.cuda.synchronize()
+    assert fnv_hex(oracle, z.cpu().numpy()) == case["outputs"]["Z"]["fnv"]
+
+
+def test_tuner_populates_cache_and_compile_replays(engine, oracle, golden, tmp_path):
+    """tune() on the GPU: every evaluated candidate min-updates the cache;
+    a later compile without options hits the cache."""
+    import paper_1802_04730_b200 as tcb
+    tcb.cache_purge()
+    log = tmp_path / "session.jsonl"
+    case, ins, seeded = case_inputs(oracle, golden, "tmm_paper")
+    p = [to_dev(ins["A"]), to_dev(ins["B"])]
+    c = torch.zeros((128, 256), device="cuda")
+    best = engine.tune("tmm", p, [c], population=8, generations=2, seed=1, timing_iters=3,
+                       session_log=str(log))
+    assert tcb.cache_size() == 1
+    lines = [json.loads(x) for x in log.read_text().splitlines()]
+    assert len(lines) == 3
+    costs = [x["best_cost"] for x in lines]
+    assert all(a >= b for a, b in zip(costs, costs[1:]))  # elitist monotonicity
+    h = engine.compile("tmm", p, [c])
+    d = engine.describe(h)
+    assert d["options_source"] == "cache"
+    assert json.loads(json.dumps(d["options"])) == best
+    engine.run(h, p, [c])
+    torch.cuda.synchronize()
+    assert fnv_hex(oracle, c.cpu().numpy()) == case["outputs"]["C"]["fnv"]
+    path = str(tmp_path / "tc-cache.json")
+    tcb.cache_save(path)
+    tcb.cache_purge()
+    h2 = engine.compile("tmm", p, [c])
+    assert engine.describe(h2)["options_source"] == "default"
+    tcb.cache_load(path)
+    h3 = engine.compile("tmm", p, [c])
+    assert engine.describe(h3)["options_source"] == "cache"
+    tcb.cache_purge()
+
+
+def test_paper_style_call(engine, oracle):
+    """ee.tmm(A, B) allocates, compiles and runs."""
+    rng = oracle.rng(5)
+    A, B = rng.f32((33, 17)), rng.f32((45, 17))
+    C = engine.tmm(to_dev(A), to_dev(B))
+    np.testing.assert_array_equal(C.cpu().numpy(), oracle.tmm(A, B))
