@@ -114,7 +114,7 @@ struct tcb_engine {
       const auto& p = params[i];
       if (p.scalar()) continue;
       int want = p.elem == lang::Elem::Int ? TCB_I32 : TCB_F32;
-      if (in[i].dtype != want)
+      if (in[i].data && in[i].dtype != want)  // shape-only descriptors carry no dtype
         fail(ErrorKind::ShapeMismatch, "parameter '" + p.name + "' must be " + (want == TCB_I32 ? "int32" : "float32"));
       m[p.name] = shapeOf(in[i]);
     }

@@ -1,19 +1,25 @@
-// fc_chain.cu — fused chains of FC+bias+ReLU layers in ONE kernel:
+// fc_chain.cu — chains of FC+bias+ReLU layers in ONE kernel, split across a
+// thread-block cluster:
 //   MLP1     proj/kernels/mlp1.tc:2-6        (1 layer)
 //   2FCRelu  paper_1802_04730_b200/tc/ops.tc (2 layers)
-//   MLP3     proj/kernels/mlp3.tc:4-16       (3 layers, single kernel as in
-//            the paper's claim)
+//   MLP3     proj/kernels/mlp3.tc:4-16       (3 layers; the paper's single-
+//            kernel claim)
 //
-// One CTA owns R batch rows. Every layer's input activations live in
-// shared memory (the first layer's rows are staged once, each later
-// layer reads the previous layer's smem output), so intermediate layers
-// never round-trip through HBM; each layer's output is also written to its
-// global return tensor. Weights stream through a double-buffered
-// shared-memory ring of KC-wide column chunks filled by 16-byte cp.async.
-// Thread t owns output features t, t+T (Q ≤ 2 per thread) for all R rows:
-// R independent chains per feature, each a sequential FFMA chain in
-// ascending k starting from bias[o] — the reference order — followed by
-// fmaxf(·, 0) (interpreter.cc:22-24: std::fmax, NaN-ignoring).
+// A cluster of CN CTAs owns R batch rows. Layer l's output features are
+// split across the cluster (CTA c owns columns [c*cols_l, (c+1)*cols_l)),
+// so each CTA streams only its slice of every weight matrix. At kernel
+// start one warp issues EVERY bulk async copy the CTA will need — the R
+// input rows and the weight slices of all layers (cp.async.bulk, global →
+// shared, completing on mbarriers; the first layer is split in K-chunks
+// with one barrier each so its reduction starts as soon as the first chunk
+// lands). After a layer, each CTA publishes its output slice in shared
+// memory, the cluster synchronises, and every CTA gathers the full next-
+// layer input from its peers over DSMEM (mapa + ld.shared::cluster): the
+// activations never touch HBM except as the layer's own return tensor.
+//
+// Exactness: each (row, column) output is one thread's sequential FFMA
+// chain in ascending k from bias[o], then fmaxf(·, 0) — the interpreter's
+// order (interpreter.cc:218-233; builtin fmaxf → std::fmax, :22-24).
 #include "kernels.cuh"
 
 namespace tcb {
@@ -21,183 +27,326 @@ namespace k {
 
 namespace {
 
-constexpr int KC = 32;       // weight chunk depth (columns)
-constexpr int WLD = KC + 4;  // padded smem row stride
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
-}
+struct FcPlan {
+  int cn, R;
+  int cols[kMaxLayers];      // columns per CTA
+  int wld[kMaxLayers];       // padded row stride of the weight slice (floats)
+  int ald[kMaxLayers + 1];   // padded row stride of layer l's input activations
+  int offW[kMaxLayers];      // smem float offsets
+  int offAct, offSlice0, offSlice1, offBar;
+  int kc, nchunk0;           // first-layer K chunking
+  int bulk;                  // 1: cp.async.bulk path, 0: cooperative loads
+};
 
 __host__ __device__ inline int up4(int x) { return (x + 3) & ~3; }
-
-template <int R, int Q>
-__global__ void fc_chain_kernel(const FcChainArgs a, const int wvec, const int outMax) {
-  extern __shared__ __align__(16) float sm[];
-  const int T = blockDim.x, tid = threadIdx.x;
-  const int row0 = blockIdx.x * R;
-
-  // [2][outMax][WLD] weight ring, then the activation buffers: each
-  // layer's input [R][ld] is followed by its output (the next layer's input)
-  float* wbuf = sm;
-  float* in = wbuf + 2 * outMax * WLD;
-  int ldi = up4(a.L[0].kred);
-
-  // stage the first layer's input rows (only the kred columns it reads)
-  for (int e = tid; e < R * ldi; e += T) {
-    int r = e / ldi, c = e % ldi;
-    int b = row0 + r;
-    in[e] = (b < a.batch && c < a.L[0].kred) ? a.I[(int64_t)b * a.ldi + c] : 0.0f;
-  }
-
-#pragma unroll
-  for (int l = 0; l < kMaxLayers; ++l) {
-    if (l >= a.layers) break;
-    const FcLayer L = a.L[l];
-    float acc[Q][R];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      int o = tid + q * T;
-#pragma unroll
-      for (int r = 0; r < R; ++r) acc[q][r] = (o < L.out) ? __ldg(L.bias + o) : 0.0f;
-    }
-    const int nch = (L.kred + KC - 1) / KC;
-    auto loadChunk = [&](int stage, int k0) {
-      float* dst = wbuf + stage * outMax * WLD;
-      if (wvec) {
-        for (int e = tid; e < L.out * (KC / 4); e += T) {
-          int o = e / (KC / 4), c = (e % (KC / 4)) * 4;
-          bool ok = k0 + c < L.kred;
-          const float* src = ok ? L.W + (int64_t)o * L.ldw + k0 + c : L.W;
-          cp_async16(dst + o * WLD + c, src, ok ? 16 : 0);
-        }
-      } else {
-        for (int e = tid; e < L.out * KC; e += T) {
-          int o = e / KC, c = e % KC;
-          dst[o * WLD + c] = (k0 + c < L.kred) ? L.W[(int64_t)o * L.ldw + k0 + c] : 0.0f;
-        }
-      }
-    };
-    __syncthreads();  // previous layer's outputs (this layer's inputs) complete; wbuf free
-    loadChunk(0, 0);
-    asm volatile("cp.async.commit_group;\n" ::);
-    for (int c = 0; c < nch; ++c) {
-      const int st = c & 1;
-      if (c + 1 < nch) {
-        loadChunk(st ^ 1, (c + 1) * KC);
-        asm volatile("cp.async.commit_group;\n" ::);
-        asm volatile("cp.async.wait_group 1;\n" ::);
-      } else {
-        asm volatile("cp.async.wait_group 0;\n" ::);
-      }
-      __syncthreads();
-      const float* wch = wbuf + st * outMax * WLD;
-      const int k0 = c * KC;
-      const int klim = min(KC, L.kred - k0);
-      const int k4 = klim & ~3;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        int o = tid + q * T;
-        if (o < L.out) {
-          const float* wr = wch + o * WLD;
-          int kk = 0;
-          for (; kk < k4; kk += 4) {
-            float4 w4 = *reinterpret_cast<const float4*>(wr + kk);
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              float4 x4 = *reinterpret_cast<const float4*>(in + r * ldi + k0 + kk);
-              float v = acc[q][r];
-              v = __fmaf_rn(x4.x, w4.x, v);
-              v = __fmaf_rn(x4.y, w4.y, v);
-              v = __fmaf_rn(x4.z, w4.z, v);
-              v = __fmaf_rn(x4.w, w4.w, v);
-              acc[q][r] = v;
-            }
-          }
-          for (; kk < klim; ++kk) {
-            float w = wr[kk];
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[q][r] = __fmaf_rn(in[r * ldi + k0 + kk], w, acc[q][r]);
-          }
-        }
-      }
-      __syncthreads();
-    }
-    // epilogue: ReLU, keep in smem for the next layer, write the return
-    float* nxt = in + R * ldi;
-    const int ldn = up4(L.out);
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      int o = tid + q * T;
-      if (o < L.out) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          float v = fmaxf(acc[q][r], 0.0f);
-          nxt[r * ldn + o] = v;
-          int b = row0 + r;
-          if (b < a.batch) L.O[(int64_t)b * L.out + o] = v;
-        }
-      }
-    }
-    // zero the pad columns so float4 reads of the next layer stay defined
-    for (int e = tid; e < R * (ldn - L.out); e += T) {
-      int r = e / (ldn - L.out), c = L.out + e % (ldn - L.out);
-      nxt[r * ldn + c] = 0.0f;
-    }
-    in = nxt;
-    ldi = ldn;
-  }
+// row stride ≡ 4 (mod 32) floats: float4 reads of 8 consecutive rows hit 8
+// distinct 16-byte bank groups
+__host__ __device__ inline int padRow(int k) {
+  int l = up4(k);
+  while (l % 32 != 4) l += 4;
+  return l;
 }
 
-template <int R>
-cudaError_t launchR(const FcChainArgs& a, int threads, int wvec, int outMax, size_t smem, cudaStream_t s) {
-  dim3 grid((a.batch + R - 1) / R);
-  int q = (outMax + threads - 1) / threads;
-  if (q <= 1) {
-    auto kfn = fc_chain_kernel<R, 1>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kfn<<<grid, threads, smem, s>>>(a, wvec, outMax);
-  } else if (q == 2) {
-    auto kfn = fc_chain_kernel<R, 2>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kfn<<<grid, threads, smem, s>>>(a, wvec, outMax);
+__device__ __forceinline__ unsigned smemAddr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbarInit(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smemAddr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbarExpectTx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemAddr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbarWait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smemAddr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulkCopy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smemAddr(dst)),
+      "l"(src), "r"(bytes), "r"(smemAddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void clusterSync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned clusterRank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ float ldCluster(const float* local, unsigned rank) {
+  unsigned remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smemAddr(local)), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ float4 lds4(unsigned addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float lds1(unsigned addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float fma4(float4 x, float4 w, float acc) {
+  acc = __fmaf_rn(x.x, w.x, acc);
+  acc = __fmaf_rn(x.y, w.y, acc);
+  acc = __fmaf_rn(x.z, w.z, acc);
+  return __fmaf_rn(x.w, w.w, acc);
+}
+
+// acc = chain over k in [k0, k1) of act[k] * w[k]; operands addressed as
+// 32-bit shared-window byte addresses. Three register sets rotate by code
+// position (no moves): the loads of 4-k group g+2 are in flight while the
+// dependent FFMAs of group g run.
+__device__ __forceinline__ float chainSegment(unsigned xa, unsigned wa, int k0, int k1, float acc) {
+  const int ng = (k1 - k0) >> 2;
+  const unsigned x0 = xa + k0 * 4, w0 = wa + k0 * 4;
+  float4 xA, wA, xB, wB, xC, wC;
+  if (ng > 0) {
+    xA = lds4(x0);
+    wA = lds4(w0);
+  }
+  if (ng > 1) {
+    xB = lds4(x0 + 16);
+    wB = lds4(w0 + 16);
+  }
+  int g = 0;
+  for (; g + 3 <= ng; g += 3) {
+    const unsigned o = g * 16;
+    xC = lds4(x0 + o + 32);
+    wC = lds4(w0 + o + 32);
+    acc = fma4(xA, wA, acc);
+    if (g + 3 < ng) {
+      xA = lds4(x0 + o + 48);
+      wA = lds4(w0 + o + 48);
+    }
+    acc = fma4(xB, wB, acc);
+    if (g + 4 < ng) {
+      xB = lds4(x0 + o + 64);
+      wB = lds4(w0 + o + 64);
+    }
+    acc = fma4(xC, wC, acc);
+  }
+  if (g < ng) acc = fma4(xA, wA, acc);
+  if (g + 1 < ng) acc = fma4(xB, wB, acc);
+  for (int kk = k0 + 4 * ng; kk < k1; ++kk) acc = __fmaf_rn(lds1(xa + kk * 4), lds1(wa + kk * 4), acc);
+  return acc;
+}
+
+__global__ void fc_cluster_kernel(const FcChainArgs a, const FcPlan p) {
+  extern __shared__ __align__(128) float sm[];
+  const int tid = threadIdx.x, T = blockDim.x, R = p.R;
+  const unsigned rank = p.cn > 1 ? clusterRank() : 0;
+  const int row0 = blockIdx.y * R;
+  const int rows = min(R, a.batch - row0);
+  float* act = sm + p.offAct;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + p.offBar);  // [nchunk0 + layers]
+  const int nbar = p.nchunk0 + a.layers;
+
+  // ---- issue every load of the kernel up front
+  if (p.bulk) {
+    if (tid == 0) {
+      for (int b = 0; b < nbar; ++b) mbarInit(&bars[b], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid < 32) {
+      const int lane = tid;
+      // expected bytes per barrier (one elected lane), then the copies
+      if (lane == 0) {
+        for (int q = 0; q < p.nchunk0; ++q) {
+          int k0 = q * p.kc, len = min(p.kc, a.L[0].kred - k0);
+          int c0 = rank * p.cols[0], nc = max(0, min(p.cols[0], a.L[0].out - c0));
+          mbarExpectTx(&bars[q], (unsigned)(len * 4 * (rows + nc)));
+        }
+        for (int l = 1; l < a.layers; ++l) {
+          int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
+          mbarExpectTx(&bars[p.nchunk0 + l], (unsigned)(a.L[l].kred * 4 * nc));
+        }
+        mbarExpectTx(&bars[p.nchunk0], 0u);  // the layer-0 slot of the per-layer range is unused
+      }
+      __syncwarp();
+      // layer 0: input rows and weight slice, chunked along k
+      {
+        const int c0 = rank * p.cols[0], nc = max(0, min(p.cols[0], a.L[0].out - c0));
+        const int units = p.nchunk0 * (rows + nc);
+        for (int u = lane; u < units; u += 32) {
+          int q = u / (rows + nc), j = u % (rows + nc);
+          int k0 = q * p.kc, len = min(p.kc, a.L[0].kred - k0);
+          if (j < rows)
+            bulkCopy(act + j * p.ald[0] + k0, a.I + (int64_t)(row0 + j) * a.ldi + k0, len * 4, &bars[q]);
+          else
+            bulkCopy(sm + p.offW[0] + (j - rows) * p.wld[0] + k0,
+                     a.L[0].W + (int64_t)(c0 + j - rows) * a.L[0].ldw + k0, len * 4, &bars[q]);
+        }
+      }
+      for (int l = 1; l < a.layers; ++l) {
+        const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
+        for (int j = lane; j < nc; j += 32)
+          bulkCopy(sm + p.offW[l] + j * p.wld[l], a.L[l].W + (int64_t)(c0 + j) * a.L[l].ldw,
+                   a.L[l].kred * 4, &bars[p.nchunk0 + l]);
+      }
+    }
+    // rows past the batch end are zero
+    for (int e = tid; e < (R - rows) * p.ald[0]; e += T) act[rows * p.ald[0] + e] = 0.0f;
+    __syncthreads();
   } else {
-    return cudaErrorInvalidConfiguration;
+    for (int e = tid; e < R * p.ald[0]; e += T) {
+      int r = e / p.ald[0], kk = e % p.ald[0];
+      act[e] = (r < rows && kk < a.L[0].kred) ? a.I[(int64_t)(row0 + r) * a.ldi + kk] : 0.0f;
+    }
+    for (int l = 0; l < a.layers; ++l) {
+      const int c0 = rank * p.cols[l];
+      for (int e = tid; e < p.cols[l] * a.L[l].kred; e += T) {
+        int j = e / a.L[l].kred, kk = e % a.L[l].kred;
+        sm[p.offW[l] + j * p.wld[l] + kk] =
+            (c0 + j < a.L[l].out) ? a.L[l].W[(int64_t)(c0 + j) * a.L[l].ldw + kk] : 0.0f;
+      }
+    }
+    __syncthreads();
   }
-  return cudaGetLastError();
-}
 
-int outMaxOf(const FcChainArgs& a) {
-  int m = 0;
-  for (int l = 0; l < a.layers; ++l) m = a.L[l].out > m ? a.L[l].out : m;
-  return m;
+#pragma unroll 1
+  for (int l = 0; l < a.layers; ++l) {
+    const FcLayer L = a.L[l];
+    const int cols = p.cols[l], c0 = rank * cols;
+    const float* W = sm + p.offW[l];
+    const int wld = p.wld[l], ald = p.ald[l];
+    float* slice = sm + ((l & 1) ? p.offSlice1 : p.offSlice0);  // [R][cols]
+    const unsigned actBase = smemAddr(act), wBase = smemAddr(W);
+    const int nchains = R * cols;
+    for (int base = 0; base < nchains; base += T) {
+      // one (row, column) chain per thread and pass; idle lanes run a dummy
+      // chain on row 0 / column 0 (no branches inside the reduction)
+      const int idx = base + tid;
+      const bool live = idx < nchains && c0 + idx / R < L.out;
+      const int r = live ? idx % R : 0, c = live ? idx / R : 0;
+      const unsigned xa = actBase + (unsigned)(r * ald) * 4u, wa = wBase + (unsigned)(c * wld) * 4u;
+      float acc = live ? __ldg(L.bias + c0 + c) : 0.0f;
+      const int nq = l == 0 ? p.nchunk0 : 1;
+      const int kcl = l == 0 ? p.kc : L.kred;
+      for (int q = 0; q < nq; ++q) {
+        if (p.bulk) mbarWait(&bars[l == 0 ? q : p.nchunk0 + l], 0);
+        acc = chainSegment(xa, wa, q * kcl, min(L.kred, (q + 1) * kcl), acc);
+      }
+      if (live) {
+        float v = fmaxf(acc, 0.0f);
+        slice[r * cols + c] = v;
+        if (r < rows) L.O[(int64_t)(row0 + r) * L.out + c0 + c] = v;
+      }
+    }
+    if (l + 1 < a.layers) {
+      // publish the slice to the cluster, then gather the next layer's input
+      if (p.cn > 1) clusterSync();
+      else __syncthreads();
+      const int ldn = p.ald[l + 1];
+      for (int e = tid; e < R * L.out; e += T) {
+        int r = e / L.out, col = e % L.out;
+        int owner = col / cols, c = col % cols;
+        const float* src = slice + r * cols + c;
+        act[r * ldn + col] = p.cn > 1 ? ldCluster(src, owner) : *src;
+      }
+      __syncthreads();
+    }
+  }
+  // keep this CTA's shared memory alive until every peer finished its DSMEM reads
+  if (p.cn > 1 && a.layers > 1) clusterSync();
 }
 
 }  // namespace
 
-size_t fcChainSmem(const FcChainArgs& a, int rows) {
-  size_t floats = (size_t)rows * up4(a.L[0].kred);
-  for (int l = 0; l < a.layers; ++l) floats += (size_t)rows * up4(a.L[l].out);
-  floats += 2 * (size_t)outMaxOf(a) * WLD;
-  return floats * sizeof(float);
+// Builds the plan; returns the dynamic shared-memory size (0 if infeasible).
+static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p) {
+  p = FcPlan{};
+  p.cn = cn;
+  p.R = R;
+  int off = 0;
+  for (int l = 0; l < a.layers; ++l) {
+    p.cols[l] = (a.L[l].out + cn - 1) / cn;
+    p.wld[l] = padRow(a.L[l].kred);
+    p.offW[l] = off;
+    off += p.cols[l] * p.wld[l];
+  }
+  int aldMax = 0;
+  p.ald[0] = padRow(a.L[0].kred);
+  for (int l = 1; l < a.layers; ++l) p.ald[l] = padRow(a.L[l].kred);
+  for (int l = 0; l < a.layers; ++l) aldMax = p.ald[l] > aldMax ? p.ald[l] : aldMax;
+  p.offAct = off;
+  off += R * aldMax;
+  int sliceMax = 0;
+  for (int l = 0; l < a.layers; ++l) sliceMax = R * p.cols[l] > sliceMax ? R * p.cols[l] : sliceMax;
+  p.offSlice0 = off;
+  off += sliceMax;
+  p.offSlice1 = off;
+  off += sliceMax;
+  off = (off + 3) & ~3;  // 16-byte alignment for the mbarriers
+  p.offBar = off;
+  p.kc = 128;
+  p.nchunk0 = (a.L[0].kred + p.kc - 1) / p.kc;
+  off += 2 * (p.nchunk0 + a.layers);  // uint64 each
+  bool bulk = (a.ldi % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.I) & 15) == 0);
+  for (int l = 0; l < a.layers; ++l)
+    bulk = bulk && (a.L[l].kred % 4 == 0) && (a.L[l].ldw % 4 == 0) &&
+           ((reinterpret_cast<uintptr_t>(a.L[l].W) & 15) == 0);
+  p.bulk = bulk ? 1 : 0;
+  return (size_t)off * sizeof(float);
 }
 
-cudaError_t launchFcChain(const FcChainArgs& a, int rows, int threads, cudaStream_t s) {
-  if (a.batch <= 0) return cudaSuccess;
-  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  int wvec = 1;
-  for (int l = 0; l < a.layers; ++l)
-    wvec &= (a.L[l].ldw % 4 == 0) && al16(a.L[l].W);
-  int outMax = outMaxOf(a);
-  size_t smem = fcChainSmem(a, rows);
-  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  switch (rows) {
-    case 1: return launchR<1>(a, threads, wvec, outMax, smem, s);
-    case 2: return launchR<2>(a, threads, wvec, outMax, smem, s);
-    case 4: return launchR<4>(a, threads, wvec, outMax, smem, s);
-    case 8: return launchR<8>(a, threads, wvec, outMax, smem, s);
-    default: return cudaErrorInvalidConfiguration;
+size_t fcChainSmem(const FcChainArgs& a, int rows, int cn) {
+  FcPlan p;
+  return planFc(a, rows, cn, p);
+}
+
+int fcChainThreads(const FcChainArgs& a, int rows, int cn) {
+  int need = 0;
+  for (int l = 0; l < a.layers; ++l) {
+    int cols = (a.L[l].out + cn - 1) / cn;
+    need = cols * rows > need ? cols * rows : need;
   }
+  // block size that runs every layer in one pass (any multiple of 32 works;
+  // smaller blocks take several passes)
+  int t = ((need + 31) / 32) * 32;
+  return t > 1024 ? 1024 : t;
+}
+
+cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s) {
+  if (a.batch <= 0) return cudaSuccess;
+  FcPlan p;
+  size_t smem = planFc(a, rows, cn, p);
+  if (smem > 227 * 1024 || cn < 1 || cn > 16 || rows < 1) return cudaErrorInvalidConfiguration;
+  if (threads < 32 || threads > 1024 || threads % 32) return cudaErrorInvalidConfiguration;
+  cudaFuncSetAttribute(fc_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cn > 8) cudaFuncSetAttribute(fc_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cn, (a.batch + rows - 1) / rows, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cn;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fc_cluster_kernel, a, p);
 }
 
 }  // namespace k

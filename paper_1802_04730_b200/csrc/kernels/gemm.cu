@@ -9,7 +9,8 @@
 // ascending k from the init value, with one fused multiply-add per step —
 // the reference interpreter's per-step rounding order (interpreter.cc:
 // 218-233). Operand tiles (TM×TK, TN×TK) are staged row-major in shared
-// memory by 16-byte cp.async (zero-filled at the edges), double buffered,
+// memory by 16-byte cp.async (zero-filled at the edges) through a 4- or
+// 8-stage ring (S-1 tiles in flight: the K loop is load-latency bound),
 // with a +4-float row pad that keeps the per-thread float4 k-reads
 // conflict-free. Tensor cores are deliberately not used here: their
 // internal accumulation order cannot reproduce the reference chain, and
@@ -37,13 +38,14 @@ __device__ __forceinline__ float initValue(const GemmArgs& a, const float* C, in
   return 0.0f;
 }
 
-template <int TM, int TN, int RM, int RN, int TK>
+template <int TM, int TN, int RM, int RN, int TK, int S>
 __global__ void __launch_bounds__((TM / RM) * (TN / RN))
     gemm_nt_tiled(const GemmArgs a, const int vec) {
   constexpr int TX = TN / RN, TY = TM / RM, NT = TX * TY;
   constexpr int LD = TK + 4;  // padded row stride, keeps 16B alignment
-  __shared__ __align__(16) float As[2][TM][LD];
-  __shared__ __align__(16) float Bs[2][TN][LD];
+  extern __shared__ __align__(16) float smem[];
+  float (*As)[TM][LD] = reinterpret_cast<float (*)[TM][LD]>(smem);            // [S][TM][LD]
+  float (*Bs)[TN][LD] = reinterpret_cast<float (*)[TN][LD]>(smem + S * TM * LD);  // [S][TN][LD]
 
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -92,28 +94,30 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
     }
   };
 
+  // S-stage cp.async ring: S-1 tiles in flight while one is consumed
   const int ntiles = (a.K + TK - 1) / TK;
-  loadTile(0, 0);
-  cp_async_commit();
+#pragma unroll
+  for (int s = 0; s < S - 1; ++s) {
+    if (s < ntiles) loadTile(s, s * TK);
+    cp_async_commit();
+  }
   for (int t = 0; t < ntiles; ++t) {
-    const int st = t & 1;
-    if (t + 1 < ntiles) {
-      loadTile(st ^ 1, (t + 1) * TK);
+    cp_async_wait<S - 2>();
+    __syncthreads();  // tile t landed for everyone; stage (t-1)%S is free
+    {
+      const int nt = t + S - 1;
+      if (nt < ntiles) loadTile(nt % S, nt * TK);
       cp_async_commit();
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
     }
-    __syncthreads();
-    const int klim = min(TK, a.K - t * TK);
-    const int k4 = klim & ~3;
-    int kk = 0;
-    for (; kk < k4; kk += 4) {
+    const int st = t % S;
+    const float* Ast = &As[st][ty][0];
+    const float* Bst = &Bs[st][tx][0];
+    auto group = [&](int kk) {  // one 4-k step of every chain of the micro-tile
       float4 av[RM], bv[RN];
 #pragma unroll
-      for (int i = 0; i < RM; ++i) av[i] = *reinterpret_cast<const float4*>(&As[st][ty + i * TY][kk]);
+      for (int i = 0; i < RM; ++i) av[i] = *reinterpret_cast<const float4*>(Ast + i * TY * LD + kk);
 #pragma unroll
-      for (int j = 0; j < RN; ++j) bv[j] = *reinterpret_cast<const float4*>(&Bs[st][tx + j * TX][kk]);
+      for (int j = 0; j < RN; ++j) bv[j] = *reinterpret_cast<const float4*>(Bst + j * TX * LD + kk);
 #pragma unroll
       for (int i = 0; i < RM; ++i)
 #pragma unroll
@@ -130,15 +134,24 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
       for (int i = 0; i < RM; ++i)
 #pragma unroll
         for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(av[i].w, bv[j].w, acc[i][j]);
-    }
-    for (; kk < klim; ++kk) {
+    };
+    const int klim = min(TK, a.K - t * TK);
+    if (klim == TK) {
+      // full tile: fully unrolled so the scheduler hoists the next group's
+      // shared loads above the current group's FFMAs
 #pragma unroll
-      for (int i = 0; i < RM; ++i)
+      for (int kk = 0; kk < TK; kk += 4) group(kk);
+    } else {
+      const int k4 = klim & ~3;
+      int kk = 0;
+      for (; kk < k4; kk += 4) group(kk);
+      for (; kk < klim; ++kk) {
 #pragma unroll
-        for (int j = 0; j < RN; ++j)
-          acc[i][j] = __fmaf_rn(As[st][ty + i * TY][kk], Bs[st][tx + j * TX][kk], acc[i][j]);
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(Ast[i * TY * LD + kk], Bst[j * TX * LD + kk], acc[i][j]);
+      }
     }
-    __syncthreads();
   }
 
 #pragma unroll
@@ -201,12 +214,22 @@ const GemmVariant kGemmVariants[] = {
     {13, 32, 32, 2, 4, 32, "t32x32_r2x4_k32"},
     {14, 16, 16, 2, 2, 32, "t16x16_r2x2_k32"},
     {15, 32, 64, 4, 4, 32, "t32x64_r4x4_k32"},
+    {16, 32, 32, 2, 2, 32, "t32x32_r2x2_k32_s8", 8},
+    {17, 16, 32, 2, 2, 32, "t16x32_r2x2_k32_s8", 8},
+    {18, 16, 16, 1, 1, 64, "t16x16_r1x1_k64"},
 };
 
-template <int TM, int TN, int RM, int RN, int TK>
+template <int TM, int TN, int RM, int RN, int TK, int S = 4>
 cudaError_t launchTiled(const GemmArgs& a, int vec, cudaStream_t s) {
   dim3 grid((a.N + TN - 1) / TN, (a.M + TM - 1) / TM, a.batch);
-  gemm_nt_tiled<TM, TN, RM, RN, TK><<<grid, (TM / RM) * (TN / RN), 0, s>>>(a, vec);
+  const size_t smem = (size_t)S * (TM + TN) * (TK + 4) * sizeof(float);
+  auto kfn = gemm_nt_tiled<TM, TN, RM, RN, TK, S>;
+  static bool attr = false;  // per instantiation
+  if (!attr) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  kfn<<<grid, (TM / RM) * (TN / RN), smem, s>>>(a, vec);
   return cudaGetLastError();
 }
 
@@ -242,6 +265,9 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
     case 13: return launchTiled<32, 32, 2, 4, 32>(a, vec, s);
     case 14: return launchTiled<16, 16, 2, 2, 32>(a, vec, s);
     case 15: return launchTiled<32, 64, 4, 4, 32>(a, vec, s);
+    case 16: return launchTiled<32, 32, 2, 2, 32, 8>(a, vec, s);
+    case 17: return launchTiled<16, 32, 2, 2, 32, 8>(a, vec, s);
+    case 18: return launchTiled<16, 16, 1, 1, 64>(a, vec, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -36,6 +36,7 @@ struct GemmVariant {
   int id;
   int tm, tn, rm, rn, tk;  // tm==0 ⇒ "direct" (no smem staging, 1 output / thread)
   const char* name;
+  int stages = 4;          // cp.async ring depth
 };
 int gemmVariantCount();
 const GemmVariant& gemmVariant(int i);
@@ -43,8 +44,9 @@ const GemmVariant& gemmVariant(int i);
 cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t s);
 
 // ------------------------------------------------------------ FC chain
-// Fused FC+bias+ReLU layers (MLP1 / 2FCRelu / MLP3): one CTA per `rows`
-// batch rows keeps every intermediate activation in shared memory.
+// Fused FC+bias+ReLU layers (MLP1 / 2FCRelu / MLP3): a cluster of `cn` CTAs
+// per `rows` batch rows; output features split across the cluster,
+// activations exchanged over DSMEM between layers.
 constexpr int kMaxLayers = 4;
 struct FcLayer {
   const float* W;     // [out][ldw]
@@ -60,8 +62,9 @@ struct FcChainArgs {
   int layers;
   FcLayer L[kMaxLayers];
 };
-cudaError_t launchFcChain(const FcChainArgs& a, int rows, int threads, cudaStream_t s);
-size_t fcChainSmem(const FcChainArgs& a, int rows);
+cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s);
+size_t fcChainSmem(const FcChainArgs& a, int rows, int cn);
+int fcChainThreads(const FcChainArgs& a, int rows, int cn);  // single-pass block size
 
 // ------------------------------------------------------------------ KRU
 struct KruArgs {

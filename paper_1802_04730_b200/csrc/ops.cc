@@ -64,9 +64,10 @@ void decodeGemm(const MappingOptions& o, Mapping& m) {
   int64_t tm = o.tileSizes[0], tn = o.tileSizes[1], tk = o.tileSizes[2];
   int64_t tx = o.threadShape[0], ty = o.threadShape[1];
   if (tm % ty || tn % tx) invalid("tile extents must be multiples of the thread block extents");
+  const int stages = o.unrollCopyShared ? 8 : 4;  // deeper copy pipeline
   for (int i = 1; i < k::gemmVariantCount(); ++i) {
     const auto& v = k::gemmVariant(i);
-    if (v.tm == tm && v.tn == tn && v.tk == tk && v.rm == tm / ty && v.rn == tn / tx) {
+    if (v.tm == tm && v.tn == tn && v.tk == tk && v.rm == tm / ty && v.rn == tn / tx && v.stages == stages) {
       m.gemmVariant = i;
       m.gemmThreads = static_cast<int>(tx * ty);
       return;
@@ -133,7 +134,7 @@ std::string Mapping::describe() const {
       os << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
       break;
     case Family::FcChain:
-      if (fused) os << "fused rows=" << rows << " threads=" << threads;
+      if (fused) os << "cluster rows=" << rows << " cn=" << cn << " threads=" << threads;
       else os << "per-layer " << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
       break;
     case Family::Kru3: os << "fused dchunk=" << dchunk << " threads=" << threads; break;
@@ -298,19 +299,19 @@ Mapping decode(const Problem& p, const MappingOptions& o) {
       }
       m.fused = true;
       m.rows = o.tileSizes.empty() ? 1 : static_cast<int>(o.tileSizes[0]);
-      if (m.rows != 1 && m.rows != 2 && m.rows != 4 && m.rows != 8) invalid("fused FC chain rows per CTA must be 1, 2, 4 or 8");
+      m.cn = o.tileSizes.size() < 2 ? 1 : static_cast<int>(o.tileSizes[1]);
+      if (m.rows < 1 || m.rows > 32) invalid("fused FC chain rows per cluster must be in [1, 32]");
+      if (m.cn < 1 || m.cn > 16) invalid("fused FC chain cluster size must be in [1, 16]");
       m.threads = static_cast<int>(o.threads());
       if (m.threads < 32 || m.threads % 32) invalid("fused FC chain needs a multiple of 32 threads");
-      int outMax = 0;
-      for (const auto& L : p.fc.layers) outMax = std::max(outMax, L.out);
-      if (outMax > 2 * m.threads) invalid("fused FC chain: more than two output features per thread");
       k::FcChainArgs a{};
       a.layers = static_cast<int>(p.fc.layers.size());
+      a.batch = p.fc.batch;
       for (int l = 0; l < a.layers; ++l) {
         a.L[l].out = p.fc.layers[l].out;
         a.L[l].kred = p.fc.layers[l].kred;
       }
-      if (k::fcChainSmem(a, m.rows) > 227 * 1024) invalid("fused FC chain exceeds the shared-memory capacity");
+      if (k::fcChainSmem(a, m.rows, m.cn) > 227 * 1024) invalid("fused FC chain exceeds the shared-memory capacity");
       break;
     }
     case Family::Kru3: {
@@ -367,22 +368,43 @@ MappingOptions defaultOptions(const Problem& p) {
   MappingOptions o;
   switch (p.family) {
     case Family::Gemm: {
-      // the reference's contraction preset (options.cc:182-191) is a valid
-      // tile here: 32x32 CTA tile, 16x16 threads, 2x2 register micro-tile
+      // start from the reference's contraction preset (options.cc:182-191:
+      // 32x32 tile, 16x16 threads, 2x2 micro-tile) and adapt the tile to
+      // the problem: finer tiles when the grid would not cover the SMs, an
+      // 8-deep copy ring when the reduction is long
       o = baselineOptions()[0];
       const GemmDesc& g = p.gemm;
-      double ctas = (double)g.batch * ((g.M + 31) / 32) * ((g.N + 31) / 32);
-      if (ctas < 148) {  // small problems: finer tiles to cover the SMs
-        o.tileSizes = {16, 16, 32};
-        o.threadShape = {{16, 16, 1}};
+      auto ctas = [&](int tm, int tn) { return (double)g.batch * ((g.M + tm - 1) / tm) * ((g.N + tn - 1) / tn); };
+      o.unrollCopyShared = g.K > 128;
+      if (ctas(32, 32) < 148) {
+        if (o.unrollCopyShared) {
+          o.tileSizes = {16, 32, 32};
+          o.threadShape = {{16, 8, 1}};
+        } else {
+          o.tileSizes = {16, 16, 32};
+          o.threadShape = {{16, 16, 1}};
+        }
       }
       break;
     }
     case Family::FcChain: {
+      // clusters of up to 8 CTAs split the widest layer into ~16-column
+      // slices; rows per cluster chosen so the grid covers ~128 CTAs
       int outMax = 0;
       for (const auto& L : p.fc.layers) outMax = std::max(outMax, L.out);
-      o.tileSizes = {1, 1, 1};
-      o.threadShape = {{outMax > 256 ? 512 : outMax > 128 ? 256 : 128, 1, 1}};
+      int cn = std::min(8, std::max(1, (outMax + 15) / 16));
+      int rows = 1;
+      while (rows < 16 && (int64_t)((p.fc.batch + rows * 2 - 1) / (rows * 2)) * cn >= 128) rows *= 2;
+      k::FcChainArgs a{};
+      a.layers = static_cast<int>(p.fc.layers.size());
+      for (int l = 0; l < a.layers; ++l) {
+        a.L[l].out = p.fc.layers[l].out;
+        a.L[l].kred = p.fc.layers[l].kred;
+      }
+      while (rows > 1 && k::fcChainSmem(a, rows, cn) > 200 * 1024) rows /= 2;
+      int t = std::max(64, k::fcChainThreads(a, rows, cn));  // one pass per layer
+      o.tileSizes = {rows, cn, 1};
+      o.threadShape = {{t, 1, 1}};
       o.fusion = Fusion::Max;
       o.useShared = true;
       break;
@@ -436,7 +458,8 @@ GenePools genePools(const Problem& p) {
       g.fusion = {Fusion::Max};
       if (p.family == Family::FcChain) {
         g.tile0 = {1, 2, 4, 8, 16, 32, 64};
-        g.tx = {4, 8, 16, 32, 64, 128, 256};
+        g.tile1 = {1, 2, 4, 8, 16, 32, 64};
+        g.tx = {4, 8, 16, 32, 64, 128, 256, 512};
         g.fusion = {Fusion::Max, Fusion::Min};
       }
       break;
@@ -522,7 +545,7 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
         a.L[l].kred = L.kred;
         a.L[l].ldw = L.ldw;
       }
-      check(k::launchFcChain(a, m.rows, m.threads, s), "FC chain");
+      check(k::launchFcChain(a, m.rows, m.cn, m.threads, s), "FC chain");
       return;
     }
     case Family::Kru3: {

@@ -82,7 +82,7 @@ struct Mapping {
   int gemmVariant = 4, gemmThreads = 0;
   // FcChain
   bool fused = true;
-  int rows = 1, threads = 128;
+  int rows = 1, cn = 1, threads = 128;
   // Kru3
   int dchunk = 16;
   // Gconv

@@ -103,16 +103,28 @@ def test_every_gemm_variant_identical(engine, oracle, golden, name):
     assert ran == len(variants) + 1
 
 
-@pytest.mark.parametrize("rows,threads", [(1, 64), (2, 128), (4, 128), (8, 256)])
-def test_fc_chain_fused_variants(engine, oracle, golden, rows, threads):
-    for name in ["2fcrelu_small", "mlp3_small", "mlp3_paper"]:
+@pytest.mark.parametrize("rows,cn,threads", [(1, 1, 64), (2, 2, 64), (4, 8, 64), (8, 8, 64), (8, 4, 256),
+                                             (16, 8, 128), (3, 3, 96), (8, 16, 64)])
+def test_fc_chain_cluster_variants(engine, oracle, golden, rows, cn, threads):
+    """Cluster sizes 1..16 (16 = non-portable), ragged rows and column splits.
+    Combinations whose weight slices exceed shared memory must be rejected
+    with MappingInvalid (never silently run)."""
+    from paper_1802_04730_b200 import TcError
+    ran = 0
+    for name in ["2fcrelu_small", "mlp3_small", "mlp3_paper", "mlp1_ragged", "2fcrelu_paper"]:
         case, ins, seeded = case_inputs(oracle, golden, name)
         o = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0,
-             "shared_memory_budget": 49152, "thread_shape": [threads, 1, 1], "tile_sizes": [rows, 1, 1],
+             "shared_memory_budget": 49152, "thread_shape": [threads, 1, 1], "tile_sizes": [rows, cn, 1],
              "unroll_copy_shared": False, "unroll_factor": 1, "use_private": False, "use_shared": True}
-        got, _ = run_on_gpu(engine, case["def"], ins, seeded, options=o)
+        try:
+            got, _ = run_on_gpu(engine, case["def"], ins, seeded, options=o)
+        except TcError as e:
+            assert e.kind == "MappingInvalid", str(e)
+            continue
+        ran += 1
         for k, rec in case["outputs"].items():
             assert_exact(oracle, name, k, got[k], rec["fnv"])
+    assert ran >= 3
 
 
 @pytest.mark.parametrize("dchunk,threads", [(1, 64), (3, 128), (8, 256), (16, 512)])
