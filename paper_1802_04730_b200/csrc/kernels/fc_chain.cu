@@ -8,11 +8,11 @@
 // A cluster of CN CTAs owns R batch rows. Layer l's output features are
 // split across the cluster (CTA c owns columns [c*cols_l, (c+1)*cols_l)),
 // so each CTA streams only its slice of every weight matrix. At kernel
-// start one warp issues EVERY bulk async copy the CTA will need — the R
-// input rows and the weight slices of all layers (cp.async.bulk, global →
-// shared, completing on mbarriers; the first layer is split in K-chunks
-// with one barrier each so its reduction starts as soon as the first chunk
-// lands). After a layer, each CTA publishes its output slice in shared
+// start one warp issues EVERY bulk async copy the CTA will need — one
+// cp.async.bulk per row: the R input rows and the weight-slice rows of all
+// layers, completing on mbarriers (one per first-layer operand row, so a
+// thread starts its chain as soon as its two rows landed; one per later
+// layer). After a layer, each CTA publishes its output slice in shared
 // memory, the cluster synchronises, and every CTA gathers the full next-
 // layer input from its peers over DSMEM (mapa + ld.shared::cluster): the
 // activations never touch HBM except as the layer's own return tensor.
@@ -20,6 +20,8 @@
 // Exactness: each (row, column) output is one thread's sequential FFMA
 // chain in ascending k from bias[o], then fmaxf(·, 0) — the interpreter's
 // order (interpreter.cc:218-233; builtin fmaxf → std::fmax, :22-24).
+#include <cstdio>
+
 #include "kernels.cuh"
 
 namespace tcb {
@@ -35,7 +37,7 @@ struct FcPlan {
   int ald[kMaxLayers + 1];   // padded row stride of layer l's input activations
   int offW[kMaxLayers];      // smem float offsets
   int offAct, offSlice0, offSlice1, offBar;
-  int kc, nchunk0;           // first-layer K chunking
+  int kc, nchunk0;           // (unused: first layer loads one copy per row)
   int bulk;                  // 1: cp.async.bulk path, 0: cooperative loads
 };
 
@@ -58,16 +60,29 @@ __device__ __forceinline__ void mbarExpectTx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemAddr(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbarWait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smemAddr(bar)),
-      "r"(parity)
-      : "memory");
+// Waits for the barrier phase; traps (a launch error the host reports as
+// ErrorKind::Cuda) instead of hanging if the phase never completes.
+__device__ __forceinline__ void mbarWait(uint64_t* bar, unsigned parity, int tag = -1) {
+  const unsigned addr = smemAddr(bar);
+  for (unsigned spin = 0;; ++spin) {
+    unsigned done;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spin > (1u << 22)) {
+      if ((threadIdx.x & 31) == 0)
+        printf("tc-b200: mbarrier %d never completed (block %d,%d thread %d)\n", tag, blockIdx.x, blockIdx.y,
+               threadIdx.x);
+      __trap();
+    }
+  }
 }
 __device__ __forceinline__ void bulkCopy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
   asm volatile(
@@ -76,8 +91,11 @@ __device__ __forceinline__ void bulkCopy(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smemAddr(bar))
       : "memory");
 }
+// Non-.aligned form: callers may reach it with a warp that diverged in an
+// mbarrier spin (lanes waiting on different barriers); we also __syncwarp().
 __device__ __forceinline__ void clusterSync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  __syncwarp();
+  asm volatile("barrier.cluster.arrive.release;\nbarrier.cluster.wait.acquire;\n" ::: "memory");
 }
 __device__ __forceinline__ unsigned clusterRank() {
   unsigned r;
@@ -153,14 +171,19 @@ __device__ __forceinline__ float chainSegment(unsigned xa, unsigned wa, int k0, 
 __global__ void fc_cluster_kernel(const FcChainArgs a, const FcPlan p) {
   extern __shared__ __align__(128) float sm[];
   const int tid = threadIdx.x, T = blockDim.x, R = p.R;
-  const unsigned rank = p.cn > 1 ? clusterRank() : 0;
+  const int rank = p.cn > 1 ? static_cast<int>(clusterRank()) : 0;
   const int row0 = blockIdx.y * R;
   const int rows = min(R, a.batch - row0);
   float* act = sm + p.offAct;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + p.offBar);  // [nchunk0 + layers]
-  const int nbar = p.nchunk0 + a.layers;
+  const int nbar = R + p.cols[0] + a.layers;
 
-  // ---- issue every load of the kernel up front
+  // ---- issue every load of the kernel up front: one bulk copy per operand
+  // row (layer-0 activation rows and weight rows each complete on their own
+  // mbarrier; each later layer's weight slice on one barrier)
+  uint64_t* rowBar = bars;                 // [R]
+  uint64_t* wBar0 = bars + R;              // [cols0]
+  uint64_t* layerBar = bars + R + p.cols[0];  // [layers] (slot 0 unused)
   if (p.bulk) {
     if (tid == 0) {
       for (int b = 0; b < nbar; ++b) mbarInit(&bars[b], 1);
@@ -169,39 +192,25 @@ __global__ void fc_cluster_kernel(const FcChainArgs a, const FcPlan p) {
     __syncthreads();
     if (tid < 32) {
       const int lane = tid;
-      // expected bytes per barrier (one elected lane), then the copies
-      if (lane == 0) {
-        for (int q = 0; q < p.nchunk0; ++q) {
-          int k0 = q * p.kc, len = min(p.kc, a.L[0].kred - k0);
-          int c0 = rank * p.cols[0], nc = max(0, min(p.cols[0], a.L[0].out - c0));
-          mbarExpectTx(&bars[q], (unsigned)(len * 4 * (rows + nc)));
-        }
-        for (int l = 1; l < a.layers; ++l) {
-          int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
-          mbarExpectTx(&bars[p.nchunk0 + l], (unsigned)(a.L[l].kred * 4 * nc));
-        }
-        mbarExpectTx(&bars[p.nchunk0], 0u);  // the layer-0 slot of the per-layer range is unused
+      const int kb0 = a.L[0].kred * 4;
+      const int c00 = rank * p.cols[0], nc0 = max(0, min(p.cols[0], a.L[0].out - c00));
+      // expected bytes first (one lane per barrier), then the copies
+      for (int r = lane; r < R; r += 32) mbarExpectTx(&rowBar[r], r < rows ? kb0 : 0);
+      for (int j = lane; j < p.cols[0]; j += 32) mbarExpectTx(&wBar0[j], j < nc0 ? kb0 : 0);
+      for (int l = lane; l < a.layers; l += 32) {
+        int nc = l == 0 ? 0 : max(0, min(p.cols[l], a.L[l].out - rank * p.cols[l]));
+        mbarExpectTx(&layerBar[l], (unsigned)(a.L[l].kred * 4 * nc));
       }
       __syncwarp();
-      // layer 0: input rows and weight slice, chunked along k
-      {
-        const int c0 = rank * p.cols[0], nc = max(0, min(p.cols[0], a.L[0].out - c0));
-        const int units = p.nchunk0 * (rows + nc);
-        for (int u = lane; u < units; u += 32) {
-          int q = u / (rows + nc), j = u % (rows + nc);
-          int k0 = q * p.kc, len = min(p.kc, a.L[0].kred - k0);
-          if (j < rows)
-            bulkCopy(act + j * p.ald[0] + k0, a.I + (int64_t)(row0 + j) * a.ldi + k0, len * 4, &bars[q]);
-          else
-            bulkCopy(sm + p.offW[0] + (j - rows) * p.wld[0] + k0,
-                     a.L[0].W + (int64_t)(c0 + j - rows) * a.L[0].ldw + k0, len * 4, &bars[q]);
-        }
-      }
+      for (int r = lane; r < rows; r += 32)
+        bulkCopy(act + r * p.ald[0], a.I + (int64_t)(row0 + r) * a.ldi, kb0, &rowBar[r]);
+      for (int j = lane; j < nc0; j += 32)
+        bulkCopy(sm + p.offW[0] + j * p.wld[0], a.L[0].W + (int64_t)(c00 + j) * a.L[0].ldw, kb0, &wBar0[j]);
       for (int l = 1; l < a.layers; ++l) {
         const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
         for (int j = lane; j < nc; j += 32)
           bulkCopy(sm + p.offW[l] + j * p.wld[l], a.L[l].W + (int64_t)(c0 + j) * a.L[l].ldw,
-                   a.L[l].kred * 4, &bars[p.nchunk0 + l]);
+                   a.L[l].kred * 4, &layerBar[l]);
       }
     }
     // rows past the batch end are zero
@@ -240,12 +249,16 @@ __global__ void fc_cluster_kernel(const FcChainArgs a, const FcPlan p) {
       const int r = live ? idx % R : 0, c = live ? idx / R : 0;
       const unsigned xa = actBase + (unsigned)(r * ald) * 4u, wa = wBase + (unsigned)(c * wld) * 4u;
       float acc = live ? __ldg(L.bias + c0 + c) : 0.0f;
-      const int nq = l == 0 ? p.nchunk0 : 1;
-      const int kcl = l == 0 ? p.kc : L.kred;
-      for (int q = 0; q < nq; ++q) {
-        if (p.bulk) mbarWait(&bars[l == 0 ? q : p.nchunk0 + l], 0);
-        acc = chainSegment(xa, wa, q * kcl, min(L.kred, (q + 1) * kcl), acc);
+      if (p.bulk) {
+        if (l == 0) {  // lanes wait on different barriers: reconverge after
+          mbarWait(&rowBar[r], 0, r);
+          mbarWait(&wBar0[c], 0, 100 + c);
+        } else {
+          mbarWait(&layerBar[l], 0, 1000 + l);
+        }
+        __syncwarp();
       }
+      acc = chainSegment(xa, wa, 0, L.kred, acc);
       if (live) {
         float v = fmaxf(acc, 0.0f);
         slice[r * cols + c] = v;
@@ -298,9 +311,9 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p) {
   off += sliceMax;
   off = (off + 3) & ~3;  // 16-byte alignment for the mbarriers
   p.offBar = off;
-  p.kc = 128;
-  p.nchunk0 = (a.L[0].kred + p.kc - 1) / p.kc;
-  off += 2 * (p.nchunk0 + a.layers);  // uint64 each
+  p.kc = a.L[0].kred;
+  p.nchunk0 = 1;
+  off += 2 * (R + p.cols[0] + a.layers);  // uint64 barriers: act rows, weight rows, layers
   bool bulk = (a.ldi % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.I) & 15) == 0);
   for (int l = 0; l < a.layers; ++l)
     bulk = bulk && (a.L[l].kred % 4 == 0) && (a.L[l].ldw % 4 == 0) &&

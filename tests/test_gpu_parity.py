@@ -141,13 +141,21 @@ def test_kru_chunks(engine, oracle, golden, dchunk, threads):
 @pytest.mark.parametrize("th,rf,rw", [(1, 4, 7), (4, 4, 7), (2, 8, 7), (4, 4, 4), (4, 4, 8), (2, 8, 4),
                                       (8, 2, 7), (1, 1, 1)])
 def test_gconv_variants(engine, oracle, golden, th, rf, rw):
+    from paper_1802_04730_b200 import TcError
+    ran = 0
     for name in ["gconv_small", "gconv_paper_n1g2"]:
         case, ins, seeded = case_inputs(oracle, golden, name)
         o = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0, "shared_memory_budget": 49152,
              "thread_shape": [1, 1, 1], "tile_sizes": [th, rf, rw], "unroll_copy_shared": False,
              "unroll_factor": 1, "use_private": False, "use_shared": True}
-        got, _ = run_on_gpu(engine, "gconv", ins, seeded, options=o)
+        try:
+            got, _ = run_on_gpu(engine, "gconv", ins, seeded, options=o)
+        except TcError as e:  # e.g. a CTA over 512 threads: rejected, never run
+            assert e.kind == "MappingInvalid", str(e)
+            continue
+        ran += 1
         assert_exact(oracle, name, "O", got["O"], case["outputs"]["O"]["fnv"])
+    assert ran >= 1
 
 
 def test_kru_full_paper_shape(engine, oracle):
