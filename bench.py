@@ -341,19 +341,18 @@ def main():
         value = world * flops_step * args.steps / el / 1e9
         ms_step = el / args.steps * 1e3
 
-        # ---- per-op device time inside the step (same stream, L2-rotated)
+        # ---- per-op device time inside the step (same stream, L2-rotated):
+        # one graph launches the op on every rotating input set back to back
         per_op = []
         for o in ops:
-            gs = []
-            for i in range(nsets):
-                g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=stream):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(nsets):
                     o.run(i)
-                gs.append(g)
-            for i in range(5):
-                gs[i % nsets].replay()
-            n = max(50, args.steps)
-            t = time_device(torch, lambda i: gs[i % nsets].replay(), n, stream) / n
+            for i in range(3):
+                g.replay()
+            reps = max(4, args.steps // nsets)
+            t = time_device(torch, lambda i: g.replay(), reps, stream) / (reps * nsets)
             per_op.append((o, t))
 
         # ---- e2e: tcb_run with pinned HOST buffers (H2D + kernel + D2H per call)
@@ -455,16 +454,16 @@ def paper_op_table(ee, torch, dev, stream, peaks):
                 for i in range(3):
                     o.run(i)
                 torch.cuda.synchronize()
-                gs = []
-                for i in range(nsets):
-                    g = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(g, stream=stream):
+                # one graph: `per` launches rotating over the input sets
+                per = max(nsets, 8 if big else 32)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for i in range(per):
                         o.run(i)
-                    gs.append(g)
-                for i in range(3):
-                    gs[i % nsets].replay()
-                iters = 20 if name == "gconv" else 200
-                t = time_device(torch, lambda i: gs[i % nsets].replay(), iters, stream) / iters
+                for i in range(2):
+                    g.replay()
+                reps = 3 if name == "gconv" else 10
+                t = time_device(torch, lambda i: g.replay(), reps, stream) / (reps * per)
                 # paper protocol: synchronised single calls incl. launch overhead
                 lat = []
                 for i in range(100 if name == "gconv" else 300):

@@ -8,14 +8,15 @@
 // A cluster of CN CTAs owns R batch rows. Layer l's output features are
 // split across the cluster (CTA c owns columns [c*cols_l, (c+1)*cols_l)),
 // so each CTA streams only its slice of every weight matrix. At kernel
-// start one warp issues EVERY bulk async copy the CTA will need — one
-// cp.async.bulk per row: the R input rows and the weight-slice rows of all
-// layers, completing on mbarriers (one per first-layer operand row, so a
-// thread starts its chain as soon as its two rows landed; one per later
-// layer). After a layer, each CTA publishes its output slice in shared
-// memory, the cluster synchronises, and every CTA gathers the full next-
-// layer input from its peers over DSMEM (mapa + ld.shared::cluster): the
-// activations never touch HBM except as the layer's own return tensor.
+// start warp 0 issues EVERY bulk async copy the CTA will need
+// (cp.async.bulk, global → shared, completing on mbarriers): the R input
+// rows (padded rows, one copy each) and each layer's weight slice (one
+// contiguous copy per layer). Each layer's output value is pushed straight
+// into the next layer's input buffer of every CTA of the cluster (mapa +
+// st.shared::cluster, double-buffered by layer parity), then one cluster
+// barrier (release/acquire) per layer makes the pushes visible: the
+// activations never touch HBM except as the layer's own return tensor, and
+// no CTA ever waits on a remote load.
 //
 // Exactness: each (row, column) output is one thread's sequential FFMA
 // chain in ascending k from bias[o], then fmaxf(·, 0) — the interpreter's
@@ -32,13 +33,12 @@ namespace {
 
 struct FcPlan {
   int cn, R;
-  int cols[kMaxLayers];      // columns per CTA
-  int wld[kMaxLayers];       // padded row stride of the weight slice (floats)
-  int ald[kMaxLayers + 1];   // padded row stride of layer l's input activations
-  int offW[kMaxLayers];      // smem float offsets
-  int offAct, offSlice0, offSlice1, offBar;
-  int kc, nchunk0;           // (unused: first layer loads one copy per row)
-  int bulk;                  // 1: cp.async.bulk path, 0: cooperative loads
+  int cols[kMaxLayers];     // output columns per CTA
+  int ald[kMaxLayers + 1];  // padded row stride of layer l's input activations (floats)
+  int wld[kMaxLayers];      // weight-slice row stride: kred rounded up to 4 (dense when kred%4==0)
+  int offW[kMaxLayers];     // weight slices [cols][wld] (floats)
+  int offAct0, offActA, offActB, offBar;
+  int bulk;                 // 1: cp.async.bulk path, 0: cooperative loads
 };
 
 __host__ __device__ inline int up4(int x) { return (x + 3) & ~3; }
@@ -102,14 +102,6 @@ __device__ __forceinline__ unsigned clusterRank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ float ldCluster(const float* local, unsigned rank) {
-  unsigned remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smemAddr(local)), "r"(rank));
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
-  return v;
-}
-
 __device__ __forceinline__ float4 lds4(unsigned addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -129,163 +121,187 @@ __device__ __forceinline__ float fma4(float4 x, float4 w, float acc) {
   return __fmaf_rn(x.w, w.w, acc);
 }
 
-// acc = chain over k in [k0, k1) of act[k] * w[k]; operands addressed as
-// 32-bit shared-window byte addresses. Three register sets rotate by code
-// position (no moves): the loads of 4-k group g+2 are in flight while the
-// dependent FFMAs of group g run.
-__device__ __forceinline__ float chainSegment(unsigned xa, unsigned wa, int k0, int k1, float acc) {
-  const int ng = (k1 - k0) >> 2;
-  const unsigned x0 = xa + k0 * 4, w0 = wa + k0 * 4;
-  float4 xA, wA, xB, wB, xC, wC;
-  if (ng > 0) {
-    xA = lds4(x0);
-    wA = lds4(w0);
+__device__ __forceinline__ void stCluster(float* local, unsigned rank, float v) {
+  unsigned remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smemAddr(local)), "r"(rank));
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+}
+
+// acc = chain over k in [0, n) of x[k] * w[k]; operands addressed as 32-bit
+// shared-window byte addresses. Double-buffered 16-wide chunks: the eight
+// vector loads of chunk c+1 are issued before the 16 dependent FFMAs of
+// chunk c, so shared-load latency hides behind a full chunk of the chain.
+// Reads up to 32 floats past n (the plan leaves that slack after every
+// operand buffer).
+__device__ __forceinline__ float chainSegment(unsigned xa, unsigned wa, int n, float acc) {
+  const int nch = n >> 4;
+  float4 X0[4], W0[4], X1[4], W1[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    X0[i] = lds4(xa + i * 16);
+    W0[i] = lds4(wa + i * 16);
   }
-  if (ng > 1) {
-    xB = lds4(x0 + 16);
-    wB = lds4(w0 + 16);
-  }
-  int g = 0;
-  for (; g + 3 <= ng; g += 3) {
-    const unsigned o = g * 16;
-    xC = lds4(x0 + o + 32);
-    wC = lds4(w0 + o + 32);
-    acc = fma4(xA, wA, acc);
-    if (g + 3 < ng) {
-      xA = lds4(x0 + o + 48);
-      wA = lds4(w0 + o + 48);
+  int c = 0;
+  for (; c + 2 <= nch; c += 2) {
+    const unsigned o = c * 64;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      X1[i] = lds4(xa + o + 64 + i * 16);
+      W1[i] = lds4(wa + o + 64 + i * 16);
     }
-    acc = fma4(xB, wB, acc);
-    if (g + 4 < ng) {
-      xB = lds4(x0 + o + 64);
-      wB = lds4(w0 + o + 64);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc = fma4(X0[i], W0[i], acc);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      X0[i] = lds4(xa + o + 128 + i * 16);
+      W0[i] = lds4(wa + o + 128 + i * 16);
     }
-    acc = fma4(xC, wC, acc);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc = fma4(X1[i], W1[i], acc);
   }
-  if (g < ng) acc = fma4(xA, wA, acc);
-  if (g + 1 < ng) acc = fma4(xB, wB, acc);
-  for (int kk = k0 + 4 * ng; kk < k1; ++kk) acc = __fmaf_rn(lds1(xa + kk * 4), lds1(wa + kk * 4), acc);
+  if (c < nch) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc = fma4(X0[i], W0[i], acc);
+    ++c;
+  }
+  int kk = c * 16;
+  for (; kk + 4 <= n; kk += 4) acc = fma4(lds4(xa + kk * 4), lds4(wa + kk * 4), acc);
+  for (; kk < n; ++kk) acc = __fmaf_rn(lds1(xa + kk * 4), lds1(wa + kk * 4), acc);
   return acc;
 }
 
-__global__ void fc_cluster_kernel(const FcChainArgs a, const FcPlan p) {
+#ifdef TCB_FC_TRACE
+// diagnostic build only (profiles/fc_trace.cu): per-CTA phase timestamps
+__device__ unsigned long long g_fc_trace[1024][16];
+#define FC_STAMP(ev)                                                                       \
+  do {                                                                                     \
+    if (threadIdx.x == 0) g_fc_trace[blockIdx.y * gridDim.x + blockIdx.x][ev] = clock64(); \
+  } while (0)
+#define FC_GSTAMP(ev)                                                                  \
+  do {                                                                                 \
+    unsigned long long t_;                                                             \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+    if (threadIdx.x == 0) g_fc_trace[blockIdx.y * gridDim.x + blockIdx.x][ev] = t_;    \
+  } while (0)
+#else
+#define FC_STAMP(ev) \
+  do {               \
+  } while (0)
+#define FC_GSTAMP(ev) \
+  do {                \
+  } while (0)
+#endif
+
+__global__ void __launch_bounds__(1024) fc_cluster_kernel(const FcChainArgs a, const FcPlan p) {
+  FC_GSTAMP(13);
+  FC_STAMP(0);
   extern __shared__ __align__(128) float sm[];
   const int tid = threadIdx.x, T = blockDim.x, R = p.R;
   const int rank = p.cn > 1 ? static_cast<int>(clusterRank()) : 0;
   const int row0 = blockIdx.y * R;
   const int rows = min(R, a.batch - row0);
-  float* act = sm + p.offAct;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + p.offBar);  // [nchunk0 + layers]
-  const int nbar = R + p.cols[0] + a.layers;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + p.offBar);  // [0]: input rows, [1+l]: layer l weights
 
-  // ---- issue every load of the kernel up front: one bulk copy per operand
-  // row (layer-0 activation rows and weight rows each complete on their own
-  // mbarrier; each later layer's weight slice on one barrier)
-  uint64_t* rowBar = bars;                 // [R]
-  uint64_t* wBar0 = bars + R;              // [cols0]
-  uint64_t* layerBar = bars + R + p.cols[0];  // [layers] (slot 0 unused)
+  // ---- every load of the kernel is issued up front by warp 0
   if (p.bulk) {
-    if (tid == 0) {
-      for (int b = 0; b < nbar; ++b) mbarInit(&bars[b], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
     if (tid < 32) {
+      for (int b = tid; b <= a.layers; b += 32) mbarInit(&bars[b], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      __syncwarp();
       const int lane = tid;
-      const int kb0 = a.L[0].kred * 4;
-      const int c00 = rank * p.cols[0], nc0 = max(0, min(p.cols[0], a.L[0].out - c00));
-      // expected bytes first (one lane per barrier), then the copies
-      for (int r = lane; r < R; r += 32) mbarExpectTx(&rowBar[r], r < rows ? kb0 : 0);
-      for (int j = lane; j < p.cols[0]; j += 32) mbarExpectTx(&wBar0[j], j < nc0 ? kb0 : 0);
+      const unsigned rowBytes = (unsigned)a.L[0].kred * 4u;
+      if (lane == 0) mbarExpectTx(&bars[0], rowBytes * rows);
       for (int l = lane; l < a.layers; l += 32) {
-        int nc = l == 0 ? 0 : max(0, min(p.cols[l], a.L[l].out - rank * p.cols[l]));
-        mbarExpectTx(&layerBar[l], (unsigned)(a.L[l].kred * 4 * nc));
+        const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
+        mbarExpectTx(&bars[1 + l], (unsigned)(a.L[l].kred * 4 * nc));
       }
       __syncwarp();
       for (int r = lane; r < rows; r += 32)
-        bulkCopy(act + r * p.ald[0], a.I + (int64_t)(row0 + r) * a.ldi, kb0, &rowBar[r]);
-      for (int j = lane; j < nc0; j += 32)
-        bulkCopy(sm + p.offW[0] + j * p.wld[0], a.L[0].W + (int64_t)(c00 + j) * a.L[0].ldw, kb0, &wBar0[j]);
-      for (int l = 1; l < a.layers; ++l) {
+        bulkCopy(sm + p.offAct0 + r * p.ald[0], a.I + (int64_t)(row0 + r) * a.ldi, rowBytes, &bars[0]);
+      for (int l = 0; l < a.layers; ++l) {
         const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
-        for (int j = lane; j < nc; j += 32)
-          bulkCopy(sm + p.offW[l] + j * p.wld[l], a.L[l].W + (int64_t)(c0 + j) * a.L[l].ldw,
-                   a.L[l].kred * 4, &layerBar[l]);
+        if (nc == 0) continue;
+        const float* src = a.L[l].W + (int64_t)c0 * a.L[l].ldw;
+        if (a.L[l].ldw == a.L[l].kred) {  // the slice is one contiguous block
+          if (lane == (l + rows) % 32) bulkCopy(sm + p.offW[l], src, (unsigned)(nc * a.L[l].kred * 4), &bars[1 + l]);
+        } else {
+          for (int j = lane; j < nc; j += 32)
+            bulkCopy(sm + p.offW[l] + j * p.wld[l], src + (int64_t)j * a.L[l].ldw, a.L[l].kred * 4, &bars[1 + l]);
+        }
       }
     }
-    // rows past the batch end are zero
-    for (int e = tid; e < (R - rows) * p.ald[0]; e += T) act[rows * p.ald[0] + e] = 0.0f;
-    __syncthreads();
+    // input rows past the batch end are zero
+    for (int e = tid; e < (R - rows) * p.ald[0]; e += T) sm[p.offAct0 + rows * p.ald[0] + e] = 0.0f;
+    __syncthreads();  // barrier inits visible to every thread
   } else {
     for (int e = tid; e < R * p.ald[0]; e += T) {
       int r = e / p.ald[0], kk = e % p.ald[0];
-      act[e] = (r < rows && kk < a.L[0].kred) ? a.I[(int64_t)(row0 + r) * a.ldi + kk] : 0.0f;
+      sm[p.offAct0 + e] = (r < rows && kk < a.L[0].kred) ? a.I[(int64_t)(row0 + r) * a.ldi + kk] : 0.0f;
     }
     for (int l = 0; l < a.layers; ++l) {
       const int c0 = rank * p.cols[l];
-      for (int e = tid; e < p.cols[l] * a.L[l].kred; e += T) {
-        int j = e / a.L[l].kred, kk = e % a.L[l].kred;
-        sm[p.offW[l] + j * p.wld[l] + kk] =
-            (c0 + j < a.L[l].out) ? a.L[l].W[(int64_t)(c0 + j) * a.L[l].ldw + kk] : 0.0f;
+      for (int e = tid; e < p.cols[l] * p.wld[l]; e += T) {
+        int j = e / p.wld[l], kk = e % p.wld[l];
+        sm[p.offW[l] + e] =
+            (c0 + j < a.L[l].out && kk < a.L[l].kred) ? a.L[l].W[(int64_t)(c0 + j) * a.L[l].ldw + kk] : 0.0f;
       }
     }
     __syncthreads();
   }
+  FC_STAMP(2);
 
 #pragma unroll 1
   for (int l = 0; l < a.layers; ++l) {
     const FcLayer L = a.L[l];
     const int cols = p.cols[l], c0 = rank * cols;
-    const float* W = sm + p.offW[l];
-    const int wld = p.wld[l], ald = p.ald[l];
-    float* slice = sm + ((l & 1) ? p.offSlice1 : p.offSlice0);  // [R][cols]
-    const unsigned actBase = smemAddr(act), wBase = smemAddr(W);
+    const bool last = l + 1 == a.layers;
+    // layer l reads buffer in(l), writes buffer in(l+1) in every cluster CTA
+    const int inOff = l == 0 ? p.offAct0 : ((l & 1) ? p.offActA : p.offActB);
+    const int outOff = (l & 1) ? p.offActB : p.offActA;
+    const int ald = p.ald[l], ldn = p.ald[l + 1];
+    const unsigned actBase = smemAddr(sm + inOff), wBase = smemAddr(sm + p.offW[l]);
+    if (p.bulk) {
+      if (l == 0) mbarWait(&bars[0], 0, 0);
+      mbarWait(&bars[1 + l], 0, 1 + l);
+    }
+    FC_STAMP(3 + 3 * l);
     const int nchains = R * cols;
     for (int base = 0; base < nchains; base += T) {
-      // one (row, column) chain per thread and pass; idle lanes run a dummy
-      // chain on row 0 / column 0 (no branches inside the reduction)
+      // one (row, column) chain per thread and pass, row fastest; idle
+      // lanes run a dummy chain on row 0 / column 0 (no branch in the chain)
       const int idx = base + tid;
       const bool live = idx < nchains && c0 + idx / R < L.out;
       const int r = live ? idx % R : 0, c = live ? idx / R : 0;
-      const unsigned xa = actBase + (unsigned)(r * ald) * 4u, wa = wBase + (unsigned)(c * wld) * 4u;
       float acc = live ? __ldg(L.bias + c0 + c) : 0.0f;
-      if (p.bulk) {
-        if (l == 0) {  // lanes wait on different barriers: reconverge after
-          mbarWait(&rowBar[r], 0, r);
-          mbarWait(&wBar0[c], 0, 100 + c);
-        } else {
-          mbarWait(&layerBar[l], 0, 1000 + l);
-        }
-        __syncwarp();
-      }
-      acc = chainSegment(xa, wa, 0, L.kred, acc);
+      acc = chainSegment(actBase + (unsigned)(r * ald) * 4u, wBase + (unsigned)(c * p.wld[l]) * 4u, L.kred, acc);
       if (live) {
-        float v = fmaxf(acc, 0.0f);
-        slice[r * cols + c] = v;
+        const float v = fmaxf(acc, 0.0f);
         if (r < rows) L.O[(int64_t)(row0 + r) * L.out + c0 + c] = v;
+        if (!last) {  // push into the next layer's input of every cluster CTA
+          float* dst = sm + outOff + r * ldn + c0 + c;
+          if (p.cn > 1) {
+            for (int q = 0; q < p.cn; ++q) stCluster(dst, q, v);
+          } else {
+            *dst = v;
+          }
+        }
       }
     }
-    if (l + 1 < a.layers) {
-      // publish the slice to the cluster, then gather the next layer's input
-      if (p.cn > 1) clusterSync();
+    FC_STAMP(4 + 3 * l);
+    if (!last) {
+      if (p.cn > 1) clusterSync();  // release/acquire: every peer's pushes landed
       else __syncthreads();
-      const int ldn = p.ald[l + 1];
-      for (int e = tid; e < R * L.out; e += T) {
-        int r = e / L.out, col = e % L.out;
-        int owner = col / cols, c = col % cols;
-        const float* src = slice + r * cols + c;
-        act[r * ldn + col] = p.cn > 1 ? ldCluster(src, owner) : *src;
-      }
-      __syncthreads();
+      FC_STAMP(5 + 3 * l);
     }
   }
-  // keep this CTA's shared memory alive until every peer finished its DSMEM reads
-  if (p.cn > 1 && a.layers > 1) clusterSync();
+  FC_STAMP(15);
+  FC_GSTAMP(14);
 }
 
 }  // namespace
 
-// Builds the plan; returns the dynamic shared-memory size (0 if infeasible).
+// Builds the plan; returns the dynamic shared-memory size. Every operand
+// buffer is followed by >= 32 floats of slack (the chain prefetches ahead).
 static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p) {
   p = FcPlan{};
   p.cn = cn;
@@ -293,27 +309,22 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p) {
   int off = 0;
   for (int l = 0; l < a.layers; ++l) {
     p.cols[l] = (a.L[l].out + cn - 1) / cn;
-    p.wld[l] = padRow(a.L[l].kred);
+    p.wld[l] = up4(a.L[l].kred);
     p.offW[l] = off;
-    off += p.cols[l] * p.wld[l];
+    off += p.cols[l] * p.wld[l] + 32;
   }
+  for (int l = 0; l <= a.layers; ++l) p.ald[l] = padRow(l < a.layers ? a.L[l].kred : a.L[l - 1].out);
   int aldMax = 0;
-  p.ald[0] = padRow(a.L[0].kred);
-  for (int l = 1; l < a.layers; ++l) p.ald[l] = padRow(a.L[l].kred);
-  for (int l = 0; l < a.layers; ++l) aldMax = p.ald[l] > aldMax ? p.ald[l] : aldMax;
-  p.offAct = off;
-  off += R * aldMax;
-  int sliceMax = 0;
-  for (int l = 0; l < a.layers; ++l) sliceMax = R * p.cols[l] > sliceMax ? R * p.cols[l] : sliceMax;
-  p.offSlice0 = off;
-  off += sliceMax;
-  p.offSlice1 = off;
-  off += sliceMax;
+  for (int l = 1; l <= a.layers; ++l) aldMax = p.ald[l] > aldMax ? p.ald[l] : aldMax;
+  p.offAct0 = off;
+  off += R * p.ald[0] + 32;
+  p.offActA = off;
+  off += R * aldMax + 32;
+  p.offActB = off;
+  off += R * aldMax + 32;
   off = (off + 3) & ~3;  // 16-byte alignment for the mbarriers
   p.offBar = off;
-  p.kc = a.L[0].kred;
-  p.nchunk0 = 1;
-  off += 2 * (R + p.cols[0] + a.layers);  // uint64 barriers: act rows, weight rows, layers
+  off += 2 * (1 + a.layers);  // uint64 barriers
   bool bulk = (a.ldi % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.I) & 15) == 0);
   for (int l = 0; l < a.layers; ++l)
     bulk = bulk && (a.L[l].kred % 4 == 0) && (a.L[l].ldw % 4 == 0) &&
@@ -336,7 +347,7 @@ int fcChainThreads(const FcChainArgs& a, int rows, int cn) {
   // block size that runs every layer in one pass (any multiple of 32 works;
   // smaller blocks take several passes)
   int t = ((need + 31) / 32) * 32;
-  return t > 1024 ? 1024 : t;
+  return t > 1024 ? 1024 : (t < 32 ? 32 : t);
 }
 
 cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s) {

@@ -393,15 +393,17 @@ MappingOptions defaultOptions(const Problem& p) {
       int outMax = 0;
       for (const auto& L : p.fc.layers) outMax = std::max(outMax, L.out);
       int cn = std::min(8, std::max(1, (outMax + 15) / 16));
+      // aim at ~2 co-resident CTAs per SM (>= 200 CTAs): a wave of 1-CTA/SM
+      // 8-clusters does not fit the GPCs (max 15 active of 16 on B200)
       int rows = 1;
-      while (rows < 16 && (int64_t)((p.fc.batch + rows * 2 - 1) / (rows * 2)) * cn >= 128) rows *= 2;
+      while (rows < 16 && (int64_t)((p.fc.batch + rows * 2 - 1) / (rows * 2)) * cn >= 200) rows *= 2;
       k::FcChainArgs a{};
       a.layers = static_cast<int>(p.fc.layers.size());
       for (int l = 0; l < a.layers; ++l) {
         a.L[l].out = p.fc.layers[l].out;
         a.L[l].kred = p.fc.layers[l].kred;
       }
-      while (rows > 1 && k::fcChainSmem(a, rows, cn) > 200 * 1024) rows /= 2;
+      while (rows > 1 && k::fcChainSmem(a, rows, cn) > 110 * 1024) rows /= 2;
       int t = std::max(64, k::fcChainThreads(a, rows, cn));  // one pass per layer
       o.tileSizes = {rows, cn, 1};
       o.threadShape = {{t, 1, 1}};

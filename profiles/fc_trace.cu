@@ -1,0 +1,109 @@
+// fc_trace.cu — diagnostic harness: builds the FC-chain kernel with phase
+// timestamps (TCB_FC_TRACE) and prints per-phase cycle offsets from kernel
+// entry (median / max over CTAs) for the paper shapes. Build + run:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DTCB_FC_TRACE \
+//        -I paper_1802_04730_b200/csrc profiles/fc_trace.cu -o profiles/fc_trace && profiles/fc_trace
+#include "kernels/fc_chain.cu"
+
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+using namespace tcb::k;
+
+static void run(const char* label, FcChainArgs a, int rows, int cn, int threads) {
+  static unsigned long long z[1024][16];
+  {
+    FcPlan pl;
+    size_t smem = planFc(a, rows, cn, pl);
+    cudaFuncSetAttribute(fc_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cn > 8) cudaFuncSetAttribute(fc_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cn, (a.batch + rows - 1) / rows, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cn;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nc = -1;
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nc, fc_cluster_kernel, &cfg);
+    printf("[%s] smem %zu B, grid %d clusters, max active clusters %d (%s)\n", label, smem,
+           (a.batch + rows - 1) / rows, nc, cudaGetErrorString(e));
+  }
+  for (int it = 0; it < 3; ++it) launchFcChain(a, rows, cn, threads, 0);
+  cudaDeviceSynchronize();
+  cudaMemcpyToSymbol(g_fc_trace, z, sizeof(z));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  launchFcChain(a, rows, cn, threads, 0);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaDeviceSynchronize();
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  static unsigned long long tr[1024][16];
+  cudaMemcpyFromSymbol(tr, g_fc_trace, sizeof(tr));
+  int nblk = cn * ((a.batch + rows - 1) / rows);
+  printf("%s: %s  %.2f us  (%d CTAs)\n", label, cudaGetErrorString(err), ms * 1e3, nblk);
+  const char* names[16] = {"start", "-", "copies_issued", "L0_data", "L0_done", "L0_csync", "L1_data",
+                           "L1_done", "L1_csync", "L2_data", "L2_done", "L2_csync", "-", "-", "-", "end"};
+  unsigned long long g0 = ~0ull, g1 = 0;
+  for (int b = 0; b < nblk; ++b) {
+    if (tr[b][13]) g0 = std::min(g0, tr[b][13]);
+    g1 = std::max(g1, tr[b][14]);
+  }
+  std::vector<long long> st;
+  for (int b = 0; b < nblk; ++b) st.push_back((long long)(tr[b][13] - g0));
+  std::sort(st.begin(), st.end());
+  printf("  globaltimer: first CTA start -> last CTA end %.2f us; CTA start skew median %lld max %lld ns\n",
+         (g1 - g0) * 1e-3, st[st.size() / 2], st.back());
+  for (int ev = 1; ev < 13; ++ev) {
+    std::vector<long long> d;
+    for (int b = 0; b < nblk; ++b)
+      if (tr[b][ev] && tr[b][0]) d.push_back((long long)(tr[b][ev] - tr[b][0]));
+    if (d.empty()) continue;
+    std::sort(d.begin(), d.end());
+    printf("  %-13s median %7lld  max %7lld cycles\n", names[ev], d[d.size() / 2], d.back());
+  }
+}
+
+int main() {
+  auto alloc = [](size_t n) {
+    float* p;
+    cudaMalloc(&p, n * 4);
+    cudaMemset(p, 0, n * 4);
+    return p;
+  };
+  FcChainArgs f{};
+  f.I = alloc(128 * 1128);
+  f.ldi = 1128;
+  f.batch = 128;
+  f.layers = 2;
+  f.L[0] = {alloc(128 * 1128), alloc(128), alloc(128 * 128), 128, 1128, 1128};
+  f.L[1] = {alloc(64 * 128), alloc(64), alloc(128 * 64), 64, 128, 128};
+  run("2FCRelu rows=8 cn=8", f, 8, 8, 128);
+  FcChainArgs one = f;
+  one.layers = 1;
+  run("MLP1 rows=8 cn=8", one, 8, 8, 128);
+  FcChainArgs m{};
+  m.I = alloc(128 * 128);
+  m.ldi = 128;
+  m.batch = 128;
+  m.layers = 3;
+  m.L[0] = {alloc(64 * 128), alloc(64), alloc(128 * 64), 64, 128, 128};
+  m.L[1] = {alloc(32 * 64), alloc(32), alloc(128 * 32), 32, 64, 64};
+  m.L[2] = {alloc(2 * 32), alloc(2), alloc(128 * 2), 2, 32, 32};
+  run("MLP3 rows=4 cn=4", m, 4, 4, 64);
+  run("MLP3 rows=8 cn=2", m, 8, 2, 128);
+  run("MLP3 rows=4 cn=1", m, 4, 1, 64);
+  run("2FCRelu rows=8 cn=4", f, 8, 4, 256);
+  run("2FCRelu rows=4 cn=8", f, 4, 8, 64);
+  run("2FCRelu rows=8 cn=16", f, 8, 16, 64);
+  run("2FCRelu rows=16 cn=8", f, 16, 8, 256);
+  return 0;
+}
