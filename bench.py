@@ -20,7 +20,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -32,6 +31,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "µs/call and GFLOP/s per TC op at paper shapes (1/2/4/8 B200) vs roofline & CPU ref"
 L2_BYTES = 126 * 1024 * 1024
+STEP_WORKLOAD = "TBMM(B=500,N=26,M=72,K=26) + 2FCRelu(B=128,1128->128->64) + MLP3(B=128,128->64->32->2) per step"
 
 # (def, parameter shapes, seeded return shapes) — BASELINE.md §2
 STEP_OPS = [
@@ -68,59 +68,68 @@ def load_peaks():
 
 # --------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled DURING the timed
+    region through NVML (a polling thread, ~1 ms period: the timed region is
+    tens of ms, too short for `nvidia-smi -lms`)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
 
-    def __init__(self, dev):
-        self.dev = dev
-        self.p = None
-        self.lines = []
+    def __init__(self, torch_dev):
+        self.samples, self.max_mhz, self.reasons = [], None, set()
+        self.h = None
+        self.err = None
+        try:
+            import pynvml as N
+            import torch
+            N.nvmlInit()
+            self.N = N
+            pr = torch.cuda.get_device_properties(torch_dev)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            try:
+                self.h = N.nvmlDeviceGetHandleByPciBusId_v2(bus.encode())
+            except Exception:
+                self.h = N.nvmlDeviceGetHandleByIndex(torch_dev.index or 0)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception as e:  # recorded, not hidden
+            self.err = f"{type(e).__name__}: {e}"
+
+    def _poll(self):
+        N = self.N
+        while not self.stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, const in self.REASONS:
+                    if r & getattr(N, const, 0):
+                        self.reasons.add(name)
+            except Exception as e:
+                self.err = f"{type(e).__name__}: {e}"
+                return
+            self.stop.wait(0.001)
 
     def __enter__(self):
-        try:
-            self.p = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        self.stop = threading.Event()
+        if self.h is not None:
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-        except Exception:
-            self.p = None
         return self
 
-    def _read(self):
-        for line in self.p.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.p:
-            self.p.terminate()
-            try:
-                self.p.wait(timeout=5)
-            except Exception:
-                self.p.kill()
+        self.stop.set()
+        if self.h is not None:
+            self.t.join(timeout=5)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 6:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[2:6]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+               "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+               "samples": len(self.samples), "source": "nvml, polled during the timed region"}
+        if self.err:
+            out["error"] = self.err
+        return out
 
 
 # ------------------------------------------------------------- workload
@@ -177,86 +186,141 @@ def time_device(torch, fn, iters, stream):
 
 
 # ----------------------------------------------------------- CPU baseline
-def cpu_reference_sample(threads=None, scale=16):
-    """The reference's own CPU implementation of the path — the interpreter
-    backend::interpretReference of the reference library (oracle/_ref, built
-    from /root/reference) — on a bounded sample of the step: 1/scale of
-    every batch, rows split across host threads (reentrant per
-    interpreter.h:78). Falls back to the C restatement (OpenMP) when the
-    reference build is absent. Returns (GFLOP/s, seconds, info dict)."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import concurrent.futures as cf
+class CpuStep:
+    """The reference's own CPU implementation of the step — the interpreter
+    backend::interpretReference (interpreter.cc:301-349) of the reference
+    library compiled by oracle/Makefile (oracle/_ref) — over the step's work
+    units: one TBMM batch (tbmm.tc), one 2FCRelu row, one MLP3 row, each a
+    call of the reference through its public entry (parse + specialize +
+    interpret). Units run on all host threads (the interpreter is reentrant,
+    interpreter.h:78). A sample = the next `n` units of the step in
+    round-robin order, so any number of samples covers the workload evenly.
+    Without oracle/_ref, the C restatement (OpenMP) is timed instead
+    ("port"). Test/bench infrastructure only."""
 
-    from oracle_lib import Oracle, RefLib
+    def __init__(self, threads=None):
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from oracle_lib import Oracle, RefLib
 
-    orc = Oracle()
-    src = open(os.path.join(ROOT, "paper_1802_04730_b200", "tc", "ops.tc")).read()
-    rng = orc.rng(7)
-    tb = 500 // scale  # TBMM batches
-    fb = max(1, 128 // scale)  # FC rows
-    X, Y = rng.f32((tb, 26, 72)), rng.f32((tb, 26, 72))
-    I, W1, B1 = rng.f32((fb, 1128)), rng.f32((128, 1128)), rng.f32((128,))
-    W2, B2 = rng.f32((64, 128)), rng.f32((64,))
-    O1 = rng.f32((fb, 128))
-    M2, C2, M3, C3b, M4, C4 = (rng.f32((64, 128)), rng.f32((64,)), rng.f32((32, 64)), rng.f32((32,)),
-                               rng.f32((2, 32)), rng.f32((2,)))
-    flops = 2.0 * tb * 26 * 26 * 72 + 2.0 * fb * (128 * 1128 + 64 * 128) + 2.0 * fb * (
-        64 * 128 + 32 * 64 + 2 * 32)
-    threads = threads or os.cpu_count() or 1
-    if RefLib.available():
-        ref = RefLib()
-        jobs = []
-        for b in range(tb):
-            jobs.append(("tbmm", {"X": X[b:b + 1], "Y": Y[b:b + 1]}, ["Z"]))
-        for r in range(fb):
-            jobs.append(("2FCRelu", {"I": I[r:r + 1], "W1": W1, "B1": B1, "W2": W2, "B2": B2}, ["O1", "O2"]))
-            jobs.append(("MLP3", {"I": O1[r:r + 1], "W2": M2, "B2": C2, "W3": M3, "B3": C3b, "W4": M4,
-                                  "B4": C4, "O1": O1[r:r + 1]}, ["O2", "O3", "O4"]))
+        self.threads = threads or os.cpu_count() or 1
+        orc = Oracle()
+        rng = orc.rng(7)
+        self.X, self.Y = rng.f32((500, 26, 72)), rng.f32((500, 26, 72))
+        self.I, self.W1, self.B1 = rng.f32((128, 1128)), rng.f32((128, 1128)), rng.f32((128,))
+        self.W2, self.B2 = rng.f32((64, 128)), rng.f32((64,))
+        self.O1 = rng.f32((128, 128))
+        self.M = [rng.f32((64, 128)), rng.f32((64,)), rng.f32((32, 64)), rng.f32((32,)),
+                  rng.f32((2, 32)), rng.f32((2,))]
+        self.units = [("tbmm", b) for b in range(500)]
+        for r in range(128):
+            self.units += [("2FCRelu", r), ("MLP3", r)]
+        # interleave so any contiguous window mixes the three ops like the step
+        self.units.sort(key=lambda u: (u[1] / (500 if u[0] == "tbmm" else 128), u[0]))
+        self.flops = {"tbmm": 2.0 * 26 * 26 * 72, "2FCRelu": 2.0 * (128 * 1128 + 64 * 128),
+                      "MLP3": 2.0 * (64 * 128 + 32 * 64 + 2 * 32)}
+        self.cursor = 0
+        self.orc = orc
+        if RefLib.available():
+            self.ref = RefLib()
+            self.src = open(os.path.join(ROOT, "paper_1802_04730_b200", "tc", "ops.tc")).read()
+            self.kind = "reference"
+        else:
+            self.ref = None
+            self.kind = "port"
+            orc.lib.orc_set_threads(self.threads)
+
+    def _run_unit(self, u):
+        op, i = u
+        if op == "tbmm":
+            self.ref.run(self.src, "tbmm", {"X": self.X[i:i + 1], "Y": self.Y[i:i + 1]}, ["Z"])
+        elif op == "2FCRelu":
+            self.ref.run(self.src, "2FCRelu", {"I": self.I[i:i + 1], "W1": self.W1, "B1": self.B1,
+                                               "W2": self.W2, "B2": self.B2}, ["O1", "O2"])
+        else:
+            m = self.M
+            self.ref.run(self.src, "MLP3", {"I": self.O1[i:i + 1], "W2": m[0], "B2": m[1], "W3": m[2],
+                                            "B3": m[3], "W4": m[4], "B4": m[5], "O1": self.O1[i:i + 1]},
+                         ["O2", "O3", "O4"])
+
+    def _port(self, us):
+        tb = [i for op, i in us if op == "tbmm"]
+        fc = [i for op, i in us if op == "2FCRelu"]
+        ml = [i for op, i in us if op == "MLP3"]
+        if tb:
+            self.orc.tbmm(self.X[tb], self.Y[tb])
+        if fc:
+            self.orc.fc_relu(self.orc.fc_relu(self.I[fc], self.W1, self.B1), self.W2, self.B2)
+        if ml:
+            m = self.M
+            self.orc.mlp3(self.O1[ml], *m)
+
+    def sample(self, n):
+        """Run the next n units; returns (flops, seconds)."""
+        import concurrent.futures as cf
+        n = max(1, min(n, len(self.units)))
+        us = [self.units[(self.cursor + k) % len(self.units)] for k in range(n)]
+        self.cursor = (self.cursor + n) % len(self.units)
         t0 = time.perf_counter()
-        with cf.ThreadPoolExecutor(threads) as ex:
-            list(ex.map(lambda j: ref.run(src, j[0], j[1], j[2]), jobs))
+        if self.ref is not None:
+            with cf.ThreadPoolExecutor(self.threads) as ex:
+                list(ex.map(self._run_unit, us))
+        else:
+            self._port(us)
         dt = time.perf_counter() - t0
-        kind = "reference"
-    else:
-        orc.lib.orc_set_threads(threads)
-        t0 = time.perf_counter()
-        orc.tbmm(X, Y)
-        o1 = orc.fc_relu(I, W1, B1)
-        orc.fc_relu(o1, W2, B2)
-        orc.mlp3(O1, M2, C2, M3, C3b, M4, C4)
-        dt = time.perf_counter() - t0
-        kind = "port"
-    info = {"kind": kind, "cores": threads,
-            "sample": f"1/{scale} of the step's batches: TBMM B={tb}, 2FCRelu B={fb}, MLP3 B={fb} "
-                      f"({flops / 1e6:.2f} MFLOP)"}
-    return flops / dt / 1e9, dt, info
+        return sum(self.flops[op] for op, _ in us), dt
+
+    def units_for(self, seconds):
+        """Units that take about `seconds` on all threads (calibrated)."""
+        f, dt = self.sample(2 * self.threads)
+        per = dt / (2 * self.threads)
+        return max(1, int(seconds / per))
+
+    def describe(self, n):
+        return (f"{n} work units per sample (of the step's 756: 500 TBMM batches, 128 2FCRelu rows, "
+                f"128 MLP3 rows), round-robin over the step, each a {self.kind} call")
+
+
+def cpu_baseline(budget_s=15.0):
+    """bench.py's cpu_baseline leg: ~budget_s of the reference's CPU path."""
+    cs = CpuStep()
+    n = cs.units_for(budget_s / 4)
+    fl = tt = 0.0
+    while tt < budget_s:
+        f, dt = cs.sample(n)
+        fl, tt = fl + f, tt + dt
+    return fl / tt / 1e9, {"kind": cs.kind, "cores": cs.threads,
+                           "sample": cs.describe(n) + f"; {tt:.1f} s timed"}
 
 
 def reference_arm(args, rank, world):
+    """--impl reference: the reference's own CPU implementation on the host
+    cores, same metric/config; each step a bounded sample sized so the whole
+    --steps/--warmup run takes about two minutes. Rank 0 only."""
     if rank != 0:
         return
-    scale = 16
+    cs = CpuStep()
+    per_step = min(10.0, 120.0 / (args.steps + args.warmup))
+    n = cs.units_for(per_step)
     for _ in range(args.warmup):
-        cpu_reference_sample(scale=scale)
-    vals, times = [], []
-    info = None
+        cs.sample(n)
+    fl = tt = 0.0
     for _ in range(args.steps):
-        v, dt, info = cpu_reference_sample(scale=scale)
-        vals.append(v)
-        times.append(dt)
-    value = statistics.median(vals)
+        f, dt = cs.sample(n)
+        fl, tt = fl + f, tt + dt
+    value = fl / tt / 1e9
+    step_flops = 500 * cs.flops["tbmm"] + 128 * (cs.flops["2FCRelu"] + cs.flops["MLP3"])
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GFLOP/s",
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(statistics.median(times) * 1e3 * scale, 3),
+        "ms_per_step": round(step_flops / (value * 1e9) * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
-        "config": {"workload": "TBMM(B=500,N=26,M=72,K=26) + 2FCRelu(B=128,1128->128->64) + "
-                               "MLP3(B=128,128->64->32->2) per step", "parallelism": f"dp{args.gpus}",
-                   "note": "reference CPU interpreter on a bounded 1/16 sample per step; ms_per_step "
-                           "extrapolated to the full step"},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GFLOP/s", **info},
-        "e2e": {"value": round(value, 4), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "data": "synthetic (U[-1,1) fp32, seeded)",
+        "config": {"workload": STEP_WORKLOAD, "parallelism": f"dp{args.gpus}",
+                   "note": "reference CPU interpreter on a bounded sample per step; ms_per_step is "
+                           "the full step's FLOPs at the measured rate"},
+        "cpu_baseline": {"value": round(value, 6), "unit": "GFLOP/s", "kind": cs.kind, "cores": cs.threads,
+                         "sample": cs.describe(n)},
+        "e2e": {"value": round(value, 6), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -265,8 +329,8 @@ def reference_arm(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="tcb", choices=["tcb", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ops", action="store_true", help="skip the per-op paper table")
@@ -283,13 +347,15 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1802_04730_b200 import ExecutionEngine, device_info
+    from paper_1802_04730_b200 import ExecutionEngine, device_info, measure_peaks
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     peaks, peak_src = load_peaks()
+    peaks = dict(peaks)
+    peaks["ffma_tflops"] = round(measure_peaks(local)["ffma_tflops"], 2)  # measured now, this GPU
     ee = ExecutionEngine()
 
     # rotating input sets larger than L2 (inputs AND weights rotate)
@@ -330,7 +396,7 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        with ClockSampler(local) as clk:
+        with ClockSampler(dev) as clk:
             el = time_device(torch, lambda i: graphs[i % nsets].replay(), args.steps, stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -406,14 +472,14 @@ def main():
     roofline_ops = {
         o.name: {"us": round(t * 1e6, 3), "gflops": round(o.flops / t / 1e9, 1),
                  "hbm_gbs": round(o.bytes / t / 1e9, 1), "hbm_frac": round(o.bytes / t / 1e9 / hbm_peak, 4),
+                 "ffma_frac": round(o.flops / t / 1e12 / peaks["ffma_tflops"], 4),
                  "share": round(t / step_dev, 3), "kernel": o.kernel} for o, t in per_op}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (U[-1,1) fp32, seeded)",
-        "config": {"workload": "TBMM(B=500,N=26,M=72,K=26) + 2FCRelu(B=128,1128->128->64) + "
-                               "MLP3(B=128,128->64->32->2) per step (BASELINE.json configs[1])",
+        "config": {"workload": STEP_WORKLOAD + " (BASELINE.json configs[1])",
                    "global_batch": {"tbmm": 500 * world, "fc": 128 * world}, "parallelism": f"dp{world}",
                    "l2": f"{nsets} rotating input+weight sets ({nsets * set_bytes / 2**20:.0f} MiB > 2x L2)",
                    "graphs": "one CUDA graph per input set (3 kernel launches)",
@@ -424,13 +490,15 @@ def main():
         "roofline": roofline,
         "step_ops": roofline_ops,
         "clocks": clk.summary(),
+        "peaks": {"hbm_gbs": hbm_peak, "hbm_source": peak_src, "ffma_tflops": peaks["ffma_tflops"],
+                  "ffma_source": "measured in this run (tcb_measure_peaks: fma.rn.f32 chains, all SMs)"},
         "device": device_info(local),
     }
     if not args.no_ops:
         line["ops"] = paper_op_table(ee, torch, dev, stream, peaks)
     if world == 1 and not args.no_cpu_baseline:
-        v, dt, info = cpu_reference_sample()
-        line["cpu_baseline"] = {"value": round(v, 4), "unit": "GFLOP/s", **info}
+        v, info = cpu_baseline()
+        line["cpu_baseline"] = {"value": round(v, 6), "unit": "GFLOP/s", **info}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -475,6 +543,7 @@ def paper_op_table(ee, torch, dev, stream, peaks):
             lat.sort()
             out[label] = {"us": round(t * 1e6, 3), "gflops": round(o.flops / t / 1e9, 1),
                           "hbm_gbs": round(o.bytes / t / 1e9, 1), "hbm_frac": round(o.bytes / t / 1e9 / hbm, 4),
+                          "ffma_frac": round(o.flops / t / 1e12 / peaks["ffma_tflops"], 4),
                           "us_p0_p50_p90_sync": [round(lat[0] * 1e6, 1), round(lat[len(lat) // 2] * 1e6, 1),
                                                  round(lat[int(len(lat) * 0.9)] * 1e6, 1)],
                           "l2": "cold (rotated)" if nsets > 1 else "warm (working set > L2)" if big else "warm",

@@ -101,6 +101,9 @@ const char* tcb_version(void);
 const char* tcb_last_error(void);
 /* "B200 sm_100 148 SMs ..." for device `dev`; fails without a GPU */
 int tcb_device_info(int dev, char* buf, int len);
+/* measured device peaks not in MEASURED_PEAKS.json, as JSON:
+ * {"ffma_tflops": fp32 fma.rn throughput, ...}; fails without a GPU */
+int tcb_measure_peaks(int dev, char* buf, int len);
 
 int tcb_engine_create(tcb_engine** out);
 void tcb_engine_destroy(tcb_engine* e);

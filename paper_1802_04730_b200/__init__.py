@@ -10,11 +10,11 @@ ExecutionEngine API.
 from ._lib import TcError, lib  # noqa: F401  (raises ImportError if libtcb.so is not built)
 from .engine import (ExecutionEngine, cache_deserialize, cache_load, cache_purge, cache_save,  # noqa: F401
                      cache_serialize, cache_set_history, cache_size, device_info, fill_uniform,
-                     options_baseline, options_digest, options_normalize, options_validate, version)
+                     measure_peaks, options_baseline, options_digest, options_normalize, options_validate, version)
 
 __all__ = [
     "ExecutionEngine", "TcError", "cache_load", "cache_save", "cache_size", "cache_purge",
     "cache_set_history", "cache_serialize", "cache_deserialize", "fill_uniform",
     "options_baseline", "options_digest", "options_normalize", "options_validate", "version",
-    "device_info",
+    "device_info", "measure_peaks",
 ]

@@ -47,7 +47,7 @@ class Tensor(C.Structure):
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_1802_04730_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_1802_04730_b200/build.py` "
             "(tc-b200 has no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     T = C.POINTER(Tensor)
@@ -56,6 +56,7 @@ def _load():
         "tcb_version": (C.c_char_p, []),
         "tcb_last_error": (C.c_char_p, []),
         "tcb_device_info": (C.c_int, [C.c_int, C.c_char_p, C.c_int]),
+        "tcb_measure_peaks": (C.c_int, [C.c_int, C.c_char_p, C.c_int]),
         "tcb_engine_create": (C.c_int, [C.POINTER(C.c_void_p)]),
         "tcb_engine_destroy": (None, [C.c_void_p]),
         "tcb_builtin_ops": (C.c_char_p, []),
@@ -107,7 +108,7 @@ lib = _load()
 
 # every symbol the C header declares (checked by tests/test_capi_symbols.py)
 EXPORTED = [
-    "tcb_version", "tcb_last_error", "tcb_device_info", "tcb_engine_create", "tcb_engine_destroy",
+    "tcb_version", "tcb_last_error", "tcb_device_info", "tcb_measure_peaks", "tcb_engine_create", "tcb_engine_destroy",
     "tcb_define", "tcb_builtin_ops", "tcb_def_signature", "tcb_infer_outputs", "tcb_compile",
     "tcb_run", "tcb_check", "tcb_describe", "tcb_tune", "tcb_cache_load", "tcb_cache_save",
     "tcb_cache_size", "tcb_cache_purge", "tcb_cache_set_history", "tcb_cache_serialize",

@@ -1,6 +1,6 @@
 """In-tree build of libtcb.so (the tc-b200 runtime + sm_100a kernels).
 
-    python -m paper_1802_04730_b200.build        (or __graft_entry__.build())
+    python paper_1802_04730_b200/build.py        (or __graft_entry__.build())
 
 * embeds tc/ops.tc into csrc/ops_tc.inc (the operator corpus the runtime
   recognises),

@@ -164,6 +164,21 @@ int tcb_device_info(int dev, char* buf, int len) {
   });
 }
 
+int tcb_measure_peaks(int dev, char* buf, int len) {
+  return guarded([&] {
+    cudaOk(cudaSetDevice(dev), "cudaSetDevice");
+    cudaDeviceProp p;
+    cudaOk(cudaGetDeviceProperties(&p, dev), "cudaGetDeviceProperties");
+    double ffma = 0;
+    float ms = 0;
+    cudaOk(k::probeFfma(p.multiProcessorCount, &ffma, &ms), "ffma probe");
+    std::ostringstream os;
+    os << "{\"ffma_tflops\": " << ffma << ", \"ffma_probe_ms\": " << ms
+       << ", \"sms\": " << p.multiProcessorCount << "}";
+    copyOut(os.str(), buf, len);
+  });
+}
+
 int tcb_engine_create(tcb_engine** out) {
   return guarded([&] { *out = new tcb_engine(); });
 }

@@ -106,5 +106,9 @@ struct LutArgs {
 };
 cudaError_t launchLut(const LutArgs* tables, int ntables, int threads, cudaStream_t s);
 
+// ---------------------------------------------------------------- probes
+// fp32 FFMA throughput of the whole device (TFLOP/s, 2 flops per FMA)
+cudaError_t probeFfma(int sms, double* tflops, float* ms);
+
 }  // namespace k
 }  // namespace tcb

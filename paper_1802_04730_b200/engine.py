@@ -291,6 +291,14 @@ def version():
     return lib.tcb_version().decode()
 
 
+def measure_peaks(dev=0):
+    """Device peaks not in MEASURED_PEAKS.json (fp32 FFMA TFLOP/s), measured now."""
+    import json
+    b = _lib.buf(1024)
+    check(lib.tcb_measure_peaks(dev, b, 1024))
+    return json.loads(b.value.decode())
+
+
 def device_info(dev=0):
     b = _lib.buf(1024)
     check(lib.tcb_device_info(dev, b, 1024))
