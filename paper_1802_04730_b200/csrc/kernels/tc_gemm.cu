@@ -1,0 +1,369 @@
+// tc_gemm.cu — tensor-core (tcgen05, TF32) variant of the GEMM-NT family:
+//   C[b][m][n] = epi(init + sum_k A[b][m][k] * B[b][n][k])
+// for TMM (tmm.tc), C3, TBMM (tbmm.tc) and the FC layers
+// of MLP1/2FCRelu/MLP3 when the caller asks for tensor-core math
+// (TCB_MATH_TF32 / TCB_MATH_3XTF32). The exact FFMA kernels (gemm.cu) stay
+// the default: a tensor-core reduction cannot reproduce the reference's
+// per-step fp32 chain (interpreter.cc:218-233), so these variants carry a
+// stated tolerance instead of bit equality.
+//
+// Structure (one CTA = one 128 x BN output tile of one K split):
+//   warp 0       TMA producer: 128x32 A and BNx32 B fp32 boxes, SWIZZLE_128B,
+//                into an S-stage shared-memory ring (mbarrier full/empty);
+//   warps 4..7   (3xTF32 only) split each landed fp32 tile in place into
+//                hi = tf32(x) and lo = tf32(x - hi) (a second buffer);
+//   warp 1       one elected lane issues tcgen05.mma.kind::tf32 (M=128,
+//                N=BN, K=8 per instruction; 3xTF32: lo*hi + hi*lo + hi*hi)
+//                into a TMEM accumulator, tcgen05.commit frees the stage;
+//   warp 2       allocates / frees the TMEM columns;
+//   warps 4..7   epilogue: tcgen05.ld the accumulator (lane = row) into a
+//                shared-memory partial tile.
+// Split-K: the `splits` CTAs of one output tile form a thread-block
+// cluster along z. After a cluster barrier, CTA r reduces rows
+// [r*128/splits, (r+1)*128/splits) of the tile by reading every CTA's
+// partial over DSMEM in fixed rank order (deterministic), adds the init
+// (bias / incoming C), applies ReLU and stores coalesced rows.
+#include <cuda.h>
+
+#include <mutex>
+
+#include "kernels.cuh"
+#include "sm100.cuh"
+
+namespace tcb {
+namespace k {
+
+namespace {
+
+using namespace sm100;
+
+constexpr int kBM = 128;   // UMMA M (one TMEM lane per output row)
+constexpr int kBK = 32;    // fp32 elements per 128-byte swizzle row
+constexpr int kThreads = 256;
+
+struct TcParams {
+  float* C;
+  const float* bias;
+  int M, N, K;
+  int64_t ldc, sC;
+  int init, relu;
+  int splits, kbPerSplit, nkb;
+  int aBatched, bBatched;
+};
+
+template <int BN, bool X3>
+struct TcCfg {
+  static constexpr int kABytes = kBM * kBK * 4;
+  static constexpr int kBBytes = BN * kBK * 4;
+  static constexpr int kStage = (kABytes + kBBytes) * (X3 ? 2 : 1);
+  static constexpr int kPartLd = BN + 4;  // partial tile row stride (floats)
+  static constexpr int kPartBytes = kBM * kPartLd * 4;
+  static constexpr int kBudget = 200 * 1024;
+  static constexpr int kStagesRaw = kBudget / kStage;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  static constexpr int kRing = kStages * kStage > kPartBytes ? kStages * kStage : kPartBytes;
+  static constexpr int kSmem = 1024 + kRing + 256;
+  static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static_assert(kStages >= 2, "stage ring too small");
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 is a multiple of 16 in [16, 256]");
+};
+
+template <int BN, bool X3>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+  using Cfg = TcCfg<BN, X3>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  auto aBig = [&](int s) { return sm + s * Cfg::kStage; };
+  auto bBig = [&](int s) { return sm + s * Cfg::kStage + Cfg::kABytes; };
+  auto aLo = [&](int s) { return sm + s * Cfg::kStage + Cfg::kABytes + Cfg::kBBytes; };
+  auto bLo = [&](int s) { return sm + s * Cfg::kStage + 2 * Cfg::kABytes + Cfg::kBBytes; };
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + Cfg::kRing);
+  uint64_t* conv = full + S;
+  uint64_t* empty = conv + S;
+  uint64_t* tmemFull = empty + S;
+  uint32_t* tmemSlot = reinterpret_cast<uint32_t*>(tmemFull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = blockIdx.x, mt = blockIdx.y;
+  const int split = blockIdx.z % p.splits, b = blockIdx.z / p.splits;
+  const int kb0 = split * p.kbPerSplit;
+  const int nk = min(p.nkb, kb0 + p.kbPerSplit) - kb0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbarInit(&full[s], 1);
+      mbarInit(&conv[s], 128);
+      mbarInit(&empty[s], 1);
+    }
+    mbarInit(tmemFull, 1);
+    fenceBarrierInit();
+  }
+  if (warp == 0 && lane == 0) {
+    tmaPrefetch(&tmA);
+    tmaPrefetch(&tmB);
+  }
+  if (warp == 2) tmemAlloc<Cfg::kTmemCols>(tmemSlot);
+  tcFenceBefore();
+  __syncthreads();
+  tcFenceAfter();
+  const uint32_t tmem = *tmemSlot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int ba = p.aBatched ? b : 0, bb = p.bBatched ? b : 0;
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % S;
+        if (i >= S) mbarWait(&empty[s], ((i / S) - 1) & 1, 1);
+        mbarExpectTx(&full[s], Cfg::kABytes + Cfg::kBBytes);
+        const int kc = (kb0 + i) * kBK;
+        tmaLoad3d(aBig(s), &tmA, kc, mt * kBM, ba, &full[s]);
+        tmaLoad3d(bBig(s), &tmB, kc, nt * BN, bb, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idescTf32(kBM, BN);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % S;
+        mbarWait(X3 ? &conv[s] : &full[s], (i / S) & 1, 2);
+        tcFenceAfter();
+        const uint32_t ab = smem(aBig(s)), bbg = smem(bBig(s));
+#pragma unroll
+        for (int kk = 0; kk < kBK / 8; ++kk) {
+          const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
+          const uint32_t acc = (i | kk) != 0;
+          if constexpr (X3) {
+            const uint32_t al = smem(aLo(s)), bl = smem(bLo(s));
+            mmaTf32(tmem, descSw128(al + off), descSw128(bbg + off), idesc, acc);
+            mmaTf32(tmem, descSw128(ab + off), descSw128(bl + off), idesc, 1);
+            mmaTf32(tmem, descSw128(ab + off), descSw128(bbg + off), idesc, 1);
+          } else {
+            mmaTf32(tmem, descSw128(ab + off), descSw128(bbg + off), idesc, acc);
+          }
+        }
+        mmaCommit(&empty[s]);
+      }
+      mmaCommit(tmemFull);
+    }
+  } else if (warp >= 4) {
+    const int et = threadIdx.x - 128;
+    if constexpr (X3) {
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % S;
+        mbarWait(&full[s], (i / S) & 1, 4);
+        float4* a = reinterpret_cast<float4*>(aBig(s));
+        float4* al = reinterpret_cast<float4*>(aLo(s));
+        for (int j = et; j < Cfg::kABytes / 16; j += 128) {
+          float4 x = a[j], h, l;
+          h.x = toTf32(x.x); h.y = toTf32(x.y); h.z = toTf32(x.z); h.w = toTf32(x.w);
+          l.x = toTf32(x.x - h.x); l.y = toTf32(x.y - h.y); l.z = toTf32(x.z - h.z); l.w = toTf32(x.w - h.w);
+          a[j] = h;
+          al[j] = l;
+        }
+        float4* bv = reinterpret_cast<float4*>(bBig(s));
+        float4* bl = reinterpret_cast<float4*>(bLo(s));
+        for (int j = et; j < Cfg::kBBytes / 16; j += 128) {
+          float4 x = bv[j], h, l;
+          h.x = toTf32(x.x); h.y = toTf32(x.y); h.z = toTf32(x.z); h.w = toTf32(x.w);
+          l.x = toTf32(x.x - h.x); l.y = toTf32(x.y - h.y); l.z = toTf32(x.z - h.z); l.w = toTf32(x.w - h.w);
+          bv[j] = h;
+          bl[j] = l;
+        }
+        fenceProxyAsyncSmem();
+        mbarArrive(&conv[s]);
+      }
+    }
+    // accumulator → shared partial tile (the ring is idle once tmemFull fires)
+    mbarWait(tmemFull, 0, 3);
+    tcFenceAfter();
+    const int q = warp - 4, row = q * 32 + lane;
+    float* part = reinterpret_cast<float*>(sm) + row * Cfg::kPartLd;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      tmemLoad32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
+      tmemLoadWait();
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(part + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+    tcFenceBefore();
+  }
+  __syncthreads();
+  if (p.splits > 1) clusterSync();
+
+  // split-K reduction + epilogue: this CTA's slice of rows, columns coalesced
+  {
+    const int R = kBM / p.splits;
+    const uint32_t base = smem(sm);
+    const int64_t cb = static_cast<int64_t>(b) * p.sC;
+    for (int idx = threadIdx.x; idx < R * BN; idx += kThreads) {
+      const int row = split * R + idx / BN, col = idx % BN;
+      const int m = mt * kBM + row, n = nt * BN + col;
+      if (m >= p.M || n >= p.N) continue;
+      const uint32_t off = base + (row * Cfg::kPartLd + col) * 4;
+      float acc = 0.f;
+      if (p.splits == 1) {
+        acc = *reinterpret_cast<const float*>(sm + (row * Cfg::kPartLd + col) * 4);
+      } else {
+        for (int r = 0; r < p.splits; ++r) acc += ldsCluster(mapa(off, r));
+      }
+      float* cp = p.C + cb + static_cast<int64_t>(m) * p.ldc + n;
+      float v = acc;
+      if (p.init == kInitInout) v = *cp + acc;
+      else if (p.init == kInitBias) v = p.bias[n] + acc;
+      if (p.relu) v = fmaxf(v, 0.f);
+      *cp = v;
+    }
+  }
+  if (p.splits > 1) clusterSync();  // peers may still be reading this CTA's partial
+  if (warp == 2) {
+    tcFenceAfter();
+    tmemFree<Cfg::kTmemCols>(tmem);
+  }
+}
+
+// ----------------------------------------------------------------- host
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encodeFn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 3-D map {K, rows, batch} of a row-major fp32 operand; box {32, boxRows, 1}
+bool makeMap(CUtensorMap* m, const float* base, int K, int rows, int batch, int64_t ld, int64_t sBatch,
+             int boxRows) {
+  EncodeFn enc = encodeFn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(batch)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 4,
+                           static_cast<cuuint64_t>(batch > 1 ? sBatch : ld * rows) * 4};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(boxRows), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, bool X3>
+cudaError_t launchT(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p, int tilesN, int tilesM,
+                    int batch, cudaStream_t s) {
+  using Cfg = TcCfg<BN, X3>;
+  auto kern = tc_gemm_kernel<BN, X3>;
+  static std::once_flag once;
+  static cudaError_t attrErr = cudaSuccess;
+  std::call_once(once, [&] {
+    attrErr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (attrErr == cudaSuccess) attrErr = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  });
+  if (attrErr != cudaSuccess) return attrErr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(tilesN, tilesM, batch * p.splits);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = p.splits;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+}
+
+template <bool X3>
+cudaError_t dispatchBn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p, int tilesN,
+                       int tilesM, int batch, cudaStream_t s) {
+  switch (bn) {
+    case 16: return launchT<16, X3>(ta, tb, p, tilesN, tilesM, batch, s);
+    case 32: return launchT<32, X3>(ta, tb, p, tilesN, tilesM, batch, s);
+    case 64: return launchT<64, X3>(ta, tb, p, tilesN, tilesM, batch, s);
+    case 128: return launchT<128, X3>(ta, tb, p, tilesN, tilesM, batch, s);
+    case 256: return launchT<256, X3>(ta, tb, p, tilesN, tilesM, batch, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+bool tcGemmSupported(const GemmArgs& a, const char** why) {
+  auto no = [&](const char* w) {
+    if (why) *why = w;
+    return false;
+  };
+  if (a.lda % 4 || a.ldb % 4) return no("tensor-core GEMM needs operand rows that are multiples of 16 bytes");
+  if (a.batch > 1 && ((a.sA && a.sA % 4) || (a.sB && a.sB % 4)))
+    return no("tensor-core GEMM needs batch strides that are multiples of 16 bytes");
+  if ((reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.B)) & 15)
+    return no("tensor-core GEMM needs 16-byte aligned operands");
+  if (a.K < 1 || a.M < 1 || a.N < 1) return no("empty GEMM");
+  return true;
+}
+
+TcPlan tcGemmPlan(int batch, int M, int N, int K, int sms) {
+  TcPlan pl;
+  const int tilesM = (M + kBM - 1) / kBM;
+  const int nkb = (K + kBK - 1) / kBK;
+  int bn = 256;
+  while (bn > 16 && bn / 2 >= N) bn /= 2;  // no wider than the problem
+  bn = std::max(16, bn);
+  auto ctas = [&](int b) { return static_cast<int64_t>(batch) * tilesM * ((N + b - 1) / b); };
+  while (bn > 32 && ctas(bn) * 2 <= sms) bn /= 2;  // spread columns before splitting K
+  int splits = 1;
+  while (splits < 16 && ctas(bn) * splits * 2 <= sms && splits * 2 <= nkb) splits *= 2;
+  pl.bn = bn;
+  pl.splits = splits;
+  return pl;
+}
+
+cudaError_t launchTcGemm(const GemmArgs& a, int math, const TcPlan& pl, cudaStream_t s) {
+  const char* why = nullptr;
+  if (!tcGemmSupported(a, &why)) return cudaErrorInvalidValue;
+  if (math != kMathTf32 && math != kMath3xTf32) return cudaErrorInvalidValue;
+  const int bn = pl.bn, splits = pl.splits;
+  if (splits < 1 || splits > 16 || (splits & (splits - 1))) return cudaErrorInvalidValue;
+  CUtensorMap ta, tb;
+  if (!makeMap(&ta, a.A, a.K, a.M, a.sA ? a.batch : 1, a.lda, a.sA, kBM)) return cudaErrorInvalidValue;
+  if (!makeMap(&tb, a.B, a.K, a.N, a.sB ? a.batch : 1, a.ldb, a.sB, bn)) return cudaErrorInvalidValue;
+  TcParams p;
+  p.C = a.C;
+  p.bias = a.bias;
+  p.M = a.M;
+  p.N = a.N;
+  p.K = a.K;
+  p.ldc = a.ldc;
+  p.sC = a.sC;
+  p.init = a.init;
+  p.relu = a.relu;
+  p.nkb = (a.K + kBK - 1) / kBK;
+  p.splits = std::min(splits, p.nkb);
+  while (p.splits & (p.splits - 1)) --p.splits;  // keep a power of two
+  p.kbPerSplit = (p.nkb + p.splits - 1) / p.splits;
+  // every split must own at least one k-block
+  while (p.splits > 1 && (p.splits - 1) * p.kbPerSplit >= p.nkb) {
+    p.splits /= 2;
+    p.kbPerSplit = (p.nkb + p.splits - 1) / p.splits;
+  }
+  p.aBatched = a.sA != 0 && a.batch > 1;
+  p.bBatched = a.sB != 0 && a.batch > 1;
+  const int tilesN = (a.N + bn - 1) / bn, tilesM = (a.M + kBM - 1) / kBM;
+  return math == kMath3xTf32 ? dispatchBn<true>(bn, ta, tb, p, tilesN, tilesM, a.batch, s)
+                             : dispatchBn<false>(bn, ta, tb, p, tilesN, tilesM, a.batch, s);
+}
+
+}  // namespace k
+}  // namespace tcb

@@ -8,7 +8,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O
 timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
 timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"gemm_nt|fc_cluster|tc_gemm|tbmm" -c 300 --csv \
     --log-file $OUT/launches.csv python bench.py --profile-only --steps 40 --warmup 3 > $OUT/ncu_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm_nt|fc_cluster" -s 2 -c 6 \
     -o $OUT/step python profiles/ncu_ops.py tbmm 2fcrelu mlp3 > $OUT/ncu_step.log 2>&1
