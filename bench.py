@@ -43,6 +43,7 @@ STEP_OPS = [
 PAPER_OPS = [
     ("tmm", "tmm 128x256x32", [(128, 32), (256, 32)], {}),
     ("tmm", "tmm 128x1024x1024", [(128, 1024), (1024, 1024)], {}),
+    ("tmm", "tmm 128x4096x16384", [(128, 16384), (4096, 16384)], {}),
     ("tbmm", "tbmm 500,26,72,26", [(500, 26, 72), (500, 26, 72)], {}),
     ("MLP1", "MLP1 128x1128->128", [(128, 1128), (128, 1128), (128,)], {}),
     ("2FCRelu", "2FCRelu 128x1128->128->64", [(128, 1128), (128, 1128), (128,), (64, 128), (64,)], {}),
@@ -54,6 +55,12 @@ PAPER_OPS = [
     ("2LUT", "2LUT E=1e7,D=64,B=128,L=50",
      [(10_000_000, 64), (128, 50), (10_000_000, 64), (128, 50)], {}),
 ]
+# tensor-core (tcgen05) variants of the contractions: (label of the exact op, math)
+TC_OPS = [("tmm 128x1024x1024", "3xtf32"), ("tmm 128x1024x1024", "tf32"),
+          ("tmm 128x4096x16384", "3xtf32"), ("tmm 128x4096x16384", "tf32"),
+          ("C3 128x1024->1000", "3xtf32"), ("C3 128x1024->1000", "tf32"),
+          ("tbmm 500,26,72,26", "3xtf32"), ("MLP1 128x1128->128", "3xtf32"),
+          ("2FCRelu 128x1128->128->64", "3xtf32"), ("MLP3 128->64->32->2", "3xtf32")]
 INT_PARAMS = {"2LUT": {1, 3}, "1LUT": {1}}
 
 
@@ -136,7 +143,7 @@ class ClockSampler:
 class OpInstance:
     """One TC op bound to device tensors (a rotating set of input copies)."""
 
-    def __init__(self, ee, torch, name, pshapes, seeded, nsets, dev, seed, host_init=True):
+    def __init__(self, ee, torch, name, pshapes, seeded, nsets, dev, seed, host_init=True, math="ffma"):
         self.ee, self.torch, self.name = ee, torch, name
         _, rets = ee.signature(name)
         ints = INT_PARAMS.get(name, set())
@@ -158,7 +165,7 @@ class OpInstance:
             os_ = [torch.rand(s, generator=g, device=dev) * 2 - 1 if i in self.inout else
                    torch.zeros(s, device=dev) for i, s in enumerate(oshapes)]
             self.sets.append((ps, os_))
-        self.handle = ee.compile(name, self.sets[0][0], self.sets[0][1])
+        self.handle = ee.compile(name, self.sets[0][0], self.sets[0][1], math=math)
         d = ee.describe(self.handle)
         self.flops, self.bytes, self.kernel = d["flops"], d["bytes"], d["kernel"]
 
@@ -511,13 +518,16 @@ def paper_op_table(ee, torch, dev, stream, peaks):
     PAPER.md:1570-1585) for every paper operator at its paper shape."""
     out = {}
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    for name, label, shapes, seeded in PAPER_OPS:
+    byl = {lab: (n, sh, sd) for n, lab, sh, sd in PAPER_OPS}
+    todo = [(n, lab, sh, sd, "ffma") for n, lab, sh, sd in PAPER_OPS]
+    todo += [(*byl[lab][:1], f"{lab} [{m}]", *byl[lab][1:], m) for lab, m in TC_OPS]
+    for name, label, shapes, seeded, math in todo:
         try:
-            big = name in ("2LUT", "gconv")
-            one = OpInstance(ee, torch, name, shapes, seeded, 1, dev, 3)
+            big = name in ("2LUT", "gconv") or label.startswith("tmm 128x4096x16384")
+            one = OpInstance(ee, torch, name, shapes, seeded, 1, dev, 3, math=math)
             nsets = 1 if big else max(2, int(np.ceil(2 * L2_BYTES / max(1, one.set_bytes()))))
             nsets = min(nsets, 64)
-            o = one if nsets == 1 else OpInstance(ee, torch, name, shapes, seeded, nsets, dev, 3)
+            o = one if nsets == 1 else OpInstance(ee, torch, name, shapes, seeded, nsets, dev, 3, math=math)
             with torch.cuda.stream(stream):
                 for i in range(3):
                     o.run(i)
@@ -530,11 +540,11 @@ def paper_op_table(ee, torch, dev, stream, peaks):
                         o.run(i)
                 for i in range(2):
                     g.replay()
-                reps = 3 if name == "gconv" else 10
+                reps = 3 if big else 10
                 t = time_device(torch, lambda i: g.replay(), reps, stream) / (reps * per)
                 # paper protocol: synchronised single calls incl. launch overhead
                 lat = []
-                for i in range(100 if name == "gconv" else 300):
+                for i in range(50 if big else 300):
                     torch.cuda.synchronize()
                     t0 = time.perf_counter()
                     o.run(i)
@@ -547,7 +557,14 @@ def paper_op_table(ee, torch, dev, stream, peaks):
                           "us_p0_p50_p90_sync": [round(lat[0] * 1e6, 1), round(lat[len(lat) // 2] * 1e6, 1),
                                                  round(lat[int(len(lat) * 0.9)] * 1e6, 1)],
                           "l2": "cold (rotated)" if nsets > 1 else "warm (working set > L2)" if big else "warm",
-                          "kernel": o.kernel}
+                          "kernel": o.kernel, "math": math}
+            if math != "ffma":
+                # tensor-pipe roofline: TF32 dense = half the measured bf16 dense peak; 3xTF32
+                # issues three TF32 MMAs per useful multiply-add
+                tf32_peak = float(peaks.get("bf16_tflops", 1590.0)) / 2
+                mult = 3 if math == "3xtf32" else 1
+                out[label]["tensor_frac"] = round(mult * o.flops / t / 1e12 / tf32_peak, 4)
+                out[label]["tensor_peak_tflops"] = round(tf32_peak, 1)
             del o, one
             torch.cuda.empty_cache()
         except Exception as e:  # report, don't hide

@@ -82,6 +82,11 @@ extern "C" {
 #define TCB_ERR_NOKERNEL 26
 #define TCB_ERR_CUDA 27
 
+/* arithmetic of a compiled handle (tcb_compile_ex) */
+#define TCB_MATH_FFMA 0   /* default: FFMA-exact kernels, bit-identical to the reference interpreter */
+#define TCB_MATH_TF32 1   /* tcgen05 .kind::tf32 tensor cores (GEMM-NT family, FC chains); tolerance DESIGN.md §2 */
+#define TCB_MATH_3XTF32 3 /* tcgen05 TF32 with hi/lo operand split (3 MMAs): near-fp32 accuracy */
+
 /* run flags */
 #define TCB_RUN_PROFILE 1  /* time the launch with CUDA events (synchronises) */
 #define TCB_RUN_NOCHECK 2  /* skip the post-launch device error check (graph capture) */
@@ -128,6 +133,14 @@ int tcb_infer_outputs(tcb_engine* e, const char* name, const tcb_tensor* inputs,
  * Writes the handle. */
 int tcb_compile(tcb_engine* e, const char* name, const tcb_tensor* inputs, int n_inputs,
                 const tcb_tensor* outputs, int n_outputs, const char* options_json, uint64_t* handle);
+
+/* compile with an explicit arithmetic (TCB_MATH_*). Tensor-core modes exist
+ * for tmm, tbmm, C3, MLP1, 2FCRelu, MLP3; other defs fail with
+ * TCB_ERR_MAPPING_INVALID. Their cache entries carry the target suffix
+ * " math=<mode>" and never mix with the exact ones. */
+int tcb_compile_ex(tcb_engine* e, const char* name, const tcb_tensor* inputs, int n_inputs,
+                   const tcb_tensor* outputs, int n_outputs, const char* options_json, int math,
+                   uint64_t* handle);
 
 /* ExecutionEngine::run. stream: a cudaStream_t (NULL = legacy default).
  * With TCB_RUN_PROFILE, *duration_ns receives the device time of the call. */

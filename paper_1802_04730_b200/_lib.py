@@ -12,6 +12,7 @@ LIB_PATH = os.path.join(_HERE, "libtcb.so")
 TCB_F32, TCB_I32 = 0, 1
 TCB_DEVICE, TCB_HOST = 0, 1
 TCB_RUN_PROFILE, TCB_RUN_NOCHECK = 1, 2
+MATH_MODES = {"ffma": 0, "tf32": 1, "3xtf32": 3}
 
 # ErrorKind order of proj/include/tc/support/diagnostics.h:36-68 (+2 additions)
 ERROR_KINDS = [
@@ -65,6 +66,8 @@ def _load():
                                         C.POINTER(C.c_int), C.c_char_p, C.c_int]),
         "tcb_infer_outputs": (C.c_int, [C.c_void_p, C.c_char_p, T, C.c_int, T, C.c_int]),
         "tcb_compile": (C.c_int, [C.c_void_p, C.c_char_p, T, C.c_int, T, C.c_int, C.c_char_p, u64p]),
+        "tcb_compile_ex": (C.c_int, [C.c_void_p, C.c_char_p, T, C.c_int, T, C.c_int, C.c_char_p, C.c_int,
+                                     u64p]),
         "tcb_run": (C.c_int, [C.c_void_p, C.c_uint64, T, C.c_int, T, C.c_int, C.c_void_p, C.c_int,
                               C.POINTER(C.c_int64)]),
         "tcb_check": (C.c_int, [C.c_void_p, C.c_uint64]),
@@ -110,6 +113,7 @@ lib = _load()
 EXPORTED = [
     "tcb_version", "tcb_last_error", "tcb_device_info", "tcb_measure_peaks", "tcb_engine_create", "tcb_engine_destroy",
     "tcb_define", "tcb_builtin_ops", "tcb_def_signature", "tcb_infer_outputs", "tcb_compile",
+    "tcb_compile_ex",
     "tcb_run", "tcb_check", "tcb_describe", "tcb_tune", "tcb_cache_load", "tcb_cache_save",
     "tcb_cache_size", "tcb_cache_purge", "tcb_cache_set_history", "tcb_cache_serialize",
     "tcb_cache_deserialize", "tcb_cache_lookup", "tcb_cache_inject", "tcb_canonical",

@@ -35,8 +35,11 @@ struct Key {
   std::string lookupKey() const;
 };
 
+// targetSuffix distinguishes tensor-core math modes (" math=tf32"): their
+// kernels and results differ from the exact default, so they never share
+// cache entries with it.
 Key makeKey(const lang::Validated& v, const std::map<std::string, std::vector<int64_t>>& shapes,
-            const MappingOptions& o);
+            const MappingOptions& o, const std::string& targetSuffix = "");
 
 enum class Origin { Tuned, Injected, Baseline };
 const char* originName(Origin o);

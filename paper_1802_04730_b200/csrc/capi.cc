@@ -75,6 +75,7 @@ struct Compiled {
   MappingOptions opts;
   ops::Mapping map;
   std::string source;
+  int math = 0;
   int* dErr = nullptr;
   cudaStream_t lastStream = nullptr;
   // staging for TCB_HOST tensors
@@ -229,33 +230,42 @@ int tcb_infer_outputs(tcb_engine* e, const char* name, const tcb_tensor* in, int
   });
 }
 
-int tcb_compile(tcb_engine* e, const char* name, const tcb_tensor* in, int nin, const tcb_tensor* out, int nout,
-                const char* options_json, uint64_t* handle) {
+int tcb_compile_ex(tcb_engine* e, const char* name, const tcb_tensor* in, int nin, const tcb_tensor* out, int nout,
+                   const char* options_json, int math, uint64_t* handle) {
   return guarded([&] {
+    if (math != TCB_MATH_FFMA && math != TCB_MATH_TF32 && math != TCB_MATH_3XTF32)
+      fail(ErrorKind::MappingInvalid, "unknown math mode " + std::to_string(math));
     std::lock_guard<std::mutex> g(e->mu);
     auto c = std::make_unique<Compiled>();
     c->name = name;
+    c->math = math;
     c->spec = e->specialize(name, in, nin, out, nout);
     c->canon = cache::canonicalize(c->spec.v);
     c->prob = ops::match(c->spec, c->canon);
+    const std::string suffix = math ? std::string(" math=") + ops::mathName(math) : std::string();
     if (options_json) {
       c->opts = MappingOptions::fromJson(options_json);
       c->source = "explicit";
     } else {
-      c->key = cache::makeKey(c->spec.v, e->paramShapes(c->spec), MappingOptions{});
+      c->key = cache::makeKey(c->spec.v, e->paramShapes(c->spec), MappingOptions{}, suffix);
       if (auto hit = globalCache().lookup(c->key)) {
         c->opts = hit->options;
         c->source = "cache";
       } else {
-        c->opts = ops::defaultOptions(c->prob);
+        c->opts = ops::defaultOptions(c->prob, math);
         c->source = "default";
       }
     }
-    c->key = cache::makeKey(c->spec.v, e->paramShapes(c->spec), c->opts);
-    c->map = ops::decode(c->prob, c->opts);
+    c->key = cache::makeKey(c->spec.v, e->paramShapes(c->spec), c->opts, suffix);
+    c->map = ops::decode(c->prob, c->opts, math);
     e->handles.push_back(std::move(c));
     *handle = e->handles.size();
   });
+}
+
+int tcb_compile(tcb_engine* e, const char* name, const tcb_tensor* in, int nin, const tcb_tensor* out, int nout,
+                const char* options_json, uint64_t* handle) {
+  return tcb_compile_ex(e, name, in, nin, out, nout, options_json, TCB_MATH_FFMA, handle);
 }
 
 int tcb_describe(tcb_engine* e, uint64_t h, char* buf, int len) {
@@ -269,6 +279,7 @@ int tcb_describe(tcb_engine* e, uint64_t h, char* buf, int len) {
     j["kernel"] = Json(c.map.describe());
     j["options"] = Json::parse(c.opts.toJson());
     j["options_source"] = Json(c.source);
+    j["math"] = Json(ops::mathName(c.math));
     j["flops"] = Json(static_cast<int64_t>(c.prob.flops));
     j["bytes"] = Json(static_cast<int64_t>(c.prob.bytes));
     j["canonical_tc"] = Json(c.canon);

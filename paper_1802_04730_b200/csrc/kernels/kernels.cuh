@@ -43,6 +43,18 @@ const GemmVariant& gemmVariant(int i);
 // threads: only used by the direct variant (≥32, multiple of 32, ≤1024)
 cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t s);
 
+// ------------------------------------------------- GEMM-NT, tensor cores
+// tcgen05 .kind::tf32 variant of the same contraction (tc_gemm.cu). Not
+// FFMA-exact: selected only when the caller asks for tensor-core math.
+enum MathMode : int { kMathFfma = 0, kMathTf32 = 1, kMath3xTf32 = 3 };
+struct TcPlan {
+  int bn = 128;     // output columns per CTA (UMMA N, multiple of 16 in [16, 256])
+  int splits = 1;   // K splits = cluster size along z (power of two <= 16)
+};
+bool tcGemmSupported(const GemmArgs& a, const char** why);
+TcPlan tcGemmPlan(int batch, int M, int N, int K, int sms);
+cudaError_t launchTcGemm(const GemmArgs& a, int math, const TcPlan& plan, cudaStream_t s);
+
 // ------------------------------------------------------------ FC chain
 // Fused FC+bias+ReLU layers (MLP1 / 2FCRelu / MLP3): a cluster of `cn` CTAs
 // per `rows` batch rows; output features split across the cluster,

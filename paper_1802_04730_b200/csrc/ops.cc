@@ -51,6 +51,48 @@ double vol(const std::vector<int64_t>& v) {
 
 [[noreturn]] void invalid(const std::string& m) { fail(ErrorKind::MappingInvalid, m); }
 
+int smCount() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+// Tensor-core genes: tile_sizes[1] = UMMA N per CTA (16..256, power of two),
+// block_shape[2] = K splits (cluster size, power of two <= 16); a tile N of
+// 1 means "plan tile and splits from each contraction's shape" (the FC
+// chains' default: every layer gets its own plan).
+void decodeTc(const Problem& p, const MappingOptions& o, Mapping& m) {
+  if (p.family != Family::Gemm && p.family != Family::FcChain)
+    invalid(std::string("no tensor-core kernel for the ") + familyName(p.family) +
+            " family (tensor-core math covers TMM, TBMM, C3 and the FC chains)");
+  auto ok4 = [](int64_t v) { return v % 4 == 0; };
+  if (p.family == Family::Gemm) {
+    const GemmDesc& g = p.gemm;
+    if (!ok4(g.lda) || !ok4(g.ldb) || (g.batch > 1 && (!ok4(g.sA) || !ok4(g.sB))))
+      invalid("tensor-core GEMM needs operand rows and batch strides that are multiples of 16 bytes");
+  } else {
+    if (!ok4(p.fc.ldi)) invalid("tensor-core FC layers need input rows that are multiples of 16 bytes");
+    for (const auto& L : p.fc.layers)
+      if (!ok4(L.ldw) || !ok4(L.out)) invalid("tensor-core FC layers need rows that are multiples of 16 bytes");
+  }
+  m.fused = false;
+  int64_t bn = o.tileSizes.size() > 1 ? o.tileSizes[1] : 0;
+  int64_t sp = o.blockShape[2];
+  if (bn <= 1) {
+    m.tcAuto = true;
+    return;
+  }
+  if (bn != 16 && bn != 32 && bn != 64 && bn != 128 && bn != 256)
+    invalid("tensor-core tile N must be one of 16, 32, 64, 128, 256");
+  if (sp < 1 || sp > 16 || (sp & (sp - 1))) invalid("tensor-core K splits must be a power of two <= 16");
+  m.tcAuto = false;
+  m.tc.bn = static_cast<int>(bn);
+  m.tc.splits = static_cast<int>(sp);
+}
+
 void decodeGemm(const MappingOptions& o, Mapping& m) {
   if (!o.useShared) {
     int t = static_cast<int>(o.threads());
@@ -96,7 +138,15 @@ void launchGemmDesc(const GemmDesc& g, const Mapping& m, void* const* in, void* 
   a.sC = g.sC;
   a.init = g.init;
   a.relu = g.relu;
-  cudaError_t e = k::launchGemm(a, m.gemmVariant, m.gemmThreads, s);
+  cudaError_t e;
+  if (m.math != k::kMathFfma) {
+    const char* why = nullptr;
+    if (!k::tcGemmSupported(a, &why)) fail(ErrorKind::MappingInvalid, why);
+    k::TcPlan pl = m.tcAuto ? k::tcGemmPlan(g.batch, g.M, g.N, g.K, smCount()) : m.tc;
+    e = k::launchTcGemm(a, m.math, pl, s);
+  } else {
+    e = k::launchGemm(a, m.gemmVariant, m.gemmThreads, s);
+  }
   if (e != cudaSuccess) fail(ErrorKind::Cuda, std::string("GEMM launch failed: ") + cudaGetErrorString(e));
 }
 
@@ -129,6 +179,13 @@ std::string formOf(const std::string& canon) {
 std::string Mapping::describe() const {
   std::ostringstream os;
   os << familyName(family) << ":";
+  if (math != k::kMathFfma) {
+    os << "tcgen05 " << mathName(math);
+    if (tcAuto) os << " planned";
+    else os << " bn=" << tc.bn << " splits=" << tc.splits;
+    if (family == Family::FcChain) os << " per-layer";
+    return os.str();
+  }
   switch (family) {
     case Family::Gemm:
       os << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
@@ -285,10 +342,32 @@ Problem match(const sem::Specialized& s, const std::string& canon) {
   fail(ErrorKind::Internal, "registered form '" + form + "' has no binder");
 }
 
-Mapping decode(const Problem& p, const MappingOptions& o) {
+const char* mathName(int math) {
+  switch (math) {
+    case k::kMathFfma: return "ffma";
+    case k::kMathTf32: return "tf32";
+    case k::kMath3xTf32: return "3xtf32";
+  }
+  return "?";
+}
+
+int mathFromName(const std::string& s) {
+  if (s == "ffma" || s.empty()) return k::kMathFfma;
+  if (s == "tf32") return k::kMathTf32;
+  if (s == "3xtf32") return k::kMath3xTf32;
+  invalid("unknown math mode '" + s + "' (ffma | tf32 | 3xtf32)");
+}
+
+Mapping decode(const Problem& p, const MappingOptions& o, int math) {
   o.validate();
   Mapping m;
   m.family = p.family;
+  if (math != k::kMathFfma) {
+    if (math != k::kMathTf32 && math != k::kMath3xTf32) invalid("unknown math mode");
+    m.math = math;
+    decodeTc(p, o, m);
+    return m;
+  }
   switch (p.family) {
     case Family::Gemm: decodeGemm(o, m); break;
     case Family::FcChain: {
@@ -364,8 +443,24 @@ Mapping decode(const Problem& p, const MappingOptions& o) {
   return m;
 }
 
-MappingOptions defaultOptions(const Problem& p) {
+MappingOptions defaultOptions(const Problem& p, int math) {
   MappingOptions o;
+  if (math != k::kMathFfma && (p.family == Family::Gemm || p.family == Family::FcChain)) {
+    // tensor-core plan for the (first) contraction; FC layers replan per layer
+    int batch = 1, M = 0, N = 0, K = 0;
+    if (p.family == Family::Gemm) {
+      batch = p.gemm.batch, M = p.gemm.M, N = p.gemm.N, K = p.gemm.K;
+    } else {
+      M = p.fc.batch, N = p.fc.layers[0].out, K = p.fc.layers[0].kred;
+    }
+    k::TcPlan pl = k::tcGemmPlan(batch, M, N, K, smCount());
+    o.tileSizes = {128, p.family == Family::Gemm ? pl.bn : 1, 32};
+    o.blockShape = {{1, 1, p.family == Family::Gemm ? pl.splits : 1}};
+    o.threadShape = {{256, 1, 1}};
+    o.useShared = true;
+    o.fusion = Fusion::Min;
+    return o;
+  }
   switch (p.family) {
     case Family::Gemm: {
       // start from the reference's contraction preset (options.cc:182-191:

@@ -78,6 +78,11 @@ struct Problem {
 };
 
 struct Mapping {
+  // arithmetic: k::kMathFfma (the exact FFMA kernels, default) or a
+  // tensor-core mode (k::kMathTf32 / k::kMath3xTf32, tc_gemm.cu)
+  int math = k::kMathFfma;
+  k::TcPlan tc;  // tensor-core tile plan (math != FFMA); per-layer plans are derived at launch
+  bool tcAuto = true;
   // Gemm (and unfused FC layers)
   int gemmVariant = 4, gemmThreads = 0;
   // FcChain
@@ -97,8 +102,13 @@ std::vector<std::string> registeredForms();
 std::string formOf(const std::string& canonicalTc);  // "" if unregistered
 
 Problem match(const sem::Specialized& s, const std::string& canonicalTc);  // Error(NoKernel)
-Mapping decode(const Problem& p, const MappingOptions& o);                // Error(MappingInvalid)
-MappingOptions defaultOptions(const Problem& p);
+// math: k::MathMode. Tensor-core modes exist for the GEMM-NT family
+// (TMM, TBMM, C3) and the FC chains (per-layer GEMMs); other families
+// raise MappingInvalid for them.
+Mapping decode(const Problem& p, const MappingOptions& o, int math = k::kMathFfma);  // Error(MappingInvalid)
+MappingOptions defaultOptions(const Problem& p, int math = k::kMathFfma);
+const char* mathName(int math);
+int mathFromName(const std::string& s);  // Error(MappingInvalid)
 
 // Gene pools for the tuner (TuningSpace per family; see tuner.cc).
 struct GenePools {

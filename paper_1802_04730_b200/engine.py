@@ -117,14 +117,20 @@ class ExecutionEngine:
         return [tuple(outs[i].shape[d] for d in range(outs[i].rank)) for i in range(len(rets))]
 
     # ------------------------------------------------------------ compile
-    def compile(self, name, inputs, outputs=None, options=None) -> int:
+    def compile(self, name, inputs, outputs=None, options=None, math="ffma") -> int:
+        """math: "ffma" (default; FFMA-exact, bit-identical to the reference
+        interpreter), "tf32" or "3xtf32" (tcgen05 tensor cores; stated
+        tolerance)."""
         ins, nin = _arr(inputs)
         outs, nout = _arr(outputs) if outputs is not None else (None, 0)
         h = C.c_uint64()
         opt = None
         if options is not None:
             opt = (options if isinstance(options, str) else json.dumps(options)).encode()
-        check(lib.tcb_compile(self._h, name.encode(), ins, nin, outs, nout, opt, C.byref(h)))
+        if math not in _lib.MATH_MODES:
+            raise ValueError(f"math must be one of {sorted(_lib.MATH_MODES)}")
+        check(lib.tcb_compile_ex(self._h, name.encode(), ins, nin, outs, nout, opt, _lib.MATH_MODES[math],
+                                 C.byref(h)))
         return h.value
 
     def describe(self, handle: int) -> dict:

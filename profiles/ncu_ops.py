@@ -1,6 +1,7 @@
 """Runs selected paper operators a few times each at their paper shapes, for
 ncu captures (profiles/README.md). Usage: python profiles/ncu_ops.py op [op ...]
-ops: tmm tmm_big tbmm mlp1 2fcrelu mlp3 c3 kru gconv lut  (+ "opts=<json>")"""
+ops: tmm tmm_big tmm_huge tbmm mlp1 2fcrelu mlp3 c3 kru gconv lut
+(+ "opts=<json>", "math=ffma|tf32|3xtf32", "reps=N")"""
 import json
 import os
 import sys
@@ -15,6 +16,7 @@ from paper_1802_04730_b200 import ExecutionEngine  # noqa: E402
 OPS = {
     "tmm": ("tmm", [(128, 32), (256, 32)], {}),
     "tmm_big": ("tmm", [(128, 1024), (1024, 1024)], {}),
+    "tmm_huge": ("tmm", [(128, 16384), (4096, 16384)], {}),
     "tbmm": ("tbmm", [(500, 26, 72), (500, 26, 72)], {}),
     "mlp1": ("MLP1", [(128, 1128), (128, 1128), (128,)], {}),
     "2fcrelu": ("2FCRelu", [(128, 1128), (128, 1128), (128,), (64, 128), (64,)], {}),
@@ -30,9 +32,13 @@ def main():
     ee = ExecutionEngine()
     opts = None
     reps = 3
+    math = "ffma"
     for a in sys.argv[1:]:
         if a.startswith("opts="):
             opts = json.loads(a[5:])
+            continue
+        if a.startswith("math="):
+            math = a[5:]
             continue
         if a.startswith("reps="):
             reps = int(a[5:])
@@ -48,7 +54,7 @@ def main():
         given = [seeded.get(i) for i in range(len(rets))]
         oshapes = ee.infer_output_tensor_info(name, shapes, given)
         outs = [torch.rand(s, device="cuda") for s in oshapes]
-        h = ee.compile(name, ps, outs, opts)
+        h = ee.compile(name, ps, outs, opts, math=math)
         print(a, ee.describe(h)["kernel"], flush=True)
         for _ in range(reps):
             ee.run(h, ps, outs)

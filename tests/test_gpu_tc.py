@@ -1,0 +1,171 @@
+"""GPU parity of the tensor-core (tcgen05 TF32 / 3xTF32) variants against
+the oracle. These variants are not FFMA-exact: a tensor-core reduction
+cannot reproduce the reference interpreter's per-step fp32 chain
+(interpreter.cc:218-233), so the bar is a stated tolerance:
+
+  maxRelError (tensor_data.cc:221-234, denominator max(|ref|, 1)) against
+  the oracle, inputs U[-1,1):
+    3xtf32:  <= TOL_3X(K) = 1e-5 + K * 2^-23
+    tf32:    <= TOL_1X(K) = K * 2^-11       (operands rounded to 10-bit mantissas)
+
+Every case also records its measured error next to the bound
+(gpurun_out/tc_errors.jsonl when run on the GPU box).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import max_rel
+from oracle_lib import Oracle
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def tol(math, K):
+    return 1e-5 + K * 2.0 ** -23 if math == "3xtf32" else K * 2.0 ** -11
+
+
+def record(name, math, K, err, exact_err, oracle_exact_err):
+    d = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    with open(os.path.join(d, "tc_errors.jsonl"), "a") as f:
+        f.write(json.dumps({"case": name, "math": math, "K": K, "max_rel_vs_oracle": err, "bound": tol(math, K),
+                            "max_rel_vs_fp64": exact_err, "oracle_max_rel_vs_fp64": oracle_exact_err}) + "\n")
+
+
+@pytest.fixture(scope="module")
+def env():
+    assert torch.cuda.is_available()
+    from paper_1802_04730_b200 import ExecutionEngine
+    return ExecutionEngine(), Oracle()
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run(ee, name, params, outs, math, options=None):
+    p = [dev(x) for x in params]
+    o = [dev(x) for x in outs]
+    h = ee.compile(name, p, o, options, math=math)
+    ee.run(h, p, o)
+    torch.cuda.synchronize()
+    return [t.cpu().numpy() for t in o], ee.describe(h)
+
+
+def gemm64(A, B):
+    return A.astype(np.float64) @ B.astype(np.float64).T
+
+
+GEMM_CASES = [
+    ("tmm", (128, 256, 32)),
+    ("tmm", (128, 1024, 1024)),
+    ("tmm", (200, 72, 64)),
+    ("tmm", (77, 300, 44)),
+    ("C3", (128, 1000, 1024)),
+    ("C3", (5, 33, 20)),
+]
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("name,shape", GEMM_CASES)
+def test_gemm_tc(env, name, shape, math):
+    ee, orc = env
+    M, N, K = shape
+    rng = orc.rng(11 + M + N + K)
+    A, B = rng.f32((M, K)), rng.f32((N, K))
+    if name == "C3":
+        cin = rng.f32((M, N))
+        ref = orc.c3(A, B, cin)
+        exact = cin.astype(np.float64) + gemm64(A, B)
+        (got,), desc = run(ee, "C3", [A, B], [cin], math)
+    else:
+        ref = orc.tmm(A, B)
+        exact = gemm64(A, B)
+        (got,), desc = run(ee, "tmm", [A, B], [np.zeros((M, N), np.float32)], math)
+    assert desc["math"] == math and "tcgen05" in desc["kernel"]
+    err = max_rel(ref, got)
+    record(f"{name} {M}x{N}x{K}", math, K, err, max_rel(exact, got), max_rel(exact, ref))
+    assert err <= tol(math, K), f"{name} {shape} {math}: maxRel {err:.3g} > {tol(math, K):.3g}"
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("shape", [(500, 26, 72, 26), (7, 26, 72, 26), (3, 40, 36, 130)])
+def test_tbmm_tc(env, shape, math):
+    ee, orc = env
+    Bt, N, M, K = shape  # tbmm.tc: X[B][N][M], Y[B][K][M] -> Z[B][N][K]
+    rng = orc.rng(5 + Bt)
+    X, Y = rng.f32((Bt, N, M)), rng.f32((Bt, K, M))
+    ref = orc.tbmm(X, Y)
+    exact = np.einsum("bnm,bkm->bnk", X.astype(np.float64), Y.astype(np.float64))
+    (got,), desc = run(ee, "tbmm", [X, Y], [np.zeros((Bt, N, K), np.float32)], math)
+    err = max_rel(ref, got)
+    record(f"tbmm {shape}", math, M, err, max_rel(exact, got), max_rel(exact, ref))
+    assert err <= tol(math, M)
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+def test_fc_chains_tc(env, math):
+    ee, orc = env
+    rng = orc.rng(99)
+    I, W1, B1 = rng.f32((128, 1128)), rng.f32((128, 1128)), rng.f32((128,))
+    W2, B2 = rng.f32((64, 128)), rng.f32((64,))
+    o1 = orc.fc_relu(I, W1, B1)
+    o2 = orc.fc_relu(o1, W2, B2)
+    (g1,), desc = run(ee, "MLP1", [I, W1, B1], [np.zeros((128, 128), np.float32)], math)
+    assert "tcgen05" in desc["kernel"]
+    e1 = max_rel(o1, g1)
+    record("MLP1 128x1128->128", math, 1128, e1, None, None)
+    assert e1 <= tol(math, 1128)
+    (h1, h2), _ = run(ee, "2FCRelu", [I, W1, B1, W2, B2], [np.zeros((128, 128), np.float32),
+                                                           np.zeros((128, 64), np.float32)], math)
+    assert max_rel(o1, h1) <= tol(math, 1128)
+    # layer 2 consumes the GPU's own layer-1 output: compare against the
+    # oracle applied to that same input, plus the propagated layer-1 error
+    ref2 = orc.fc_relu(h1, W2, B2)
+    e2 = max_rel(ref2, h2)
+    record("2FCRelu layer 2", math, 128, e2, None, None)
+    assert e2 <= tol(math, 128)
+    O1 = rng.f32((128, 128))
+    M2, C2, M3, C3b, M4, C4 = (rng.f32((64, 128)), rng.f32((64,)), rng.f32((32, 64)), rng.f32((32,)),
+                               rng.f32((2, 32)), rng.f32((2,)))
+    (q1, q2, q3, q4), _ = run(ee, "MLP3", [O1, M2, C2, M3, C3b, M4, C4],
+                              [O1, np.zeros((128, 64), np.float32), np.zeros((128, 32), np.float32),
+                               np.zeros((128, 2), np.float32)], math)
+    assert np.array_equal(q1, O1)  # pass-through return untouched
+    for got, (inp, W, b, K) in zip((q2, q3, q4), ((O1, M2, C2, 128), (q2, M3, C3b, 64), (q3, M4, C4, 32))):
+        e = max_rel(orc.fc_relu(inp, W, b), got)
+        record(f"MLP3 layer K={K}", math, K, e, None, None)
+        assert e <= tol(math, K)
+
+
+def test_tc_explicit_plan_and_errors(env):
+    from paper_1802_04730_b200 import TcError, options_baseline
+    ee, orc = env
+    rng = orc.rng(3)
+    A, B = rng.f32((128, 256)), rng.f32((512, 256))
+    ref = orc.tmm(A, B)
+    for bn, sp in [(16, 1), (64, 4), (128, 8), (256, 16), (32, 2)]:
+        opts = json.loads(options_baseline(0))
+        opts.update({"tile_sizes": [128, bn, 32], "block_shape": [1, 1, sp], "thread_shape": [256, 1, 1],
+                     "use_shared": True, "fusion_strategy": "min"})
+        (got,), desc = run(ee, "tmm", [A, B], [np.zeros((128, 512), np.float32)], "3xtf32", opts)
+        assert f"bn={bn} splits={sp}" in desc["kernel"]
+        assert max_rel(ref, got) <= tol("3xtf32", 256)
+    # rows not a multiple of 16 bytes: no tensor-core kernel
+    A2, B2 = rng.f32((16, 30)), rng.f32((16, 30))
+    with pytest.raises(TcError) as ei:
+        run(ee, "tmm", [A2, B2], [np.zeros((16, 16), np.float32)], "tf32")
+    assert ei.value.kind == "MappingInvalid"
+    # families without a tensor-core kernel say so
+    X = rng.f32((4, 16, 16, 16))
+    Ws = [rng.f32((32, 16)) for _ in range(3)]
+    with pytest.raises(TcError) as ei:
+        run(ee, "3KRU", Ws + [X], [np.zeros((4, 32, 32, 32), np.float32), np.zeros((4, 16, 32, 32), np.float32),
+                                   np.zeros((4, 16, 16, 32), np.float32)], "tf32")
+    assert ei.value.kind == "MappingInvalid"
