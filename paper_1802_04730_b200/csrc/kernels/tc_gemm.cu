@@ -180,14 +180,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     tcFenceAfter();
     const int q = warp - 4, row = q * 32 + lane;
     float* part = reinterpret_cast<float*>(sm) + row * Cfg::kPartLd;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    if constexpr (BN % 32 == 0) {
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
-      float v[32];
-      tmemLoad32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
-      tmemLoadWait();
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmemLoad32(trow + c, v);
+        tmemLoadWait();
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<float4*>(part + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(part + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
+    } else {
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        tmemLoad16(trow + c, v);
+        tmemLoadWait();
+#pragma unroll
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(part + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      }
     }
     tcFenceBefore();
   }
@@ -315,18 +328,23 @@ bool tcGemmSupported(const GemmArgs& a, const char** why) {
 }
 
 TcPlan tcGemmPlan(int batch, int M, int N, int K, int sms) {
-  TcPlan pl;
+  // Wide N tiles first (operand bytes per MMA flop fall as BN grows, and A
+  // is re-read once per N tile), then split K across a cluster until the
+  // grid covers the SMs; narrow the tile only if splitting cannot.
   const int tilesM = (M + kBM - 1) / kBM;
   const int nkb = (K + kBK - 1) / kBK;
+  auto ctas = [&](int b) { return static_cast<int64_t>(batch) * tilesM * ((N + b - 1) / b); };
+  auto splitsFor = [&](int b) {
+    int s = 1;
+    while (s < 16 && ctas(b) * s * 2 <= sms && s * 4 <= nkb) s *= 2;  // one wave, >= 2 k-blocks per split
+    return s;
+  };
   int bn = 256;
   while (bn > 16 && bn / 2 >= N) bn /= 2;  // no wider than the problem
-  bn = std::max(16, bn);
-  auto ctas = [&](int b) { return static_cast<int64_t>(batch) * tilesM * ((N + b - 1) / b); };
-  while (bn > 32 && ctas(bn) * 2 <= sms) bn /= 2;  // spread columns before splitting K
-  int splits = 1;
-  while (splits < 16 && ctas(bn) * splits * 2 <= sms && splits * 2 <= nkb) splits *= 2;
+  while (bn > 16 && ctas(bn) * splitsFor(bn) * 2 <= sms) bn /= 2;
+  TcPlan pl;
   pl.bn = bn;
-  pl.splits = splits;
+  pl.splits = splitsFor(bn);
   return pl;
 }
 

@@ -75,8 +75,12 @@ void decodeTc(const Problem& p, const MappingOptions& o, Mapping& m) {
       invalid("tensor-core GEMM needs operand rows and batch strides that are multiples of 16 bytes");
   } else {
     if (!ok4(p.fc.ldi)) invalid("tensor-core FC layers need input rows that are multiples of 16 bytes");
-    for (const auto& L : p.fc.layers)
-      if (!ok4(L.ldw) || !ok4(L.out)) invalid("tensor-core FC layers need rows that are multiples of 16 bytes");
+    for (size_t l = 0; l < p.fc.layers.size(); ++l) {
+      const auto& L = p.fc.layers[l];
+      // a layer's output is the next layer's A operand
+      if (!ok4(L.ldw) || (l + 1 < p.fc.layers.size() && !ok4(L.out)))
+        invalid("tensor-core FC layers need rows that are multiples of 16 bytes");
+    }
   }
   m.fused = false;
   int64_t bn = o.tileSizes.size() > 1 ? o.tileSizes[1] : 0;

@@ -26,8 +26,13 @@ torch = pytest.importorskip("torch")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def tol(math, K):
-    return 1e-5 + K * 2.0 ** -23 if math == "3xtf32" else K * 2.0 ** -11
+def tol(math, K, scale=1.0):
+    """scale = max|a| * max|b| of the contraction's operands (1 for U[-1,1) inputs)."""
+    return (1e-5 + K * 2.0 ** -23 if math == "3xtf32" else K * 2.0 ** -11) * max(1.0, scale)
+
+
+def opscale(a, b):
+    return float(np.max(np.abs(a))) * float(np.max(np.abs(b)))
 
 
 def record(name, math, K, err, exact_err, oracle_exact_err):
@@ -130,7 +135,7 @@ def test_fc_chains_tc(env, math):
     ref2 = orc.fc_relu(h1, W2, B2)
     e2 = max_rel(ref2, h2)
     record("2FCRelu layer 2", math, 128, e2, None, None)
-    assert e2 <= tol(math, 128)
+    assert e2 <= tol(math, 128, opscale(h1, W2))
     O1 = rng.f32((128, 128))
     M2, C2, M3, C3b, M4, C4 = (rng.f32((64, 128)), rng.f32((64,)), rng.f32((32, 64)), rng.f32((32,)),
                                rng.f32((2, 32)), rng.f32((2,)))
@@ -141,7 +146,7 @@ def test_fc_chains_tc(env, math):
     for got, (inp, W, b, K) in zip((q2, q3, q4), ((O1, M2, C2, 128), (q2, M3, C3b, 64), (q3, M4, C4, 32))):
         e = max_rel(orc.fc_relu(inp, W, b), got)
         record(f"MLP3 layer K={K}", math, K, e, None, None)
-        assert e <= tol(math, K)
+        assert e <= tol(math, K, opscale(inp, W))
 
 
 def test_tc_explicit_plan_and_errors(env):
@@ -150,7 +155,7 @@ def test_tc_explicit_plan_and_errors(env):
     rng = orc.rng(3)
     A, B = rng.f32((128, 256)), rng.f32((512, 256))
     ref = orc.tmm(A, B)
-    for bn, sp in [(16, 1), (64, 4), (128, 8), (256, 16), (32, 2)]:
+    for bn, sp in [(16, 1), (16, 4), (64, 4), (128, 8), (256, 16), (32, 2)]:
         opts = json.loads(options_baseline(0))
         opts.update({"tile_sizes": [128, bn, 32], "block_shape": [1, 1, sp], "thread_shape": [256, 1, 1],
                      "use_shared": True, "fusion_strategy": "min"})
