@@ -340,6 +340,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="tcb", choices=["tcb", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--serial-step", action="store_true", help="run the step's operators back to back on one stream")
     ap.add_argument("--no-ops", action="store_true", help="skip the per-op paper table")
     ap.add_argument("--profile-only", action="store_true", help="run a few steps, print nothing (ncu)")
     args = ap.parse_args()
@@ -374,11 +375,24 @@ def main():
     del probe
     flops_step = sum(o.flops for o in ops)
     stream = torch.cuda.Stream(device=dev)
+    # the step's three operators are independent: inside the graph they fork
+    # onto their own streams and join back (concurrent kernels share the SMs)
+    side = [torch.cuda.Stream(device=dev) for _ in ops[1:]]
 
     with torch.cuda.stream(stream):
         def step(i):
-            for o in ops:
-                o.run(i)
+            if args.serial_step:
+                for o in ops:
+                    o.run(i)
+                return
+            for sd in side:
+                sd.wait_stream(stream)
+            ops[0].run(i)
+            for o, sd in zip(ops[1:], side):
+                with torch.cuda.stream(sd):
+                    o.run(i)
+            for sd in side:
+                stream.wait_stream(sd)
 
         # capture one CUDA graph per input set (3 launches each)
         for i in range(nsets):
@@ -489,7 +503,9 @@ def main():
         "config": {"workload": STEP_WORKLOAD + " (BASELINE.json configs[1])",
                    "global_batch": {"tbmm": 500 * world, "fc": 128 * world}, "parallelism": f"dp{world}",
                    "l2": f"{nsets} rotating input+weight sets ({nsets * set_bytes / 2**20:.0f} MiB > 2x L2)",
-                   "graphs": "one CUDA graph per input set (3 kernel launches)",
+                   "graphs": "one CUDA graph per input set (3 kernel launches)" + (
+                       ", operators serialised on one stream" if args.serial_step else
+                       ", the 3 independent operators forked onto 3 streams and joined"),
                    "flops_per_step": int(flops_step)},
         "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "us_per_step": round(e2e_t / ke * 1e6, 2)},

@@ -15,6 +15,8 @@
 // conflict-free. Tensor cores are deliberately not used here: their
 // internal accumulation order cannot reproduce the reference chain, and
 // at the paper shapes these contractions are launch- or HBM-bound.
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace tcb {
@@ -197,6 +199,139 @@ __global__ void gemm_nt_direct(const GemmArgs a, const int vec) {
   C[(int64_t)m * a.ldc + n] = acc;
 }
 
+// Persistent batched GEMM for many small independent problems (TBMM:
+// 500 batches of 26x72 · 72x26). Each CTA walks batches b = blockIdx.x +
+// j*gridDim.x; a whole batch (A[b]: M rows, B[b]: N rows, K floats each)
+// is one stage of an S-deep shared-memory ring, filled by per-row
+// cp.async.bulk copies issued up front by warp 0 and completing on the
+// stage's mbarrier — all of a CTA's first S batches are in flight before
+// any compute starts. Rows are padded to ldS ≡ 4 (mod 32) floats. Every
+// output is one thread's sequential FFMA chain in ascending k (RM x RN
+// independent chains per thread), as in gemm_nt_tiled.
+__device__ __forceinline__ unsigned smemU32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulkG2S(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smemU32(dst)),
+      "l"(src), "r"(bytes), "r"(smemU32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void barWait(uint64_t* bar, unsigned parity) {
+  const unsigned addr = smemU32(bar);
+  for (unsigned spin = 0;; ++spin) {
+    unsigned done;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spin > (1u << 24)) __trap();  // never hang: the host reports the launch failure
+  }
+}
+
+template <int RM, int RN>
+__global__ void __launch_bounds__(512) gemm_nt_batched(const GemmArgs a, const int ldS, const int S) {
+  extern __shared__ __align__(16) float smem[];
+  const int stageF = (a.M + a.N) * ldS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stageF);
+  const int tid = threadIdx.x, T = blockDim.x;
+  const int nb = (a.batch - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // batches of this CTA
+  const unsigned rowBytes = (unsigned)a.K * 4u;
+
+  auto issue = [&](int j, int s) {  // warp 0: stage s <- batch blockIdx.x + j*gridDim.x
+    const int b = blockIdx.x + j * gridDim.x;
+    const float* A = a.A + (int64_t)b * a.sA;
+    const float* B = a.B + (int64_t)b * a.sB;
+    float* dst = smem + s * stageF;
+    if (tid == 0) asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemU32(&bars[s])),
+                               "r"(rowBytes * (unsigned)(a.M + a.N))
+                               : "memory");
+    __syncwarp();
+    for (int r = tid; r < a.M + a.N; r += 32) {
+      const float* src = r < a.M ? A + (int64_t)r * a.lda : B + (int64_t)(r - a.M) * a.ldb;
+      bulkG2S(dst + r * ldS, src, rowBytes, &bars[s]);
+    }
+  };
+  if (tid < 32) {
+    if (tid == 0) {
+      for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smemU32(&bars[s])));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    for (int j = 0; j < min(S, nb); ++j) issue(j, j);
+  }
+  __syncthreads();
+
+  const int tm = (a.M + RM - 1) / RM, tn = (a.N + RN - 1) / RN, ntask = tm * tn;
+  for (int j = 0; j < nb; ++j) {
+    const int s = j % S;
+    const int b = blockIdx.x + j * gridDim.x;
+    barWait(&bars[s], (j / S) & 1);
+    const float* As = smem + s * stageF;
+    const float* Bs = As + a.M * ldS;
+    float* C = a.C + (int64_t)b * a.sC;
+    for (int t = tid; t < ntask; t += T) {
+      const int ti = t / tn, tj = t % tn;
+      int mr[RM], nr[RN];
+#pragma unroll
+      for (int i = 0; i < RM; ++i) mr[i] = min(ti * RM + i, a.M - 1);  // clamped reads, masked stores
+#pragma unroll
+      for (int q = 0; q < RN; ++q) nr[q] = min(tj * RN + q, a.N - 1);
+      float acc[RM][RN];
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int q = 0; q < RN; ++q) acc[i][q] = initValue(a, C, mr[i], nr[q]);
+      int kk = 0;
+      for (; kk + 4 <= a.K; kk += 4) {
+        float4 av[RM], bv[RN];
+#pragma unroll
+        for (int i = 0; i < RM; ++i) av[i] = *reinterpret_cast<const float4*>(As + mr[i] * ldS + kk);
+#pragma unroll
+        for (int q = 0; q < RN; ++q) bv[q] = *reinterpret_cast<const float4*>(Bs + nr[q] * ldS + kk);
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int q = 0; q < RN; ++q) {
+            acc[i][q] = __fmaf_rn(av[i].x, bv[q].x, acc[i][q]);
+            acc[i][q] = __fmaf_rn(av[i].y, bv[q].y, acc[i][q]);
+            acc[i][q] = __fmaf_rn(av[i].z, bv[q].z, acc[i][q]);
+            acc[i][q] = __fmaf_rn(av[i].w, bv[q].w, acc[i][q]);
+          }
+      }
+      for (; kk < a.K; ++kk)
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int q = 0; q < RN; ++q) acc[i][q] = __fmaf_rn(As[mr[i] * ldS + kk], Bs[nr[q] * ldS + kk], acc[i][q]);
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int q = 0; q < RN; ++q) {
+          const int m = ti * RM + i, n = tj * RN + q;
+          if (m < a.M && n < a.N) {
+            float v = acc[i][q];
+            if (a.relu) v = fmaxf(v, 0.0f);
+            C[(int64_t)m * a.ldc + n] = v;
+          }
+        }
+    }
+    __syncthreads();  // stage s fully consumed
+    if (tid < 32 && j + S < nb) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async refill
+      issue(j + S, s);
+    }
+  }
+}
+
+int batchedLd(int K) {
+  int l = (K + 3) & ~3;
+  while (l % 32 != 4) l += 4;
+  return l;
+}
+
 const GemmVariant kGemmVariants[] = {
     {0, 0, 0, 1, 1, 0, "direct"},
     {1, 16, 16, 1, 1, 32, "t16x16_r1x1_k32"},
@@ -217,7 +352,34 @@ const GemmVariant kGemmVariants[] = {
     {16, 32, 32, 2, 2, 32, "t32x32_r2x2_k32_s8", 8},
     {17, 16, 32, 2, 2, 32, "t16x32_r2x2_k32_s8", 8},
     {18, 16, 16, 1, 1, 64, "t16x16_r1x1_k64"},
+    // persistent batched (tk = 0 marks "whole reduction per stage")
+    {19, 1, 1, 2, 2, 0, "batched_r2x2", 0},
+    {20, 1, 1, 1, 1, 0, "batched_r1x1", 0},
+    {21, 1, 1, 2, 1, 0, "batched_r2x1", 0},
+    {22, 1, 1, 1, 2, 0, "batched_r1x2", 0},
 };
+
+template <int RM, int RN>
+cudaError_t launchBatched(const GemmArgs& a, int grid, cudaStream_t s) {
+  const int ldS = batchedLd(a.K);
+  const size_t stageB = (size_t)(a.M + a.N) * ldS * 4;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (grid <= 0) grid = std::min(a.batch, 2 * sms);
+  grid = std::min(grid, a.batch);
+  const int perCta = (a.batch + grid - 1) / grid;
+  int S = std::min(4, perCta);
+  while (S > 1 && S * stageB + 64 > 100 * 1024) --S;
+  const size_t smem = S * stageB + 8 * S;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  const int ntask = ((a.M + RM - 1) / RM) * ((a.N + RN - 1) / RN);
+  const int threads = std::max(32, std::min(512, (ntask + 31) / 32 * 32));
+  auto kfn = gemm_nt_batched<RM, RN>;
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kfn<<<grid, threads, smem, s>>>(a, ldS, S);
+  return cudaGetLastError();
+}
 
 template <int TM, int TN, int RM, int RN, int TK, int S = 4>
 cudaError_t launchTiled(const GemmArgs& a, int vec, cudaStream_t s) {
@@ -236,6 +398,12 @@ cudaError_t launchTiled(const GemmArgs& a, int vec, cudaStream_t s) {
 }  // namespace
 
 int gemmVariantCount() { return sizeof(kGemmVariants) / sizeof(kGemmVariants[0]); }
+
+bool batchedOk(const GemmArgs& a) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (a.K % 4 || a.lda % 4 || a.ldb % 4 || a.sA % 4 || a.sB % 4 || !al16(a.A) || !al16(a.B)) return false;
+  return (size_t)(a.M + a.N) * batchedLd(a.K) * 4 + 64 <= 100 * 1024;
+}
 const GemmVariant& gemmVariant(int i) { return kGemmVariants[i]; }
 
 cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t s) {
@@ -268,6 +436,17 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
     case 16: return launchTiled<32, 32, 2, 2, 32, 8>(a, vec, s);
     case 17: return launchTiled<16, 32, 2, 2, 32, 8>(a, vec, s);
     case 18: return launchTiled<16, 16, 1, 1, 64>(a, vec, s);
+    case 19:
+    case 20:
+    case 21:
+    case 22: {
+      if (!batchedOk(a)) return cudaErrorInvalidValue;
+      const int g = threads;  // the batched variants take their grid size here (0 = auto)
+      if (variant == 19) return launchBatched<2, 2>(a, g, s);
+      if (variant == 20) return launchBatched<1, 1>(a, g, s);
+      if (variant == 21) return launchBatched<2, 1>(a, g, s);
+      return launchBatched<1, 2>(a, g, s);
+    }
     default: return cudaErrorInvalidValue;
   }
 }

@@ -40,8 +40,12 @@ struct GemmVariant {
 };
 int gemmVariantCount();
 const GemmVariant& gemmVariant(int i);
-// threads: only used by the direct variant (≥32, multiple of 32, ≤1024)
+// threads: the direct variant's block size (≥32, multiple of 32, ≤1024);
+// for the persistent batched variants (tk == 0) the grid size (0 = auto)
 cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t s);
+// whether the persistent batched variants can take this problem (16-byte
+// rows/strides/pointers, one batch's operands fit a shared-memory stage)
+bool batchedOk(const GemmArgs& a);
 
 // ------------------------------------------------- GEMM-NT, tensor cores
 // tcgen05 .kind::tf32 variant of the same contraction (tc_gemm.cu). Not

@@ -106,6 +106,21 @@ void decodeGemm(const MappingOptions& o, Mapping& m) {
     return;
   }
   if (o.tileSizes.size() < 3) invalid("tiled GEMM needs three tile sizes (rows, cols, reduction depth)");
+  if (o.tileSizes[2] == 1) {
+    // reduction depth 1 = stage a whole batch per step: the persistent
+    // batched kernel, micro-tile tile_sizes[0] x tile_sizes[1], grid
+    // block_shape[0] (1 = one or two CTAs per SM)
+    const int rm = static_cast<int>(o.tileSizes[0]), rn = static_cast<int>(o.tileSizes[1]);
+    for (int i = 1; i < k::gemmVariantCount(); ++i) {
+      const auto& v = k::gemmVariant(i);
+      if (v.tk == 0 && v.rm == rm && v.rn == rn) {
+        m.gemmVariant = i;
+        m.gemmThreads = o.blockShape[0] > 1 ? static_cast<int>(o.blockShape[0]) : 0;
+        return;
+      }
+    }
+    invalid("persistent batched GEMM micro-tile must be 1x1, 1x2, 2x1 or 2x2");
+  }
   if (o.threadShape[2] != 1) invalid("tiled GEMM uses a 2-D thread block");
   int64_t tm = o.tileSizes[0], tn = o.tileSizes[1], tk = o.tileSizes[2];
   int64_t tx = o.threadShape[0], ty = o.threadShape[1];
@@ -148,6 +163,10 @@ void launchGemmDesc(const GemmDesc& g, const Mapping& m, void* const* in, void* 
     if (!k::tcGemmSupported(a, &why)) fail(ErrorKind::MappingInvalid, why);
     k::TcPlan pl = m.tcAuto ? k::tcGemmPlan(g.batch, g.M, g.N, g.K, smCount()) : m.tc;
     e = k::launchTcGemm(a, m.math, pl, s);
+  } else if (k::gemmVariant(m.gemmVariant).tk == 0 && !k::batchedOk(a)) {
+    // the persistent batched kernel needs 16-byte aligned operands; the
+    // tiled kernel computes the same bit-exact chains without that need
+    e = k::launchGemm(a, 4, 256, s);
   } else {
     e = k::launchGemm(a, m.gemmVariant, m.gemmThreads, s);
   }
@@ -192,7 +211,10 @@ std::string Mapping::describe() const {
   }
   switch (family) {
     case Family::Gemm:
-      os << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
+      if (k::gemmVariant(gemmVariant).tk == 0)
+        os << k::gemmVariant(gemmVariant).name << " grid=" << (gemmThreads ? std::to_string(gemmThreads) : "auto");
+      else
+        os << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
       break;
     case Family::FcChain:
       if (fused) os << "cluster rows=" << rows << " cn=" << cn << " threads=" << threads;
@@ -473,6 +495,15 @@ MappingOptions defaultOptions(const Problem& p, int math) {
       // 8-deep copy ring when the reduction is long
       o = baselineOptions()[0];
       const GemmDesc& g = p.gemm;
+      if (g.batch > 1 && g.K % 4 == 0 && g.lda % 4 == 0 && g.ldb % 4 == 0 && g.sA % 4 == 0 && g.sB % 4 == 0 &&
+          (g.M + g.N) * (int64_t)((g.K + 3) / 4 * 4 + 32) * 4 <= 96 * 1024) {
+        // many small independent problems (TBMM): persistent batched kernel
+        o.tileSizes = {2, 2, 1};
+        o.threadShape = {{256, 1, 1}};
+        o.blockShape = {{1, 1, 1}};
+        o.unrollCopyShared = false;
+        break;
+      }
       auto ctas = [&](int tm, int tn) { return (double)g.batch * ((g.M + tm - 1) / tm) * ((g.N + tn - 1) / tn); };
       o.unrollCopyShared = g.K > 128;
       if (ctas(32, 32) < 148) {
@@ -552,6 +583,11 @@ GenePools genePools(const Problem& p) {
       g.tile0 = {16, 32, 64};
       g.tile1 = {16, 32, 64};
       g.tile2 = {16, 32, 64};
+      if (p.family == Family::Gemm && p.gemm.batch > 1) {  // + the persistent batched kernel
+        g.tile0 = {1, 2, 16, 32, 64};
+        g.tile1 = {1, 2, 16, 32, 64};
+        g.tile2 = {1, 16, 32, 64};
+      }
       g.tx = {4, 8, 16, 32};
       g.ty = {4, 8, 16, 32};
       g.tz = {1};

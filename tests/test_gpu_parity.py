@@ -103,6 +103,31 @@ def test_every_gemm_variant_identical(engine, oracle, golden, name):
     assert ran == len(variants) + 1
 
 
+@pytest.mark.parametrize("name", ["tbmm_small", "tbmm_paper"])
+def test_batched_persistent_variants(engine, oracle, golden, name):
+    """The persistent batched kernel (tile_sizes[2] == 1) at every micro-tile
+    and several grid sizes (1 CTA walking every batch, ragged splits, more
+    CTAs than batches) gives the reference's bits."""
+    case, ins, seeded = case_inputs(oracle, golden, name)
+    ref = oracle_outputs(oracle, case, ins, seeded)
+    base = json.loads(
+        '{"block_shape":[1,1,1],"fusion_strategy":"max","rng_seed":0,"shared_memory_budget":49152,'
+        '"thread_shape":[256,1,1],"tile_sizes":[2,2,1],"unroll_copy_shared":false,"unroll_factor":1,'
+        '"use_private":true,"use_shared":true}')
+    for rm, rn in [(1, 1), (1, 2), (2, 1), (2, 2)]:
+        for grid in [1, 3, 7, 296, 1000]:
+            o = dict(base)
+            o["tile_sizes"] = [rm, rn, 1]
+            o["block_shape"] = [grid, 1, 1]
+            got, h = run_on_gpu(engine, case["def"], ins, seeded, options=o)
+            assert "batched" in engine.describe(h)["kernel"]
+            for k in case["outputs"]:
+                assert_exact(oracle, f"{name}/{rm}x{rn}/grid{grid}", k, got[k], case["outputs"][k]["fnv"], ref[k])
+    # the default for a batched contraction is the persistent kernel
+    got, h = run_on_gpu(engine, case["def"], ins, seeded)
+    assert "batched" in engine.describe(h)["kernel"]
+
+
 @pytest.mark.parametrize("rows,cn,threads", [(1, 1, 64), (2, 2, 64), (4, 8, 64), (8, 8, 64), (8, 4, 256),
                                              (16, 8, 128), (3, 3, 96), (8, 16, 64)])
 def test_fc_chain_cluster_variants(engine, oracle, golden, rows, cn, threads):
