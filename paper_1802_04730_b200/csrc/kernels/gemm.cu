@@ -239,12 +239,24 @@ __global__ void __launch_bounds__(512) gemm_nt_batched(const GemmArgs a, const i
   const int tid = threadIdx.x, T = blockDim.x;
   const int nb = (a.batch - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // batches of this CTA
   const unsigned rowBytes = (unsigned)a.K * 4u;
+  // dense operands (row stride == K, landing unpadded): one copy per operand
+  const bool dense = ldS == a.K && a.lda == a.K && a.ldb == a.K;
 
   auto issue = [&](int j, int s) {  // warp 0: stage s <- batch blockIdx.x + j*gridDim.x
     const int b = blockIdx.x + j * gridDim.x;
     const float* A = a.A + (int64_t)b * a.sA;
     const float* B = a.B + (int64_t)b * a.sB;
     float* dst = smem + s * stageF;
+    if (dense) {
+      if (tid == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemU32(&bars[s])),
+                     "r"(rowBytes * (unsigned)(a.M + a.N))
+                     : "memory");
+        bulkG2S(dst, A, rowBytes * a.M, &bars[s]);
+        bulkG2S(dst + a.M * ldS, B, rowBytes * a.N, &bars[s]);
+      }
+      return;
+    }
     if (tid == 0) asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemU32(&bars[s])),
                                "r"(rowBytes * (unsigned)(a.M + a.N))
                                : "memory");
@@ -254,15 +266,13 @@ __global__ void __launch_bounds__(512) gemm_nt_batched(const GemmArgs a, const i
       bulkG2S(dst + r * ldS, src, rowBytes, &bars[s]);
     }
   };
-  if (tid < 32) {
-    if (tid == 0) {
-      for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smemU32(&bars[s])));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    for (int j = 0; j < min(S, nb); ++j) issue(j, j);
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smemU32(&bars[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  __syncthreads();  // barrier inits visible; copies are issued below while the other warps start waiting
+  if (tid < 32)
+    for (int j = 0; j < min(S, nb); ++j) issue(j, j);
 
   const int tm = (a.M + RM - 1) / RM, tn = (a.N + RN - 1) / RN, ntask = tm * tn;
   for (int j = 0; j < nb; ++j) {
@@ -273,7 +283,7 @@ __global__ void __launch_bounds__(512) gemm_nt_batched(const GemmArgs a, const i
     const float* Bs = As + a.M * ldS;
     float* C = a.C + (int64_t)b * a.sC;
     for (int t = tid; t < ntask; t += T) {
-      const int ti = t / tn, tj = t % tn;
+      const int ti = t % tm, tj = t / tm;  // consecutive lanes walk A rows (B rows broadcast)
       int mr[RM], nr[RN];
 #pragma unroll
       for (int i = 0; i < RM; ++i) mr[i] = min(ti * RM + i, a.M - 1);  // clamped reads, masked stores
@@ -294,12 +304,19 @@ __global__ void __launch_bounds__(512) gemm_nt_batched(const GemmArgs a, const i
 #pragma unroll
         for (int i = 0; i < RM; ++i)
 #pragma unroll
-          for (int q = 0; q < RN; ++q) {
-            acc[i][q] = __fmaf_rn(av[i].x, bv[q].x, acc[i][q]);
-            acc[i][q] = __fmaf_rn(av[i].y, bv[q].y, acc[i][q]);
-            acc[i][q] = __fmaf_rn(av[i].z, bv[q].z, acc[i][q]);
-            acc[i][q] = __fmaf_rn(av[i].w, bv[q].w, acc[i][q]);
-          }
+          for (int q = 0; q < RN; ++q) acc[i][q] = __fmaf_rn(av[i].x, bv[q].x, acc[i][q]);
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int q = 0; q < RN; ++q) acc[i][q] = __fmaf_rn(av[i].y, bv[q].y, acc[i][q]);
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int q = 0; q < RN; ++q) acc[i][q] = __fmaf_rn(av[i].z, bv[q].z, acc[i][q]);
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int q = 0; q < RN; ++q) acc[i][q] = __fmaf_rn(av[i].w, bv[q].w, acc[i][q]);
       }
       for (; kk < a.K; ++kk)
 #pragma unroll
@@ -361,7 +378,10 @@ const GemmVariant kGemmVariants[] = {
 
 template <int RM, int RN>
 cudaError_t launchBatched(const GemmArgs& a, int grid, cudaStream_t s) {
-  const int ldS = batchedLd(a.K);
+  // dense per-batch operands land with one copy each, unpadded; otherwise
+  // one copy per row into rows padded to ldS = 4 (mod 32)
+  const bool dense = a.lda == a.K && a.ldb == a.K;
+  const int ldS = dense ? a.K : batchedLd(a.K);
   const size_t stageB = (size_t)(a.M + a.N) * ldS * 4;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
