@@ -363,7 +363,9 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     peaks, peak_src = load_peaks()
     peaks = dict(peaks)
-    peaks["ffma_tflops"] = round(measure_peaks(local)["ffma_tflops"], 2)  # measured now, this GPU
+    mp = measure_peaks(local)  # measured now, this GPU
+    peaks["ffma_tflops"] = round(mp["ffma_tflops"], 2)
+    peaks["launch_floor_us"] = {k: round(v, 3) for k, v in mp["launch_floor_us"].items()}
     ee = ExecutionEngine()
 
     # rotating input sets larger than L2 (inputs AND weights rotate)
@@ -514,7 +516,9 @@ def main():
         "step_ops": roofline_ops,
         "clocks": clk.summary(),
         "peaks": {"hbm_gbs": hbm_peak, "hbm_source": peak_src, "ffma_tflops": peaks["ffma_tflops"],
-                  "ffma_source": "measured in this run (tcb_measure_peaks: fma.rn.f32 chains, all SMs)"},
+                  "ffma_source": "measured in this run (tcb_measure_peaks: fma.rn.f32 chains, all SMs)",
+                  "launch_floor_us": peaks["launch_floor_us"],
+                  "launch_floor_source": "empty kernels replayed back to back from a CUDA graph (CTAs x threads)"},
         "device": device_info(local),
     }
     if not args.no_ops:

@@ -173,8 +173,14 @@ int tcb_measure_peaks(int dev, char* buf, int len) {
     double ffma = 0;
     float ms = 0;
     cudaOk(k::probeFfma(p.multiProcessorCount, &ffma, &ms), "ffma probe");
+    double l1 = 0, l148 = 0, lcl = 0;
+    cudaOk(k::probeLaunch(1, 32, 1, &l1), "launch probe");
+    cudaOk(k::probeLaunch(2 * p.multiProcessorCount, 256, 1, &l148), "launch probe");
+    cudaOk(k::probeLaunch(256, 64, 8, &lcl), "launch probe");
     std::ostringstream os;
     os << "{\"ffma_tflops\": " << ffma << ", \"ffma_probe_ms\": " << ms
+       << ", \"launch_floor_us\": {\"1x32\": " << l1 << ", \"" << 2 * p.multiProcessorCount
+       << "x256\": " << l148 << ", \"256x64_cluster8\": " << lcl << "}"
        << ", \"sms\": " << p.multiProcessorCount << "}";
     copyOut(os.str(), buf, len);
   });

@@ -37,7 +37,9 @@ struct FcPlan {
   int ald[kMaxLayers + 1];  // padded row stride of layer l's input activations (floats)
   int wld[kMaxLayers];      // weight-slice row stride: kred rounded up to 4 (dense when kred%4==0)
   int offW[kMaxLayers];     // weight slices [cols][wld] (floats)
-  int offAct0, offActA, offActB, offBar;
+  int offAct[kMaxLayers];   // [0]: input rows; [l>0]: layer l-1's output = layer l's input
+  int offBar;
+  int denseIn;              // input rows land unpadded with one copy (ald[0] == kred, conflict-free)
   int bulk;                 // 1: cp.async.bulk path, 0: cooperative loads
 };
 
@@ -76,12 +78,7 @@ __device__ __forceinline__ void mbarWait(uint64_t* bar, unsigned parity, int tag
         : "r"(addr), "r"(parity)
         : "memory");
     if (done) return;
-    if (spin > (1u << 22)) {
-      if ((threadIdx.x & 31) == 0)
-        printf("tc-b200: mbarrier %d never completed (block %d,%d thread %d)\n", tag, blockIdx.x, blockIdx.y,
-               threadIdx.x);
-      __trap();
-    }
+    if (spin > (1u << 22)) __trap();  // never hang: the host reports the launch failure
   }
 }
 __device__ __forceinline__ void bulkCopy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
@@ -119,6 +116,17 @@ __device__ __forceinline__ float fma4(float4 x, float4 w, float acc) {
   acc = __fmaf_rn(x.y, w.y, acc);
   acc = __fmaf_rn(x.z, w.z, acc);
   return __fmaf_rn(x.w, w.w, acc);
+}
+
+// remote store that completes `bytes` on the destination CTA's mbarrier
+// (st.async): the consumer waits on its own barrier, no cluster barrier
+__device__ __forceinline__ void stAsyncCluster(const float* local, const uint64_t* localBar, unsigned rank, float v) {
+  unsigned ra, rb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smemAddr(local)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smemAddr(localBar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(ra),
+               "r"(__float_as_uint(v)), "r"(rb)
+               : "memory");
 }
 
 __device__ __forceinline__ void stCluster(float* local, unsigned rank, float v) {
@@ -192,53 +200,94 @@ __device__ unsigned long long g_fc_trace[1024][16];
   } while (0)
 #endif
 
-__global__ void __launch_bounds__(1024) fc_cluster_kernel(const FcChainArgs a, const FcPlan p) {
+// __grid_constant__: the layer loop indexes a.L[l] / p.*[l] dynamically;
+// without it those reads go through a local-memory copy of the parameters
+__global__ void __launch_bounds__(1024)
+    fc_cluster_kernel(const __grid_constant__ FcChainArgs a, const __grid_constant__ FcPlan p) {
   FC_GSTAMP(13);
   FC_STAMP(0);
   extern __shared__ __align__(128) float sm[];
   const int tid = threadIdx.x, T = blockDim.x, R = p.R;
-  const int rank = p.cn > 1 ? static_cast<int>(clusterRank()) : 0;
+  const int cn = p.cn, layers = a.layers;
+  const int rank = cn > 1 ? static_cast<int>(clusterRank()) : 0;
   const int row0 = blockIdx.y * R;
   const int rows = min(R, a.batch - row0);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + p.offBar);  // [0]: input rows, [1+l]: layer l weights
+  // bars[l]: layer l's input activations landed; bars[layers + l]: layer l's weight slice landed
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + p.offBar);
 
-  // ---- every load of the kernel is issued up front by warp 0
+  // first-pass bias of every layer, loaded now so its latency hides behind
+  // the weight copies (each chain starts from its bias)
+  float biasPre[kMaxLayers];
+#pragma unroll
+  for (int l = 0; l < kMaxLayers; ++l) {
+    const int c = tid / R, c0 = rank * (l < layers ? p.cols[l] : 0);
+    biasPre[l] = (l < layers && tid < R * p.cols[l] && c0 + c < a.L[l].out) ? __ldg(a.L[l].bias + c0 + c) : 0.0f;
+  }
+  if (tid == 0) {
+    for (int b = 0; b < 2 * layers; ++b) mbarInit(&bars[b], 1);
+    // the pushed activations of every later layer: R rows x all columns
+    // (armed before any peer can push: see the cluster arrive below)
+    for (int l = 1; l < layers; ++l) mbarExpectTx(&bars[l], (unsigned)(R * a.L[l - 1].out * 4));
+    FC_STAMP(1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    FC_STAMP(5);
+  }
+  __syncthreads();  // inits visible inside the CTA
+  FC_STAMP(8);
+  // Peers push layer outputs into this CTA's activation buffers and complete
+  // them on this CTA's barriers, so every CTA of the cluster must have
+  // initialised its barriers before the first push: arrive now, wait right
+  // before pushing (the weight loads and layer 0 hide the barrier).
+  if (cn > 1) asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+  FC_STAMP(11);
+
+  // ---- every global load of the kernel is issued up front. A bulk copy
+  // costs the issuing thread ~200 cycles, so the copies are dealt round-robin
+  // to lane 0 of every warp (copy j -> warp j % warps) and issue in parallel.
   if (p.bulk) {
-    if (tid < 32) {
-      for (int b = tid; b <= a.layers; b += 32) mbarInit(&bars[b], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      __syncwarp();
-      const int lane = tid;
-      const unsigned rowBytes = (unsigned)a.L[0].kred * 4u;
-      if (lane == 0) mbarExpectTx(&bars[0], rowBytes * rows);
-      for (int l = lane; l < a.layers; l += 32) {
+    const int warp = tid >> 5, nw = (T + 31) >> 5, lane = tid & 31;
+    const unsigned rowBytes = (unsigned)a.L[0].kred * 4u;
+    if (tid == 0) {
+      mbarExpectTx(&bars[0], rowBytes * rows);
+      for (int l = 0; l < layers; ++l) {
         const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
-        mbarExpectTx(&bars[1 + l], (unsigned)(a.L[l].kred * 4 * nc));
+        mbarExpectTx(&bars[layers + l], (unsigned)(a.L[l].kred * 4 * nc));
       }
-      __syncwarp();
-      for (int r = lane; r < rows; r += 32)
-        bulkCopy(sm + p.offAct0 + r * p.ald[0], a.I + (int64_t)(row0 + r) * a.ldi, rowBytes, &bars[0]);
-      for (int l = 0; l < a.layers; ++l) {
+    }
+    __syncthreads();  // expectations armed before any copy can complete
+    FC_STAMP(12);
+    if (lane == 0) {
+      int j = 0;  // global copy index
+      if (p.denseIn) {  // the CTA's input rows are one contiguous block
+        if (j++ % nw == warp) bulkCopy(sm + p.offAct[0], a.I + (int64_t)row0 * a.ldi, rowBytes * rows, &bars[0]);
+      } else {
+        for (int r = 0; r < rows; ++r)
+          if (j++ % nw == warp)
+            bulkCopy(sm + p.offAct[0] + r * p.ald[0], a.I + (int64_t)(row0 + r) * a.ldi, rowBytes, &bars[0]);
+      }
+      for (int l = 0; l < layers; ++l) {
         const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
         if (nc == 0) continue;
         const float* src = a.L[l].W + (int64_t)c0 * a.L[l].ldw;
         if (a.L[l].ldw == a.L[l].kred) {  // the slice is one contiguous block
-          if (lane == (l + rows) % 32) bulkCopy(sm + p.offW[l], src, (unsigned)(nc * a.L[l].kred * 4), &bars[1 + l]);
+          if (j++ % nw == warp) bulkCopy(sm + p.offW[l], src, (unsigned)(nc * a.L[l].kred * 4), &bars[layers + l]);
         } else {
-          for (int j = lane; j < nc; j += 32)
-            bulkCopy(sm + p.offW[l] + j * p.wld[l], src + (int64_t)j * a.L[l].ldw, a.L[l].kred * 4, &bars[1 + l]);
+          for (int q = 0; q < nc; ++q)
+            if (j++ % nw == warp)
+              bulkCopy(sm + p.offW[l] + q * p.wld[l], src + (int64_t)q * a.L[l].ldw, a.L[l].kred * 4,
+                       &bars[layers + l]);
         }
       }
     }
     // input rows past the batch end are zero
-    for (int e = tid; e < (R - rows) * p.ald[0]; e += T) sm[p.offAct0 + rows * p.ald[0] + e] = 0.0f;
-    __syncthreads();  // barrier inits visible to every thread
+    for (int e = tid; e < (R - rows) * p.ald[0]; e += T) sm[p.offAct[0] + rows * p.ald[0] + e] = 0.0f;
+    if (rows < R) __syncthreads();
   } else {
     for (int e = tid; e < R * p.ald[0]; e += T) {
       int r = e / p.ald[0], kk = e % p.ald[0];
-      sm[p.offAct0 + e] = (r < rows && kk < a.L[0].kred) ? a.I[(int64_t)(row0 + r) * a.ldi + kk] : 0.0f;
+      sm[p.offAct[0] + e] = (r < rows && kk < a.L[0].kred) ? a.I[(int64_t)(row0 + r) * a.ldi + kk] : 0.0f;
     }
-    for (int l = 0; l < a.layers; ++l) {
+    for (int l = 0; l < layers; ++l) {
       const int c0 = rank * p.cols[l];
       for (int e = tid; e < p.cols[l] * p.wld[l]; e += T) {
         int j = e / p.wld[l], kk = e % p.wld[l];
@@ -251,20 +300,16 @@ __global__ void __launch_bounds__(1024) fc_cluster_kernel(const FcChainArgs a, c
   FC_STAMP(2);
 
 #pragma unroll 1
-  for (int l = 0; l < a.layers; ++l) {
+  for (int l = 0; l < layers; ++l) {
     const FcLayer L = a.L[l];
     const int cols = p.cols[l], c0 = rank * cols;
-    const bool last = l + 1 == a.layers;
-    // layer l reads buffer in(l), writes buffer in(l+1) in every cluster CTA
-    const int inOff = l == 0 ? p.offAct0 : ((l & 1) ? p.offActA : p.offActB);
-    const int outOff = (l & 1) ? p.offActB : p.offActA;
-    const int ald = p.ald[l], ldn = p.ald[l + 1];
-    const unsigned actBase = smemAddr(sm + inOff), wBase = smemAddr(sm + p.offW[l]);
-    if (p.bulk) {
-      if (l == 0) mbarWait(&bars[0], 0, 0);
-      mbarWait(&bars[1 + l], 0, 1 + l);
-    }
+    const bool last = l + 1 == layers;
+    const int ald = p.ald[l];
+    const unsigned actBase = smemAddr(sm + p.offAct[l]), wBase = smemAddr(sm + p.offW[l]);
+    if (l > 0 || p.bulk) mbarWait(&bars[l], 0, l);
+    if (p.bulk) mbarWait(&bars[layers + l], 0, layers + l);
     FC_STAMP(3 + 3 * l);
+    if (!last && l == 0 && cn > 1) asm volatile("barrier.cluster.wait;" ::: "memory");
     const int nchains = R * cols;
     for (int base = 0; base < nchains; base += T) {
       // one (row, column) chain per thread and pass, row fastest; idle
@@ -272,28 +317,24 @@ __global__ void __launch_bounds__(1024) fc_cluster_kernel(const FcChainArgs a, c
       const int idx = base + tid;
       const bool live = idx < nchains && c0 + idx / R < L.out;
       const int r = live ? idx % R : 0, c = live ? idx / R : 0;
-      float acc = live ? __ldg(L.bias + c0 + c) : 0.0f;
+      float bpre = 0.0f;
+#pragma unroll
+      for (int q = 0; q < kMaxLayers; ++q)
+        if (q == l) bpre = biasPre[q];  // static register indexing
+      float acc = !live ? 0.0f : base == 0 ? bpre : __ldg(L.bias + c0 + c);
       acc = chainSegment(actBase + (unsigned)(r * ald) * 4u, wBase + (unsigned)(c * p.wld[l]) * 4u, L.kred, acc);
       if (live) {
         const float v = fmaxf(acc, 0.0f);
         if (r < rows) L.O[(int64_t)(row0 + r) * L.out + c0 + c] = v;
-        if (!last) {  // push into the next layer's input of every cluster CTA
-          float* dst = sm + outOff + r * ldn + c0 + c;
-          if (p.cn > 1) {
-            for (int q = 0; q < p.cn; ++q) stCluster(dst, q, v);
-          } else {
-            *dst = v;
-          }
+        if (!last) {  // push into the next layer's input buffer of every cluster CTA
+          const float* dst = sm + p.offAct[l + 1] + r * p.ald[l + 1] + c0 + c;
+          for (int q = 0; q < cn; ++q) stAsyncCluster(dst, &bars[l + 1], q, v);
         }
       }
     }
     FC_STAMP(4 + 3 * l);
-    if (!last) {
-      if (p.cn > 1) clusterSync();  // release/acquire: every peer's pushes landed
-      else __syncthreads();
-      FC_STAMP(5 + 3 * l);
-    }
   }
+  if (cn > 1 && layers == 1) asm volatile("barrier.cluster.wait;" ::: "memory");  // pair the arrive
   FC_STAMP(15);
   FC_GSTAMP(14);
 }
@@ -313,18 +354,33 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p) {
     p.offW[l] = off;
     off += p.cols[l] * p.wld[l] + 32;
   }
-  for (int l = 0; l <= a.layers; ++l) p.ald[l] = padRow(l < a.layers ? a.L[l].kred : a.L[l - 1].out);
-  int aldMax = 0;
-  for (int l = 1; l <= a.layers; ++l) aldMax = p.ald[l] > aldMax ? p.ald[l] : aldMax;
-  p.offAct0 = off;
-  off += R * p.ald[0] + 32;
-  p.offActA = off;
-  off += R * aldMax + 32;
-  p.offActB = off;
-  off += R * aldMax + 32;
+  // layer l >= 1 reads kred_l columns of rows that receive all out_{l-1} pushed columns
+  for (int l = 0; l <= a.layers; ++l) {
+    int w = l < a.layers ? a.L[l].kred : a.L[l - 1].out;
+    if (l > 0 && l < a.layers && a.L[l - 1].out > w) w = a.L[l - 1].out;
+    p.ald[l] = padRow(w);
+  }
+  // dense input rows (one bulk copy) when the unpadded row stride already
+  // puts the up-to-8 rows of an LDS.128 wavefront in distinct 16-byte bank groups
+  {
+    const int k0 = a.L[0].kred, nr = R < 8 ? R : 8;
+    bool ok = a.ldi == k0 && k0 % 4 == 0;
+    unsigned seen = 0;
+    for (int r = 0; r < nr && ok; ++r) {
+      const unsigned g = 1u << (((r * k0) / 4) % 8);
+      ok = !(seen & g);
+      seen |= g;
+    }
+    p.denseIn = ok ? 1 : 0;
+    if (ok) p.ald[0] = k0;
+  }
+  for (int l = 0; l < a.layers; ++l) {  // one buffer per layer boundary: never reused, so no
+    p.offAct[l] = off;                   // "buffer free" handshake between cluster CTAs
+    off += R * p.ald[l] + 32;
+  }
   off = (off + 3) & ~3;  // 16-byte alignment for the mbarriers
   p.offBar = off;
-  off += 2 * (1 + a.layers);  // uint64 barriers
+  off += 2 * (2 * a.layers);  // uint64 barriers: [l]: activations of layer l, [layers + l]: weights of layer l
   bool bulk = (a.ldi % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.I) & 15) == 0);
   for (int l = 0; l < a.layers; ++l)
     bulk = bulk && (a.L[l].kred % 4 == 0) && (a.L[l].ldw % 4 == 0) &&

@@ -125,6 +125,8 @@ cudaError_t launchLut(const LutArgs* tables, int ntables, int threads, cudaStrea
 // ---------------------------------------------------------------- probes
 // fp32 FFMA throughput of the whole device (TFLOP/s, 2 flops per FMA)
 cudaError_t probeFfma(int sms, double* tflops, float* ms);
+// device µs per launch of back-to-back empty kernels in a CUDA graph
+cudaError_t probeLaunch(int ctas, int threads, int cluster, double* us);
 
 }  // namespace k
 }  // namespace tcb

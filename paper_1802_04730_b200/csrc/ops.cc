@@ -495,15 +495,7 @@ MappingOptions defaultOptions(const Problem& p, int math) {
       // 8-deep copy ring when the reduction is long
       o = baselineOptions()[0];
       const GemmDesc& g = p.gemm;
-      if (g.batch > 1 && g.K % 4 == 0 && g.lda % 4 == 0 && g.ldb % 4 == 0 && g.sA % 4 == 0 && g.sB % 4 == 0 &&
-          (g.M + g.N) * (int64_t)((g.K + 3) / 4 * 4 + 32) * 4 <= 96 * 1024) {
-        // many small independent problems (TBMM): persistent batched kernel
-        o.tileSizes = {2, 2, 1};
-        o.threadShape = {{256, 1, 1}};
-        o.blockShape = {{1, 1, 1}};
-        o.unrollCopyShared = false;
-        break;
-      }
+
       auto ctas = [&](int tm, int tn) { return (double)g.batch * ((g.M + tm - 1) / tm) * ((g.N + tn - 1) / tn); };
       o.unrollCopyShared = g.K > 128;
       if (ctas(32, 32) < 148) {

@@ -50,8 +50,8 @@ static void run(const char* label, FcChainArgs a, int rows, int cn, int threads)
   cudaMemcpyFromSymbol(tr, g_fc_trace, sizeof(tr));
   int nblk = cn * ((a.batch + rows - 1) / rows);
   printf("%s: %s  %.2f us  (%d CTAs)\n", label, cudaGetErrorString(err), ms * 1e3, nblk);
-  const char* names[16] = {"start", "-", "copies_issued", "L0_data", "L0_done", "L0_csync", "L1_data",
-                           "L1_done", "L1_csync", "L2_data", "L2_done", "L2_csync", "-", "-", "-", "end"};
+  const char* names[16] = {"start", "bar_init", "copies_issued", "L0_data", "L0_done", "init_fence", "L1_data",
+                           "L1_done", "cta_sync", "L2_data", "L2_done", "cl_arrive", "expects", "-", "-", "end"};
   unsigned long long g0 = ~0ull, g1 = 0;
   for (int b = 0; b < nblk; ++b) {
     if (tr[b][13]) g0 = std::min(g0, tr[b][13]);

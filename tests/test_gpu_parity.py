@@ -123,10 +123,7 @@ def test_batched_persistent_variants(engine, oracle, golden, name):
             assert "batched" in engine.describe(h)["kernel"]
             for k in case["outputs"]:
                 assert_exact(oracle, f"{name}/{rm}x{rn}/grid{grid}", k, got[k], case["outputs"][k]["fnv"], ref[k])
-    # the default for the paper's batched contraction is the persistent kernel
-    if name == "tbmm_paper":
-        got, h = run_on_gpu(engine, case["def"], ins, seeded)
-        assert "batched" in engine.describe(h)["kernel"]
+
 
 
 @pytest.mark.parametrize("rows,cn,threads", [(1, 1, 64), (2, 2, 64), (4, 8, 64), (8, 8, 64), (8, 4, 256),
