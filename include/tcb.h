@@ -200,6 +200,21 @@ int tcb_options_baseline(int i, char* out, int len); /* reference presets 0..2 *
 int tcb_options_default(tcb_engine* e, const char* name, const tcb_tensor* inputs, int n_inputs,
                         const tcb_tensor* outputs, int n_outputs, char* out, int len);
 
+/* TCTN1 tensor files, byte-compatible with the reference's
+ * writeTensorFile / readTensorFile (proj/src/support/tensor_data.cc:122-189).
+ * read: fills a TCB_HOST tensor whose data the caller releases with
+ * tcb_tensor_file_free. Malformed / truncated files fail with TCB_ERR_IO. */
+int tcb_tensor_file_write(const char* path, const tcb_tensor* host_tensor);
+int tcb_tensor_file_read(const char* path, tcb_tensor* out_host_tensor);
+void tcb_tensor_file_free(void* data);
+
+/* declared parameters of a defined def, as JSON:
+ * {"params": [{"name", "elem": "float"|"int", "dims": [symbol or literal...]}],
+ *  "returns": [...], "inout_returns": [...]}  (binds CLI --sizes to shapes) */
+int tcb_def_params(tcb_engine* e, const char* name, char* buf, int len);
+/* every cache entry as a JSON array (cache list / inspect) */
+int tcb_cache_entries(char* buf, int len);
+
 /* pinned host memory for TCB_HOST tensors (cudaMallocHost) */
 int tcb_host_alloc(void** p, int64_t bytes);
 int tcb_host_free(void* p);

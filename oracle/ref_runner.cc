@@ -231,4 +231,39 @@ int tcref_cache_serialize_one(const char* src, const char* entry, int n_in,
   }
 }
 
+// TCTN1 through the reference's own writer / reader
+// (proj/src/support/tensor_data.cc:122-189), for the byte-compatibility test.
+int tcref_write_tensor(const char* path, int kind, int rank, const int64_t* shape, const void* data, char* err,
+                       int errlen) {
+  try {
+    std::vector<int64_t> sh(shape, shape + rank);
+    backend::TensorData t = backend::TensorData::zeros(kind ? lang::ElemKind::Int : lang::ElemKind::Float, sh);
+    int64_t n = t.volume();
+    if (kind) std::memcpy(t.i.data(), data, n * 4);
+    else std::memcpy(t.f.data(), data, n * 4);
+    backend::writeTensorFile(path, t);
+    return 0;
+  } catch (const Error& e) {
+    setErr(err, errlen, e.what());
+    return (int)e.kind() + 1;
+  }
+}
+
+// reads a TCTN1 file; returns the volume (or -(ErrorKind+1)); fills kind/rank/shape/data up to cap values
+int64_t tcref_read_tensor(const char* path, int* kind, int* rank, int64_t* shape, void* data, int64_t cap, char* err,
+                          int errlen) {
+  try {
+    backend::TensorData t = backend::readTensorFile(path);
+    *kind = t.elemKind == lang::ElemKind::Int ? 1 : 0;
+    *rank = (int)t.shape.size();
+    for (size_t d = 0; d < t.shape.size(); ++d) shape[d] = t.shape[d];
+    int64_t n = t.volume();
+    if (n <= cap) std::memcpy(data, *kind ? (const void*)t.i.data() : (const void*)t.f.data(), n * 4);
+    return n;
+  } catch (const Error& e) {
+    setErr(err, errlen, e.what());
+    return -((int64_t)e.kind() + 1);
+  }
+}
+
 } // extern "C"

@@ -8,7 +8,8 @@
   (-gencode arch=compute_100a,code=sm_100a -lineinfo -O3),
 * compiles the C++ host runtime (csrc/*.cc) with g++ -O2,
 * links paper_1802_04730_b200/libtcb.so with the CUDA runtime linked
-  statically (no dependence on torch's or the system's libcudart version).
+  statically (no dependence on torch's or the system's libcudart version),
+* builds the `tcb` command-line driver (paper_1802_04730_b200/bin/tcb).
 
 Incremental: objects are rebuilt only when a source or header is newer.
 """
@@ -24,6 +25,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "build", "obj")
 LIB = os.path.join(PKG, "libtcb.so")
+CLI = os.path.join(PKG, "bin", "tcb")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
@@ -75,8 +77,17 @@ def build(verbose=True, jobs=None):
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    # the `tcb` command-line driver (csrc/cli), linked against libtcb.so
+    cli_src = os.path.join(CSRC, "cli", "tcb_main.cc")
+    if not os.path.exists(CLI) or os.path.getmtime(CLI) < max(os.path.getmtime(LIB), os.path.getmtime(cli_src), hdr):
+        os.makedirs(os.path.dirname(CLI), exist_ok=True)
+        cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", CSRC, cli_src, "-o", CLI, "-L", PKG, "-ltcb",
+               "-Wl,-rpath,$ORIGIN/.."]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"CLI build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
     if verbose:
-        print(f"[build] {LIB}", file=sys.stderr)
+        print(f"[build] {LIB} {CLI}", file=sys.stderr)
     return LIB
 
 

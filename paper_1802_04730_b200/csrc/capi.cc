@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <ctime>
 #include <memory>
@@ -15,6 +16,7 @@
 #include "json.h"
 #include "ops.h"
 #include "session.h"
+#include "tensor_file.h"
 #include "tuner.h"
 
 using namespace tcb;
@@ -565,6 +567,86 @@ int tcb_options_default(tcb_engine* e, const char* name, const tcb_tensor* in, i
     sem::Specialized s = e->specialize(name, in, nin, out, nout);
     ops::Problem p = ops::match(s, cache::canonicalize(s.v));
     copyOut(ops::defaultOptions(p).toJson(), buf, len);
+  });
+}
+
+int tcb_tensor_file_write(const char* path, const tcb_tensor* t) {
+  return guarded([&] {
+    if (!t || !t->data) fail(ErrorKind::Io, "tensor has no host data");
+    if (t->location != TCB_HOST) fail(ErrorKind::Io, "tensor files are written from host tensors");
+    TensorFile h;
+    h.isInt = t->dtype == TCB_I32;
+    h.shape = shapeOf(*t);
+    int64_t n = 1;
+    for (auto e : h.shape) n *= e;
+    h.bits.assign(static_cast<const uint32_t*>(t->data), static_cast<const uint32_t*>(t->data) + n);
+    writeTensorFile(path, h);
+  });
+}
+
+int tcb_tensor_file_read(const char* path, tcb_tensor* t) {
+  return guarded([&] {
+    TensorFile h = readTensorFile(path);
+    size_t bytes = std::max<size_t>(4, h.bits.size() * 4);
+    void* p = std::malloc(bytes);
+    if (!p) fail(ErrorKind::Io, "out of host memory reading '" + std::string(path) + "'");
+    std::memcpy(p, h.bits.data(), h.bits.size() * 4);
+    t->data = p;
+    t->dtype = h.isInt ? TCB_I32 : TCB_F32;
+    t->rank = static_cast<int32_t>(h.shape.size());
+    for (size_t d = 0; d < h.shape.size(); ++d) t->shape[d] = h.shape[d];
+    t->location = TCB_HOST;
+    t->reserved = 0;
+  });
+}
+
+void tcb_tensor_file_free(void* data) { std::free(data); }
+
+int tcb_def_params(tcb_engine* e, const char* name, char* buf, int len) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> g(e->mu);
+    const DefEntry& d = e->def(name);
+    Json j = Json::object();
+    Json ps = Json::array();
+    for (const auto& p : d.v.def.params) {
+      Json q = Json::object();
+      q["name"] = Json(p.name);
+      q["elem"] = Json(p.elem == lang::Elem::Int ? "int" : "float");
+      Json dims = Json::array();
+      for (const auto& x : p.dims) dims.push(Json(x));
+      q["dims"] = dims;
+      ps.push(q);
+    }
+    j["params"] = ps;
+    Json rs = Json::array();
+    for (const auto& r : d.v.def.rets) rs.push(Json(r));
+    j["returns"] = rs;
+    Json io = Json::array();
+    for (const auto& r : sem::inoutReturns(d.v)) io.push(Json(r));
+    j["inout_returns"] = io;
+    copyOut(j.dump(), buf, len);
+  });
+}
+
+int tcb_cache_entries(char* buf, int len) {
+  return guarded([&] {
+    Json a = Json::array();
+    for (const auto& en : globalCache().entries()) {
+      Json j = Json::object();
+      j["canonical_tc"] = Json(en.key.canonicalTc);
+      Json sh = Json::array();
+      for (const auto& s : en.key.inputShapes) sh.push(Json(s));
+      j["input_shapes"] = sh;
+      j["target"] = Json(en.key.target);
+      j["options_digest"] = Json(en.key.optionsDigest);
+      j["options"] = Json::parse(en.options.toJson());
+      j["kernel"] = Json(en.kernelText);
+      j["cost_ns"] = Json(en.cost);
+      j["created_at"] = Json(en.createdAt);
+      j["origin"] = Json(cache::originName(en.origin));
+      a.push(j);
+    }
+    copyOut(a.dump(), buf, len);
   });
 }
 

@@ -234,6 +234,36 @@ class ExecutionEngine:
         return call
 
 
+def tensor_file_write(path, array):
+    """Writes a numpy float32/int32 array as a TCTN1 file (the reference's
+    writeTensorFile format, tensor_data.cc:122-147)."""
+    a = np.ascontiguousarray(array)
+    if a.dtype not in (np.float32, np.int32):
+        raise TypeError("TCTN1 tensors are float32 or int32")
+    check(lib.tcb_tensor_file_write(str(path).encode(), C.byref(_desc(a))))
+
+
+def tensor_file_read(path):
+    """Reads a TCTN1 file into a numpy array (readTensorFile, tensor_data.cc:149-189)."""
+    t = Tensor()
+    check(lib.tcb_tensor_file_read(str(path).encode(), C.byref(t)))
+    try:
+        shape = tuple(t.shape[d] for d in range(t.rank))
+        n = int(np.prod(shape)) if shape else 1
+        dt = np.int32 if t.dtype == TCB_I32 else np.float32
+        buf = (C.c_uint8 * (4 * n)).from_address(t.data)
+        return np.frombuffer(bytes(buf), dtype=dt).reshape(shape).copy()
+    finally:
+        lib.tcb_tensor_file_free(t.data)
+
+
+def cache_entries():
+    """Every cache entry (cache list / inspect)."""
+    b = _lib.buf(1 << 24)
+    check(lib.tcb_cache_entries(b, 1 << 24))
+    return json.loads(b.value.decode())
+
+
 def cache_load(path):
     check(lib.tcb_cache_load(path.encode()))
 

@@ -194,6 +194,12 @@ class RefLib:
                                                       C.POINTER(C.c_int), C.POINTER(I64),
                                                       C.c_char_p, I64, I64, C.c_char_p, C.c_int,
                                                       C.c_char_p, C.c_int]
+            lib.tcref_write_tensor.restype = C.c_int
+            lib.tcref_write_tensor.argtypes = [C.c_char_p, C.c_int, C.c_int, C.POINTER(I64), C.c_void_p,
+                                               C.c_char_p, C.c_int]
+            lib.tcref_read_tensor.restype = I64
+            lib.tcref_read_tensor.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(I64),
+                                              C.c_void_p, I64, C.c_char_p, C.c_int]
             RefLib._lib = lib
         self.lib = RefLib._lib
 
@@ -207,6 +213,30 @@ class RefLib:
         ranks = (C.c_int * len(shapes))(*[len(s) for s in shapes])
         flat = [int(d) for s in shapes for d in s] or [0]
         return ranks, (I64 * len(flat))(*flat)
+
+    def write_tensor(self, path, arr):
+        """The reference's writeTensorFile (tensor_data.cc:122-147)."""
+        a = np.ascontiguousarray(arr)
+        shape = (I64 * max(1, a.ndim))(*a.shape)
+        err = C.create_string_buffer(512)
+        rc = self.lib.tcref_write_tensor(str(path).encode(), 1 if a.dtype == np.int32 else 0, a.ndim, shape,
+                                         a.ctypes.data, err, 512)
+        if rc:
+            raise RefError(rc, err.value.decode())
+
+    def read_tensor(self, path):
+        """The reference's readTensorFile; raises RefError (kind Io) on malformed files."""
+        kind, rank = C.c_int(), C.c_int()
+        shape = (I64 * 16)()
+        cap = 1 << 22
+        buf = np.empty(cap, np.uint32)
+        err = C.create_string_buffer(512)
+        n = self.lib.tcref_read_tensor(str(path).encode(), C.byref(kind), C.byref(rank), shape,
+                                       buf.ctypes.data, cap, err, 512)
+        if n < 0:
+            raise RefError(int(-n), err.value.decode())
+        dt = np.int32 if kind.value else np.float32
+        return buf[:n].view(dt).reshape(tuple(shape[d] for d in range(rank.value))).copy()
 
     def run(self, src, entry, inputs, out_names):
         """inputs: dict name -> np.ndarray (float32 or int32). Returns dict of outputs."""
