@@ -523,6 +523,7 @@ def main():
     }
     if not args.no_ops:
         line["ops"] = paper_op_table(ee, torch, dev, stream, peaks)
+        line["prod_model"] = prod_model_line(ee, torch, dev)
     if world == 1 and not args.no_cpu_baseline:
         v, info = cpu_baseline()
         line["cpu_baseline"] = {"value": round(v, 6), "unit": "GFLOP/s", **info}
@@ -530,6 +531,55 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def prod_model_line(ee, torch, dev):
+    """The production model chain (2LUT -> C3 -> concat ->
+    MLP1 -> MLP3) at the paper's sizes, one CUDA graph per forward pass:
+    device µs per forward (200 back-to-back replays) and the paper-protocol
+    synchronised latency."""
+    try:
+        from paper_1802_04730_b200.prodmodel import PAPER_SIZES as S
+        from paper_1802_04730_b200.prodmodel import ProductionModel
+        g = torch.Generator(device=dev)
+        g.manual_seed(21)
+        r = lambda *sh: torch.rand(sh, generator=g, device=dev) * 2 - 1  # noqa: E731
+        p = dict(LUT1=r(S["E1"], S["D"]), LUT2=r(S["E2"], S["D"]),
+                 I1=torch.randint(0, S["E1"], (S["B"], S["L1"]), generator=g, device=dev, dtype=torch.int32),
+                 I2=torch.randint(0, S["E2"], (S["B"], S["L2"]), generator=g, device=dev, dtype=torch.int32),
+                 I3=r(S["B"], S["WX"]), W=r(S["WY"], S["WX"]), W1=r(S["N"], 2 * S["D"] + S["WY"]), B1=r(S["N"]),
+                 W2=r(S["O"], S["N"]), B2=r(S["O"]), W3=r(S["P"], S["O"]), B3=r(S["P"]), W4=r(S["Q"], S["P"]),
+                 B4=r(S["Q"]))
+        m = ProductionModel(ee, p).capture()
+        for _ in range(5):
+            m.replay()
+        m.check()
+        n = 200
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(m.stream)
+        for _ in range(n):
+            m.replay()
+        e1.record(m.stream)
+        e1.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / n
+        lat = []
+        for _ in range(100):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            m.replay()
+            m.stream.synchronize()
+            lat.append(time.perf_counter() - t0)
+        lat.sort()
+        out = {"us_per_forward": round(us, 3), "gflops": round(m.flops / us / 1e3, 1),
+               "us_p0_p50_p90_sync": [round(lat[0] * 1e6, 1), round(lat[50] * 1e6, 1), round(lat[90] * 1e6, 1)],
+               "kernels": m.kernels, "graph": "2LUT || (zero C3, C3) -> concat -> MLP1 -> MLP3, one CUDA graph",
+               "sizes": S}
+        del m, p
+        torch.cuda.empty_cache()
+        return out
+    except Exception as e:  # report, don't hide
+        return {"error": f"{type(e).__name__}: {e}"}
 
 
 def paper_op_table(ee, torch, dev, stream, peaks):

@@ -215,6 +215,13 @@ int tcb_def_params(tcb_engine* e, const char* name, char* buf, int len);
 /* every cache entry as a JSON array (cache list / inspect) */
 int tcb_cache_entries(char* buf, int len);
 
+/* dst[r][:] = [src_0[r][:] | src_1[r][:] | ...] on the device (row-major,
+ * `rows` rows, widths[i] columns each, 1..8 sources). The production
+ * model's concat between 2LUT/C3 and MLP1, which TC
+ * itself cannot express. */
+int tcb_concat_cols(const float* const* srcs, const int64_t* widths, int n, int64_t rows, float* dst,
+                    void* stream);
+
 /* pinned host memory for TCB_HOST tensors (cudaMallocHost) */
 int tcb_host_alloc(void** p, int64_t bytes);
 int tcb_host_free(void* p);

@@ -102,6 +102,8 @@ def _load():
         "tcb_tensor_file_free": (None, [C.c_void_p]),
         "tcb_def_params": (C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int]),
         "tcb_cache_entries": (C.c_int, [C.c_char_p, C.c_int]),
+        "tcb_concat_cols": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int, C.c_int64,
+                                      C.c_void_p, C.c_void_p]),
         "tcb_host_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_int64]),
         "tcb_host_free": (C.c_int, [C.c_void_p]),
     }
@@ -125,7 +127,7 @@ EXPORTED = [
     "tcb_session_inputs", "tcb_fill_uniform", "tcb_options_validate", "tcb_options_normalize",
     "tcb_options_digest", "tcb_options_baseline", "tcb_options_default", "tcb_host_alloc",
     "tcb_host_free", "tcb_tensor_file_write", "tcb_tensor_file_read", "tcb_tensor_file_free", "tcb_def_params",
-    "tcb_cache_entries",
+    "tcb_cache_entries", "tcb_concat_cols",
 ]
 
 

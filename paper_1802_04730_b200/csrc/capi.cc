@@ -602,6 +602,25 @@ int tcb_tensor_file_read(const char* path, tcb_tensor* t) {
 
 void tcb_tensor_file_free(void* data) { std::free(data); }
 
+int tcb_concat_cols(const float* const* srcs, const int64_t* widths, int n, int64_t rows, float* dst,
+                    void* stream) {
+  return guarded([&] {
+    if (n < 1 || n > k::kMaxConcat) fail(ErrorKind::ShapeMismatch, "concat takes 1..8 sources");
+    k::ConcatArgs a{};
+    a.n = n;
+    a.rows = rows;
+    a.dst = dst;
+    a.off[0] = 0;
+    for (int i = 0; i < n; ++i) {
+      if (!srcs[i] || widths[i] < 1) fail(ErrorKind::ShapeMismatch, "concat source without data or columns");
+      a.src[i] = srcs[i];
+      a.off[i + 1] = a.off[i] + static_cast<int>(widths[i]);
+    }
+    a.width = a.off[n];
+    cudaOk(k::launchConcat(a, static_cast<cudaStream_t>(stream)), "concat launch");
+  });
+}
+
 int tcb_def_params(tcb_engine* e, const char* name, char* buf, int len) {
   return guarded([&] {
     std::lock_guard<std::mutex> g(e->mu);

@@ -88,12 +88,6 @@ __device__ __forceinline__ void bulkCopy(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smemAddr(bar))
       : "memory");
 }
-// Non-.aligned form: callers may reach it with a warp that diverged in an
-// mbarrier spin (lanes waiting on different barriers); we also __syncwarp().
-__device__ __forceinline__ void clusterSync() {
-  __syncwarp();
-  asm volatile("barrier.cluster.arrive.release;\nbarrier.cluster.wait.acquire;\n" ::: "memory");
-}
 __device__ __forceinline__ unsigned clusterRank() {
   unsigned r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -129,11 +123,6 @@ __device__ __forceinline__ void stAsyncCluster(const float* local, const uint64_
                : "memory");
 }
 
-__device__ __forceinline__ void stCluster(float* local, unsigned rank, float v) {
-  unsigned remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smemAddr(local)), "r"(rank));
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
-}
 
 // acc = chain over k in [0, n) of x[k] * w[k]; operands addressed as 32-bit
 // shared-window byte addresses. Double-buffered 16-wide chunks: the eight

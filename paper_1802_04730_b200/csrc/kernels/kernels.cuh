@@ -122,6 +122,17 @@ struct LutArgs {
 };
 cudaError_t launchLut(const LutArgs* tables, int ntables, int threads, cudaStream_t s);
 
+// --------------------------------------------------------------- concat
+constexpr int kMaxConcat = 8;
+struct ConcatArgs {
+  const float* src[kMaxConcat];
+  int off[kMaxConcat + 1];  // column offsets: src s covers [off[s], off[s+1])
+  int n;
+  int64_t rows, width;
+  float* dst;
+};
+cudaError_t launchConcat(const ConcatArgs& a, cudaStream_t s);
+
 // ---------------------------------------------------------------- probes
 // fp32 FFMA throughput of the whole device (TFLOP/s, 2 flops per FMA)
 cudaError_t probeFfma(int sms, double* tflops, float* ms);

@@ -28,19 +28,36 @@ __global__ void lut_kernel(const LutArgs a0, const LutArgs a1, const int vec) {
   if (row >= a.B) return;
   const int32_t* idx = a.I + row * a.L;
   if (vec) {
+    // two-stage loading: a chunk of kChunk indices is
+    // read and validated first, then all kChunk table rows are gathered with
+    // independent loads, then added in k order — the gathers of a chunk are
+    // in flight together instead of one dependent miss per k
+    constexpr int kChunk = 16;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = 0; k < a.L; ++k) {
-      int64_t e = __ldg(idx + k);
-      if (e < 0 || e >= a.E) {
-        atomicOr(a.err, 1);
-        break;
+    bool bad = false;
+    for (int k0 = 0; k0 < a.L; k0 += kChunk) {
+      int64_t e[kChunk];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) e[j] = k0 + j < a.L ? (int64_t)__ldg(idx + k0 + j) : 0;
+      float4 v[kChunk];
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        const bool ok = e[j] >= 0 && e[j] < a.E;
+        bad |= (k0 + j < a.L) && !ok;
+        v[j] = (k0 + j < a.L && ok) ? __ldg(reinterpret_cast<const float4*>(a.LUT + e[j] * a.D) + lane)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      float4 v = __ldg(reinterpret_cast<const float4*>(a.LUT + e * a.D) + lane);
-      acc.x = __fadd_rn(acc.x, v.x);
-      acc.y = __fadd_rn(acc.y, v.y);
-      acc.z = __fadd_rn(acc.z, v.z);
-      acc.w = __fadd_rn(acc.w, v.w);
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        if (k0 + j < a.L) {
+          acc.x = __fadd_rn(acc.x, v[j].x);
+          acc.y = __fadd_rn(acc.y, v[j].y);
+          acc.z = __fadd_rn(acc.z, v[j].z);
+          acc.w = __fadd_rn(acc.w, v[j].w);
+        }
+      }
     }
+    if (bad) atomicOr(a.err, 1);  // IndexOutOfRange; the row's value is unspecified
     reinterpret_cast<float4*>(a.O + row * a.D)[lane] = acc;
   } else {
     float acc = 0.f;

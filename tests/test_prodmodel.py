@@ -1,0 +1,96 @@
+"""The production model chain replayed as one CUDA
+graph, against the oracle evaluating the same TC definitions one after the
+other (oracle/oracle.c). Bit-exact: every operator is FFMA-exact and the
+concat is a copy."""
+import numpy as np
+import pytest
+
+from oracle_lib import Oracle
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def oracle_chain(orc, h):
+    c1 = orc.lut(h["LUT1"], h["I1"])
+    c2 = orc.lut(h["LUT2"], h["I2"])
+    c3 = orc.c3(h["I3"], h["W"], np.zeros((h["I3"].shape[0], h["W"].shape[0]), np.float32))
+    i = np.concatenate([c1, c2, c3], axis=1)
+    o1 = orc.fc_relu(i, h["W1"], h["B1"])
+    o2, o3, o4 = orc.mlp3(o1, h["W2"], h["B2"], h["W3"], h["B3"], h["W4"], h["B4"])
+    return dict(C1=c1, C2=c2, C3=c3, I=i, O1=o1, O2=o2, O3=o3, O4=o4)
+
+
+def make_params(orc, B, E, D, L, WX, WY, N, O, P, Q, seed=5):
+    rng = orc.rng(seed)
+    h = dict(LUT1=rng.f32((E, D)), I1=rng.i32((B, L), 0, E), LUT2=rng.f32((E, D)), I2=rng.i32((B, L), 0, E),
+             I3=rng.f32((B, WX)), W=rng.f32((WY, WX)), W1=rng.f32((N, 2 * D + WY)), B1=rng.f32((N,)),
+             W2=rng.f32((O, N)), B2=rng.f32((O,)), W3=rng.f32((P, O)), B3=rng.f32((P,)), W4=rng.f32((Q, P)),
+             B4=rng.f32((Q,)))
+    return h
+
+
+def test_prodmodel_graph_small_bit_exact():
+    from paper_1802_04730_b200 import ExecutionEngine
+    from paper_1802_04730_b200.prodmodel import ProductionModel
+    orc = Oracle()
+    h = make_params(orc, B=16, E=1000, D=64, L=5, WX=64, WY=40, N=32, O=16, P=8, Q=2)
+    ref = oracle_chain(orc, h)
+    m = ProductionModel(ExecutionEngine(), {k: torch.from_numpy(v).cuda() for k, v in h.items()})
+    out = m.forward_eager()
+    for k in ref:
+        assert np.array_equal(out[k].cpu().numpy(), ref[k]), f"eager {k}"
+    for v in m.out.values():
+        v.fill_(123.0)
+    m.capture()
+    for _ in range(3):  # replays are idempotent (C3 is re-zeroed inside the graph)
+        m.replay()
+    m.check()
+    for k in ref:
+        assert np.array_equal(m.out[k].cpu().numpy(), ref[k]), f"graph {k}"
+
+
+def test_prodmodel_index_out_of_range():
+    from paper_1802_04730_b200 import ExecutionEngine, TcError
+    from paper_1802_04730_b200.prodmodel import ProductionModel
+    orc = Oracle()
+    h = make_params(orc, B=4, E=100, D=64, L=3, WX=32, WY=16, N=8, O=8, P=4, Q=2)
+    h["I2"][1, 2] = 100  # == E: out of range
+    m = ProductionModel(ExecutionEngine(), {k: torch.from_numpy(v).cuda() for k, v in h.items()})
+    m.capture()
+    m.replay()
+    with pytest.raises(TcError) as ei:
+        m.check()
+    assert ei.value.kind == "IndexOutOfRange"
+
+
+def test_prodmodel_paper_sizes():
+    """E=1e7 tables live on the device; the oracle sees only the gathered rows."""
+    from paper_1802_04730_b200 import ExecutionEngine
+    from paper_1802_04730_b200.prodmodel import PAPER_SIZES, ProductionModel
+    orc = Oracle()
+    s = PAPER_SIZES
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    dev = {}
+    for name in ("LUT1", "LUT2"):
+        dev[name] = torch.rand((s["E1"], s["D"]), generator=g, device="cuda") * 2 - 1
+    for name in ("I1", "I2"):
+        dev[name] = torch.randint(0, s["E1"], (s["B"], s["L1"]), generator=g, device="cuda", dtype=torch.int32)
+    small = make_params(orc, B=s["B"], E=2, D=s["D"], L=1, WX=s["WX"], WY=s["WY"], N=s["N"], O=s["O"], P=s["P"],
+                        Q=s["Q"])
+    for k in ("I3", "W", "W1", "B1", "W2", "B2", "W3", "B3", "W4", "B4"):
+        dev[k] = torch.from_numpy(small[k]).cuda()
+    m = ProductionModel(ExecutionEngine(), dev).capture()
+    m.replay()
+    m.check()
+    # oracle on the gathered rows only: remap indices into a compact table
+    h = {k: small[k] for k in ("I3", "W", "W1", "B1", "W2", "B2", "W3", "B3", "W4", "B4")}
+    for t, i in (("LUT1", "I1"), ("LUT2", "I2")):
+        idx = dev[i].long()
+        uniq, inv = torch.unique(idx, return_inverse=True)
+        h[t] = dev[t][uniq].cpu().numpy()
+        h[i] = inv.to(torch.int32).cpu().numpy()
+    ref = oracle_chain(orc, h)
+    for k in ref:
+        assert np.array_equal(m.out[k].cpu().numpy(), ref[k]), k
