@@ -1,10 +1,12 @@
 // lut.cu — embedding lookup-table reductions (1LUT / 2LUT,
 // proj/kernels/2lut.tc:2-6):   O(i,j) +=! LUT(I(i,k), j)
-// A warp-group of D/4 threads owns one batch row i; each thread owns four
-// consecutive columns j and walks k ascending, gathering 16-byte slices of
-// the indexed table rows (fully coalesced per row) and adding them in
-// order (__fadd_rn — the reference's double add narrowed to float is the
-// correctly rounded float add). Indices are validated on the device: an
+// Default (D % 4 == 0, 16-byte aligned): lut_smem_kernel, one CTA per
+// (row, table) staging all gathered rows in shared memory before the ordered
+// sum. Fallback (lut_kernel): a warp-group of D/4 (or D) threads owns one
+// batch row i; each thread owns four consecutive columns j and walks k
+// ascending, gathering 16-byte slices of the indexed table rows. Both add in
+// k order (__fadd_rn — the reference's double add narrowed to float is the
+// correctly rounded float add up to a double-rounding tie). Indices are validated on the device: an
 // index outside [0, E) raises the kernel's error flag, the reference's
 // IndexOutOfRange (interpreter.cc:284-292), and is never clamped. Both
 // tables of 2LUT run in one launch (blockIdx.y selects the table).
@@ -73,6 +75,54 @@ __global__ void lut_kernel(const LutArgs a0, const LutArgs a1, const int vec) {
   }
 }
 
+// Two-stage loading in shared memory, one CTA per
+// (batch row, table): stage 1 reads the row's L indices and validates them;
+// stage 2 has every thread of the CTA issue its share of the L x D/4
+// 16-byte gathers at once (all of the row's table rows in flight together)
+// into shared memory; stage 3 sums them in k order, one float4 column per
+// thread (__fadd_rn, the interpreter's order). Chunks of kRows rows keep the
+// staging buffer bounded for any L.
+constexpr int kRows = 64;
+__global__ void lut_smem_kernel(const LutArgs a0, const LutArgs a1) {
+  const LutArgs& a = blockIdx.y == 0 ? a0 : a1;
+  const int64_t row = blockIdx.x;
+  if (row >= a.B) return;
+  extern __shared__ float4 stage[];  // [kRows][D/4]
+  __shared__ int64_t sIdx[kRows];
+  __shared__ int sBad;
+  const int cols = a.D / 4, T = blockDim.x, tid = threadIdx.x;
+  const int32_t* idx = a.I + row * a.L;
+  if (tid == 0) sBad = 0;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k0 = 0; k0 < a.L; k0 += kRows) {
+    const int nk = min(kRows, a.L - k0);
+    __syncthreads();  // previous chunk consumed
+    for (int k = tid; k < nk; k += T) {
+      const int64_t e = __ldg(idx + k0 + k);
+      const bool ok = e >= 0 && e < a.E;
+      if (!ok) sBad = 1;
+      sIdx[k] = ok ? e : 0;  // never clamped into the result: the row is flagged
+    }
+    __syncthreads();
+    for (int q = tid; q < nk * cols; q += T) {
+      const int k = q / cols, c = q % cols;
+      stage[q] = __ldg(reinterpret_cast<const float4*>(a.LUT + sIdx[k] * a.D) + c);
+    }
+    __syncthreads();
+    if (tid < cols) {
+      for (int k = 0; k < nk; ++k) {
+        const float4 v = stage[k * cols + tid];
+        acc.x = __fadd_rn(acc.x, v.x);
+        acc.y = __fadd_rn(acc.y, v.y);
+        acc.z = __fadd_rn(acc.z, v.z);
+        acc.w = __fadd_rn(acc.w, v.w);
+      }
+    }
+  }
+  if (tid < cols) reinterpret_cast<float4*>(a.O + row * a.D)[tid] = acc;
+  if (tid == 0 && sBad) atomicOr(a.err, 1);  // IndexOutOfRange; the row's value is unspecified
+}
+
 }  // namespace
 
 cudaError_t launchLut(const LutArgs* tables, int ntables, int threads, cudaStream_t s) {
@@ -92,6 +142,23 @@ cudaError_t launchLut(const LutArgs* tables, int ntables, int threads, cudaStrea
     maxLanes = lanes > maxLanes ? lanes : maxLanes;
   }
   if (maxLanes == 0) return cudaSuccess;
+  int maxD = 0;
+  int64_t maxB = 0;
+  for (int i = 0; i < ntables; ++i) {
+    maxD = tables[i].D > maxD ? tables[i].D : maxD;
+    maxB = tables[i].B > maxB ? tables[i].B : maxB;
+  }
+  const size_t smem = (size_t)kRows * maxD * 4;
+  if (vec && smem <= 160 * 1024) {  // two-stage shared-memory gather: `threads` per (row, table) CTA
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(lut_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      attr = true;
+    }
+    int t = threads > 0 ? threads : 256;
+    lut_smem_kernel<<<dim3((unsigned)maxB, ntables), t, smem, s>>>(p.t[0], p.t[1]);
+    return cudaGetLastError();
+  }
   int t = threads > 0 ? threads : 256;
   dim3 grid((unsigned)((maxLanes + t - 1) / t), ntables);
   lut_kernel<<<grid, t, 0, s>>>(p.t[0], p.t[1], vec);
