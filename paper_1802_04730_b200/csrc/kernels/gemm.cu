@@ -114,12 +114,13 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
     const int st = t % S;
     const float* Ast = &As[st][ty][0];
     const float* Bst = &Bs[st][tx][0];
-    auto group = [&](int kk) {  // one 4-k step of every chain of the micro-tile
-      float4 av[RM], bv[RN];
+    auto loadGroup = [&](int kk, float4* av, float4* bv) {
 #pragma unroll
       for (int i = 0; i < RM; ++i) av[i] = *reinterpret_cast<const float4*>(Ast + i * TY * LD + kk);
 #pragma unroll
       for (int j = 0; j < RN; ++j) bv[j] = *reinterpret_cast<const float4*>(Bst + j * TX * LD + kk);
+    };
+    auto fmaGroup = [&](const float4* av, const float4* bv) {  // one 4-k step of every chain
 #pragma unroll
       for (int i = 0; i < RM; ++i)
 #pragma unroll
@@ -137,12 +138,24 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
 #pragma unroll
         for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(av[i].w, bv[j].w, acc[i][j]);
     };
+    auto group = [&](int kk) {  // one 4-k step of every chain of the micro-tile
+      float4 av[RM], bv[RN];
+      loadGroup(kk, av, bv);
+      fmaGroup(av, bv);
+    };
     const int klim = min(TK, a.K - t * TK);
     if (klim == TK) {
-      // full tile: fully unrolled so the scheduler hoists the next group's
-      // shared loads above the current group's FFMAs
+      // full tile: register double buffer — group g+1's shared loads are
+      // issued before group g's FFMAs, so their latency hides behind them
+      float4 a0[RM], b0[RN], a1[RM], b1[RN];
+      loadGroup(0, a0, b0);
 #pragma unroll
-      for (int kk = 0; kk < TK; kk += 4) group(kk);
+      for (int kk = 0; kk < TK; kk += 8) {
+        if (kk + 4 < TK) loadGroup(kk + 4, a1, b1);
+        fmaGroup(a0, b0);
+        if (kk + 8 < TK) loadGroup(kk + 8, a0, b0);
+        if (kk + 4 < TK) fmaGroup(a1, b1);
+      }
     } else {
       const int k4 = klim & ~3;
       int kk = 0;

@@ -498,6 +498,14 @@ MappingOptions defaultOptions(const Problem& p, int math) {
 
       auto ctas = [&](int tm, int tn) { return (double)g.batch * ((g.M + tm - 1) / tm) * ((g.N + tn - 1) / tn); };
       o.unrollCopyShared = g.K > 128;
+      if (g.K > 128 && ctas(32, 32) >= 96) {
+        // long reductions with enough 32x32 tiles: 64-deep k stages (measured
+        // best of the 19 variants for C3 / TMM 128x1024x1024 on B200)
+        o.tileSizes = {32, 32, 64};
+        o.threadShape = {{16, 16, 1}};
+        o.unrollCopyShared = false;
+        break;
+      }
       if (ctas(32, 32) < 148) {
         if (o.unrollCopyShared) {
           o.tileSizes = {16, 32, 32};
