@@ -212,23 +212,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int R = kBM / p.splits;
     const uint32_t base = smem(sm);
     const int64_t cb = static_cast<int64_t>(b) * p.sC;
-    for (int idx = threadIdx.x; idx < R * BN; idx += kThreads) {
-      const int row = split * R + idx / BN, col = idx % BN;
-      const int m = mt * kBM + row, n = nt * BN + col;
-      if (m >= p.M || n >= p.N) continue;
+    constexpr int Q = BN / 4;  // float4 column groups per row
+    for (int idx = threadIdx.x; idx < R * Q; idx += kThreads) {
+      const int row = split * R + idx / Q, col = (idx % Q) * 4;
+      const int m = mt * kBM + row, n0 = nt * BN + col;
+      if (m >= p.M || n0 >= p.N) continue;
       const uint32_t off = base + (row * Cfg::kPartLd + col) * 4;
-      float acc = 0.f;
+      float4 acc;
       if (p.splits == 1) {
-        acc = *reinterpret_cast<const float*>(sm + (row * Cfg::kPartLd + col) * 4);
+        acc = *reinterpret_cast<const float4*>(sm + (row * Cfg::kPartLd + col) * 4);
       } else {
-        for (int r = 0; r < p.splits; ++r) acc += ldsCluster(mapa(off, r));
+        // every rank's partial in flight at once, then summed in rank order
+        float4 part[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if (r < p.splits) part[r] = ldsCluster4(mapa(off, r));
+        acc = part[0];
+#pragma unroll
+        for (int r = 1; r < 16; ++r)
+          if (r < p.splits) {
+            acc.x += part[r].x;
+            acc.y += part[r].y;
+            acc.z += part[r].z;
+            acc.w += part[r].w;
+          }
       }
-      float* cp = p.C + cb + static_cast<int64_t>(m) * p.ldc + n;
-      float v = acc;
-      if (p.init == kInitInout) v = *cp + acc;
-      else if (p.init == kInitBias) v = p.bias[n] + acc;
-      if (p.relu) v = fmaxf(v, 0.f);
-      *cp = v;
+      const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
+      float* cp = p.C + cb + static_cast<int64_t>(m) * p.ldc + n0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (n0 + j >= p.N) break;
+        float v = a4[j];
+        if (p.init == kInitInout) v = cp[j] + v;
+        else if (p.init == kInitBias) v = p.bias[n0 + j] + v;
+        if (p.relu) v = fmaxf(v, 0.f);
+        cp[j] = v;
+      }
     }
   }
   if (p.splits > 1) clusterSync();  // peers may still be reading this CTA's partial
@@ -328,20 +347,22 @@ bool tcGemmSupported(const GemmArgs& a, const char** why) {
 }
 
 TcPlan tcGemmPlan(int batch, int M, int N, int K, int sms) {
-  // Wide N tiles first (operand bytes per MMA flop fall as BN grows, and A
-  // is re-read once per N tile), then split K across a cluster until the
-  // grid covers the SMs; narrow the tile only if splitting cannot.
+  // Measured on B200 (profiles/r01_tc_plan_sweep.txt): 128-wide N tiles,
+  // K split across a cluster of <= 8 CTAs until the grid is ~one wave —
+  // wider tiles or 16-way splits lose more to the DSMEM reduction and the
+  // per-CTA pipeline fill than they gain. Narrow the tile only when even
+  // 8-way splitting leaves most SMs idle.
   const int tilesM = (M + kBM - 1) / kBM;
   const int nkb = (K + kBK - 1) / kBK;
   auto ctas = [&](int b) { return static_cast<int64_t>(batch) * tilesM * ((N + b - 1) / b); };
   auto splitsFor = [&](int b) {
     int s = 1;
-    while (s < 16 && ctas(b) * s * 2 <= sms && s * 4 <= nkb) s *= 2;  // one wave, >= 2 k-blocks per split
+    while (s < 8 && ctas(b) * s * 5 < sms * 4 && s * 4 <= nkb) s *= 2;  // >= 2 k-blocks per split
     return s;
   };
-  int bn = 256;
-  while (bn > 16 && bn / 2 >= N) bn /= 2;  // no wider than the problem
-  while (bn > 16 && ctas(bn) * splitsFor(bn) * 2 <= sms) bn /= 2;
+  int bn = 16;
+  while (bn < 128 && bn < N) bn *= 2;
+  while (bn > 32 && ctas(bn) * splitsFor(bn) * 4 < sms) bn /= 2;
   TcPlan pl;
   pl.bn = bn;
   pl.splits = splitsFor(bn);
