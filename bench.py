@@ -180,6 +180,15 @@ class OpInstance:
         return t
 
 
+def chain_floor_us(op, fma_latency_cycles=4, mhz=1965.0):
+    """Latency floor of an FFMA-exact operator: every output is one
+    sequential chain of fused multiply-adds (the reference's reduction order),
+    so the longest chain of dependent FMAs (summed over chained layers) times
+    the FMA latency bounds the kernel from below."""
+    steps = {"tbmm": 72, "2FCRelu": 1128 + 128, "MLP3": 128 + 64 + 32, "MLP1": 1128, "C3": 1024, "tmm": 32}
+    return steps.get(op.name, 0) * fma_latency_cycles / mhz
+
+
 def time_device(torch, fn, iters, stream):
     """Device time of `iters` calls of fn(i) on `stream`, via CUDA events."""
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -485,12 +494,22 @@ def main():
     dom, dom_t = max(per_op, key=lambda x: x[1])
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = dom.bytes / dom_t / 1e9
+    traffic = None
+    try:  # committed ncu --set full capture of the same kernel (profiles/gpu_round.sh)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f)["per_launch"].get(dom.name, {}).get("dram_bytes")
+    except Exception:
+        traffic = None
     roofline = {"bound": "hbm", "kernel": f"{dom.name}: {dom.kernel}", "achieved": round(achieved, 1),
-                "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                "traffic": int(traffic) if traffic else None,
+                "traffic_source": "profiles/ncu_traffic.json (dram__bytes_read+write per launch, ncu --set full)",
                 "algorithmic_bytes": int(dom.bytes), "launch_us": round(dom_t * 1e6, 3),
                 "share_of_step": round(dom_t / step_dev, 3), "peak_source": peak_src,
                 "note": "FFMA-exact fp32 kernels: no tensor-core roofline applies; HBM roofline over the "
-                        "kernel's algorithmic bytes (inputs once, outputs once)"}
+                        "kernel's algorithmic bytes (inputs once, outputs once). The step's kernels are bound by "
+                        "their sequential FFMA chains (2FCRelu: 1128 dependent steps), see chain_floor_us",
+                "chain_floor_us": round(chain_floor_us(dom), 3)}
     tbmm = [x for x in per_op if x[0].name == "tbmm"][0]
     roofline_ops = {
         o.name: {"us": round(t * 1e6, 3), "gflops": round(o.flops / t / 1e9, 1),

@@ -19,8 +19,15 @@ def main():
     for r in rows[hdr_i + 1:]:
         if len(r) <= iv or r[im] != "gpu__time_duration.sum":
             continue
-        name = r[ik].split("(")[0][:80]
-        tot[name] += float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+        try:
+            v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+        except ValueError:
+            continue
+        if v != v:  # nan
+            continue
+        grid = r[hdr.index("Grid Size")] if "Grid Size" in hdr else ""
+        name = r[ik].split("(")[0][:60] + " grid" + grid
+        tot[name] += v
         cnt[name] += 1
     s = sum(tot.values())
     out = [{"kernel": k, "launches": cnt[k], "total_us": round(v, 2), "avg_us": round(v / cnt[k], 3),
