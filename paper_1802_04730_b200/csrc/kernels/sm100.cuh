@@ -36,7 +36,7 @@ __device__ __forceinline__ void mbarArrive(uint64_t* bar) {
 }
 // Spins on the barrier phase; traps (reported by the host as a CUDA error)
 // instead of hanging when the phase never completes.
-__device__ __forceinline__ void mbarWait(uint64_t* bar, uint32_t parity, int /*tag*/) {
+__device__ __forceinline__ void mbarWait(uint64_t* bar, uint32_t parity, int tag) {
   const uint32_t addr = smem(bar);
   for (uint32_t spin = 0;; ++spin) {
     uint32_t done;
@@ -50,7 +50,15 @@ __device__ __forceinline__ void mbarWait(uint64_t* bar, uint32_t parity, int /*t
         : "r"(addr), "r"(parity)
         : "memory");
     if (done) return;
+#ifdef TCB_DEBUG_BARRIERS
+    if (spin > (1u << 20)) {  // diagnostic builds: record the stuck barrier and give up
+      printf("tc-b200 debug: mbarrier tag %d parity %u stuck (block %d thread %d)\n", tag, parity, blockIdx.x,
+             threadIdx.x);
+      return;
+    }
+#else
     if (spin > (1u << 24)) __trap();  // never hang: the host reports the launch failure
+#endif
   }
 }
 

@@ -65,9 +65,21 @@ int smCount() {
 // 1 means "plan tile and splits from each contraction's shape" (the FC
 // chains' default: every layer gets its own plan).
 void decodeTc(const Problem& p, const MappingOptions& o, Mapping& m) {
+  if (p.family == Family::Gconv) {
+    k::GconvArgs a{};
+    a.C = p.gconv.C;
+    a.H = p.gconv.H;
+    a.W = p.gconv.W;
+    a.F = p.gconv.F;
+    a.KH = p.gconv.KH;
+    a.KW = p.gconv.KW;
+    const char* why = nullptr;
+    if (!k::tcGconvSupported(a, &why)) invalid(why);
+    return;
+  }
   if (p.family != Family::Gemm && p.family != Family::FcChain)
     invalid(std::string("no tensor-core kernel for the ") + familyName(p.family) +
-            " family (tensor-core math covers TMM, TBMM, C3 and the FC chains)");
+            " family (tensor-core math covers TMM, TBMM, C3, the FC chains and gconv)");
   auto ok4 = [](int64_t v) { return v % 4 == 0; };
   if (p.family == Family::Gemm) {
     const GemmDesc& g = p.gemm;
@@ -204,6 +216,7 @@ std::string Mapping::describe() const {
   os << familyName(family) << ":";
   if (math != k::kMathFfma) {
     os << "tcgen05 " << mathName(math);
+    if (family == Family::Gconv) return os.str() + " implicit-GEMM (on-chip im2col)";
     if (tcAuto) os << " planned";
     else os << " bn=" << tc.bn << " splits=" << tc.splits;
     if (family == Family::FcChain) os << " per-layer";
@@ -471,6 +484,12 @@ Mapping decode(const Problem& p, const MappingOptions& o, int math) {
 
 MappingOptions defaultOptions(const Problem& p, int math) {
   MappingOptions o;
+  if (math != k::kMathFfma && p.family == Family::Gconv) {
+    o.tileSizes = {128, static_cast<int64_t>(p.gconv.F), 8};  // pixels x filters x channels per UMMA
+    o.threadShape = {{384, 1, 1}};
+    o.useShared = true;
+    return o;
+  }
   if (math != k::kMathFfma && (p.family == Family::Gemm || p.family == Family::FcChain)) {
     // tensor-core plan for the (first) contraction; FC layers replan per layer
     int batch = 1, M = 0, N = 0, K = 0;
@@ -721,7 +740,13 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
       a.KH = d.KH;
       a.KW = d.KW;
       a.Mb = d.Mb;
-      check(k::launchGconv(a, m.gconvVariant, m.th, s), "gconv");
+      if (m.math != k::kMathFfma) {
+        const char* why = nullptr;
+        if (!k::tcGconvSupported(a, &why)) fail(ErrorKind::MappingInvalid, why);
+        check(k::launchTcGconv(a, m.math, s), "tensor-core gconv");
+      } else {
+        check(k::launchGconv(a, m.gconvVariant, m.th, s), "gconv");
+      }
       return;
     }
     case Family::Lut: {

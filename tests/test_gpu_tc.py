@@ -174,3 +174,40 @@ def test_tc_explicit_plan_and_errors(env):
         run(ee, "3KRU", Ws + [X], [np.zeros((4, 32, 32, 32), np.float32), np.zeros((4, 16, 32, 32), np.float32),
                                    np.zeros((4, 16, 16, 32), np.float32)], "tf32")
     assert ei.value.kind == "MappingInvalid"
+
+
+GCONV_CASES = [  # (N, G, C, H, W, F, KH, KW, Mb)
+    (2, 3, 16, 10, 10, 16, 3, 3, 16),
+    (1, 2, 16, 58, 58, 16, 3, 3, 16),     # the paper shape's N=1, G=2 slice
+    (3, 2, 8, 20, 36, 32, 3, 3, 4),       # 34-wide rows (VW=64), 8 channels, F=32
+    (2, 1, 16, 12, 20, 16, 5, 5, 3),      # 5x5 taps, 16-wide rows (VW=32)
+]
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("case", GCONV_CASES)
+def test_gconv_tc(env, case, math):
+    ee, orc = env
+    N, G, C, H, W, F, KH, KW, Mb = case
+    rng = orc.rng(31 + H + F)
+    I, W1, Bv = rng.f32((N, G, C, H, W)), rng.f32((G, F, C, KH, KW)), rng.f32((Mb,))
+    ref = orc.gconv(I, W1, Bv)
+    (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros(ref.shape, np.float32)], math)
+    assert "tcgen05" in desc["kernel"]
+    K = C * KH * KW
+    err = max_rel(ref, got)
+    record(f"gconv {case}", math, K, err, None, None)
+    assert err <= tol(math, K), f"gconv {case} {math}: maxRel {err:.3g} > {tol(math, K):.3g}"
+
+
+def test_gconv_tc_paper_shape_sampled(env):
+    """tcgen05 gconv at the BASELINE shape, 200k sampled points vs the oracle."""
+    ee, orc = env
+    rng = orc.rng(11)
+    I, W1, Bv = rng.f32((32, 32, 16, 58, 58)), rng.f32((32, 16, 16, 3, 3)), rng.f32((16,))
+    (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros((32, 32, 16, 56, 56), np.float32)], "3xtf32")
+    idx = np.random.default_rng(0).integers(0, got.size, 200_000)
+    ref = orc.gconv_points(I, W1, Bv, idx)
+    err = max_rel(ref, got.reshape(-1)[idx])
+    record("gconv paper shape sampled", "3xtf32", 144, err, None, None)
+    assert err <= tol("3xtf32", 144)
