@@ -109,6 +109,8 @@ cudaError_t launchGconv(const GconvArgs& a, int variant, int th, cudaStream_t s)
 // tcgen05 implicit-GEMM gconv (tc_gconv.cu), tensor-core math only
 bool tcGconvSupported(const GconvArgs& a, const char** why);
 cudaError_t launchTcGconv(const GconvArgs& a, int math, cudaStream_t s);
+// the default: NHWC staging copy + TMA-fed tcgen05 (tc_gconv_tma.cu)
+cudaError_t launchTcGconvTma(const GconvArgs& a, int math, cudaStream_t s);
 size_t gconvSmem(const GconvArgs& a, int th, int rw);
 int gconvThreads(const GconvArgs& a, int variant, int th);
 

@@ -43,7 +43,11 @@ __device__ __forceinline__ void mbarWait(uint64_t* bar, uint32_t parity, int tag
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
+#ifdef TCB_MBAR_TEST_WAIT
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+#endif
         "selp.u32 %0, 1, 0, p;\n"
         "}\n"
         : "=r"(done)

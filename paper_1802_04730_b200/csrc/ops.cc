@@ -75,6 +75,9 @@ void decodeTc(const Problem& p, const MappingOptions& o, Mapping& m) {
     a.KW = p.gconv.KW;
     const char* why = nullptr;
     if (!k::tcGconvSupported(a, &why)) invalid(why);
+    // tile_sizes[2] == 2 selects the NHWC-staging variant; otherwise the
+    // on-chip im2col kernel (the faster of the two on B200, profiles/README.md)
+    m.gconvVariant = (o.tileSizes.size() > 2 && o.tileSizes[2] == 2) ? 0 : 1;
     return;
   }
   if (p.family != Family::Gemm && p.family != Family::FcChain)
@@ -216,7 +219,8 @@ std::string Mapping::describe() const {
   os << familyName(family) << ":";
   if (math != k::kMathFfma) {
     os << "tcgen05 " << mathName(math);
-    if (family == Family::Gconv) return os.str() + " implicit-GEMM (on-chip im2col)";
+    if (family == Family::Gconv)
+      return os.str() + (gconvVariant == 1 ? " implicit-GEMM (on-chip im2col)" : " implicit-GEMM (NHWC staging)");
     if (tcAuto) os << " planned";
     else os << " bn=" << tc.bn << " splits=" << tc.splits;
     if (family == Family::FcChain) os << " per-layer";
@@ -485,7 +489,7 @@ Mapping decode(const Problem& p, const MappingOptions& o, int math) {
 MappingOptions defaultOptions(const Problem& p, int math) {
   MappingOptions o;
   if (math != k::kMathFfma && p.family == Family::Gconv) {
-    o.tileSizes = {128, static_cast<int64_t>(p.gconv.F), 8};  // pixels x filters x channels per UMMA
+    o.tileSizes = {128, static_cast<int64_t>(p.gconv.F), 1};  // 128 pixels x F filters; 1 = on-chip im2col
     o.threadShape = {{384, 1, 1}};
     o.useShared = true;
     return o;
@@ -743,7 +747,8 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
       if (m.math != k::kMathFfma) {
         const char* why = nullptr;
         if (!k::tcGconvSupported(a, &why)) fail(ErrorKind::MappingInvalid, why);
-        check(k::launchTcGconv(a, m.math, s), "tensor-core gconv");
+        check(m.gconvVariant == 1 ? k::launchTcGconv(a, m.math, s) : k::launchTcGconvTma(a, m.math, s),
+              "tensor-core gconv");
       } else {
         check(k::launchGconv(a, m.gconvVariant, m.th, s), "gconv");
       }

@@ -184,19 +184,27 @@ GCONV_CASES = [  # (N, G, C, H, W, F, KH, KW, Mb)
 ]
 
 
+@pytest.mark.parametrize("variant", ["nhwc", "im2col"])
 @pytest.mark.parametrize("math", ["3xtf32", "tf32"])
 @pytest.mark.parametrize("case", GCONV_CASES)
-def test_gconv_tc(env, case, math):
+def test_gconv_tc(env, case, math, variant):
+    """variant: the on-chip im2col kernel (default) or the NHWC-staging
+    kernel (tile_sizes[2] == 2)."""
+    from paper_1802_04730_b200 import options_baseline
     ee, orc = env
     N, G, C, H, W, F, KH, KW, Mb = case
     rng = orc.rng(31 + H + F)
     I, W1, Bv = rng.f32((N, G, C, H, W)), rng.f32((G, F, C, KH, KW)), rng.f32((Mb,))
     ref = orc.gconv(I, W1, Bv)
-    (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros(ref.shape, np.float32)], math)
-    assert "tcgen05" in desc["kernel"]
+    opts = None
+    if variant == "nhwc":
+        opts = json.loads(options_baseline(0))
+        opts.update({"tile_sizes": [128, F, 2], "thread_shape": [512, 1, 1]})
+    (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros(ref.shape, np.float32)], math, opts)
+    assert "tcgen05" in desc["kernel"] and ("im2col" in desc["kernel"]) == (variant == "im2col")
     K = C * KH * KW
     err = max_rel(ref, got)
-    record(f"gconv {case}", math, K, err, None, None)
+    record(f"gconv {case} {variant}", math, K, err, None, None)
     assert err <= tol(math, K), f"gconv {case} {math}: maxRel {err:.3g} > {tol(math, K):.3g}"
 
 
