@@ -158,9 +158,12 @@ int tcb_describe(tcb_engine* e, uint64_t handle, char* buf, int len);
 
 /* tuner::tune on the GPU. tune_options_json keys (all optional):
  * population (100), generations (25), mutation_rate (0.05), seed (0),
- * timing_iters (10), session_log (path), use_baselines (true).
- * Writes the best MappingOptions JSON. Every evaluated candidate updates
- * the process cache (min-update). */
+ * timing_iters (10), session_log (path), use_baselines (true),
+ * math ("ffma" | "tf32" | "3xtf32": tune the tcgen05 tile/split genes; a
+ * candidate must then agree with the mode's default plan within the stated
+ * tolerance instead of bit-for-bit). Writes the best MappingOptions JSON.
+ * Every evaluated candidate updates the process cache (min-update; the
+ * tensor-core modes under the " math=<mode>" target). */
 int tcb_tune(tcb_engine* e, const char* name, const tcb_tensor* inputs, int n_inputs,
              const tcb_tensor* outputs, int n_outputs, const char* tune_options_json, char* best_json,
              int best_len);

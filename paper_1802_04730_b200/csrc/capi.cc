@@ -428,7 +428,6 @@ int tcb_tune(tcb_engine* e, const char* name, const tcb_tensor* in, int nin, con
     sem::Specialized s = e->specialize(name, in, nin, out, nout);
     std::string canon = cache::canonicalize(s.v);
     ops::Problem p = ops::match(s, canon);
-    cache::Key key = cache::makeKey(s.v, e->paramShapes(s), MappingOptions{});
     TuneOptions o;
     if (topts && *topts) {
       Json j;
@@ -447,7 +446,10 @@ int tcb_tune(tcb_engine* e, const char* name, const tcb_tensor* in, int nin, con
       if (j.has("timing_iters")) o.timingIters = static_cast<int>(j.at("timing_iters").asInt());
       if (j.has("session_log")) o.sessionLog = j.at("session_log").asStr();
       if (j.has("use_baselines")) o.useBaselines = j.at("use_baselines").asBool();
+      if (j.has("math")) o.math = ops::mathFromName(j.at("math").asStr());
     }
+    const std::string suffix = o.math ? std::string(" math=") + ops::mathName(o.math) : std::string();
+    cache::Key key = cache::makeKey(s.v, e->paramShapes(s), MappingOptions{}, suffix);
     TuneResult r = tune(s, p, key, o, &globalCache());
     Json res = Json::parse(r.best.toJson());
     copyOut(res.dump(), best, len);

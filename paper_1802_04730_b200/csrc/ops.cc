@@ -1,6 +1,7 @@
 // ops.cc — operator registry, tensor binding, option decoding, launch.
 #include "ops.h"
 
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <sstream>
@@ -598,8 +599,43 @@ MappingOptions defaultOptions(const Problem& p, int math) {
   return o;
 }
 
-GenePools genePools(const Problem& p) {
+double tcTolerance(const Problem& p, int math) {
+  int64_t K = 1;
+  switch (p.family) {
+    case Family::Gemm: K = p.gemm.K; break;
+    case Family::FcChain:
+      for (const auto& L : p.fc.layers) K = std::max<int64_t>(K, L.kred);
+      break;
+    case Family::Gconv: K = (int64_t)p.gconv.C * p.gconv.KH * p.gconv.KW; break;
+    default: break;
+  }
+  // between two tensor-core plans both errors count: twice the per-mode bound
+  const double one = math == k::kMath3xTf32 ? 1e-5 + K * std::ldexp(1.0, -23) : K * std::ldexp(1.0, -11);
+  return 2.0 * one;
+}
+
+GenePools genePools(const Problem& p, int math) {
   GenePools g;
+  if (math != k::kMathFfma) {
+    g.tx = {256};
+    g.ty = {1};
+    g.tz = {1};
+    g.useShared = {1};
+    g.fusion = {Fusion::Min};
+    if (p.family == Family::Gconv) {
+      g.tile0 = {128};
+      g.tile1 = {static_cast<int64_t>(p.gconv.F)};
+      g.tile2 = {1, 2};  // on-chip im2col | NHWC staging
+      g.bz = {1};
+    } else {
+      g.tile0 = {128};
+      g.tile1 = {16, 32, 64, 128, 256};
+      if (p.family == Family::FcChain) g.tile1.push_back(1);  // 1 = plan each layer
+      g.tile2 = {32};
+      g.bz = {1, 2, 4, 8, 16};
+    }
+    return g;
+  }
   switch (p.family) {
     case Family::Gemm:
     case Family::FcChain:

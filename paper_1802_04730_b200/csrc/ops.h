@@ -113,10 +113,14 @@ int mathFromName(const std::string& s);  // Error(MappingInvalid)
 // Gene pools for the tuner (TuningSpace per family; see tuner.cc).
 struct GenePools {
   std::vector<int64_t> tile0, tile1, tile2, tx, ty, tz;
+  std::vector<int64_t> bz{1};  // block_shape[2]: tensor-core K splits (1 for the FFMA families)
   std::vector<Fusion> fusion;
   std::vector<int> useShared;  // {0,1} or {1}
 };
-GenePools genePools(const Problem& p);
+GenePools genePools(const Problem& p, int math = k::kMathFfma);
+// the stated tolerance of a tensor-core mode for this problem,
+// max |got - ref| / max(|ref|, 1) against the FFMA/TC reference candidate
+double tcTolerance(const Problem& p, int math);
 
 // Launches the whole definition on `stream`. in/out are device pointers in
 // declaration order. errFlag: device int for data-dependent index checks.

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <ctime>
 #include <fstream>
@@ -61,8 +62,8 @@ struct Space {
       case 1: return pick(pools.tile1, g);
       case 2: return pick(pools.tile2, g);
       case 3:
-      case 4:
-      case 5: return 1;  // grid extents are derived from the problem
+      case 4: return 1;  // grid extents are derived from the problem
+      case 5: return pick(pools.bz, g);  // tensor-core K splits (1 otherwise)
       case 6: return pick(pools.tx, g);
       case 7: return pick(pools.ty, g);
       case 8: return pick(pools.tz, g);
@@ -169,10 +170,25 @@ struct DeviceSession {
   }
 };
 
+// max |a - b| / max(|b|, 1) over fp32 buffers (tensor_data.cc:221-234)
+double maxRel(const std::vector<std::vector<char>>& a, const std::vector<std::vector<char>>& b) {
+  double worst = 0;
+  for (size_t t = 0; t < a.size() && t < b.size(); ++t) {
+    const size_t n = std::min(a[t].size(), b[t].size()) / 4;
+    const float* x = reinterpret_cast<const float*>(a[t].data());
+    const float* y = reinterpret_cast<const float*>(b[t].data());
+    for (size_t i = 0; i < n; ++i) {
+      const double d = std::fabs((double)x[i] - (double)y[i]) / std::max(1.0, std::fabs((double)y[i]));
+      if (!(d <= worst)) worst = d;  // NaN propagates as a failure
+    }
+  }
+  return worst;
+}
+
 void score(Candidate& c, const ops::Problem& p, DeviceSession& ds, int iters,
-           std::optional<std::vector<std::vector<char>>>& refOut) {
+           std::optional<std::vector<std::vector<char>>>& refOut, int math = 0) {
   try {
-    ops::Mapping m = ops::decode(p, c.genome);
+    ops::Mapping m = ops::decode(p, c.genome, math);
     c.text = m.describe();
     // correctness run from pristine outputs
     ds.reset();
@@ -182,10 +198,11 @@ void score(Candidate& c, const ops::Problem& p, DeviceSession& ds, int iters,
     if (e != cudaSuccess) fail(ErrorKind::Cuda, cudaGetErrorString(e));
     if (!refOut) {
       refOut = got;
-    } else if (got != *refOut) {
+    } else if (math == 0 ? got != *refOut : !(maxRel(got, *refOut) <= ops::tcTolerance(p, math))) {
       c.ok = false;
       c.fitness = 0;
-      c.failure = "output mismatch against the reference candidate";
+      c.failure = math == 0 ? "output mismatch against the reference candidate"
+                            : "outside the tensor-core tolerance of the reference candidate";
       return;
     }
     cudaEvent_t a, b;
@@ -230,15 +247,15 @@ TuneResult tune(const sem::Specialized& s, const ops::Problem& p, const cache::K
                 cache::Cache* c) {
   TCB_CHECK(o.population >= 1, "population must hold at least one genome");
   Space space;
-  space.pools = ops::genePools(p);
+  space.pools = ops::genePools(p, o.math);
 
   std::vector<MappingOptions> starting;
   if (c) {
     if (auto hit = c->lookup(key)) starting.push_back(hit->options);
   }
   for (const auto& x : o.extraStarting) starting.push_back(x);
-  starting.push_back(ops::defaultOptions(p));
-  if (o.useBaselines)
+  starting.push_back(ops::defaultOptions(p, o.math));
+  if (o.useBaselines && o.math == 0)  // the reference presets describe FFMA mappings
     for (const auto& b : baselineOptions()) starting.push_back(b);
 
   std::mt19937_64 g(o.seed);
@@ -265,8 +282,8 @@ TuneResult tune(const sem::Specialized& s, const ops::Problem& p, const cache::K
   std::optional<std::vector<std::vector<char>>> refOut;
   {
     Candidate ref;
-    ref.genome = ops::defaultOptions(p);
-    score(ref, p, ds, 1, refOut);
+    ref.genome = ops::defaultOptions(p, o.math);
+    score(ref, p, ds, 1, refOut, o.math);
     if (!ref.ok) fail(ErrorKind::NoViableCandidate, "the default mapping failed: " + ref.failure);
   }
 
@@ -278,7 +295,7 @@ TuneResult tune(const sem::Specialized& s, const ops::Problem& p, const cache::K
   std::optional<Candidate> best;
   for (size_t gen = 0;; ++gen) {
     for (auto& cd : pop) {
-      score(cd, p, ds, o.timingIters, refOut);
+      score(cd, p, ds, o.timingIters, refOut, o.math);
       ++res.evaluated;
       if (!cd.ok) {
         ++res.failed;

@@ -33,6 +33,11 @@ struct TuneOptions {
   std::string sessionLog;
   bool useBaselines = true;
   std::vector<MappingOptions> extraStarting;
+  // k::MathMode. Tensor-core modes tune the tcgen05 tile/split genes; a
+  // candidate then passes when it agrees with the mode's default plan within
+  // ops::tcTolerance (different K splits sum in different orders), instead
+  // of the FFMA modes' bit equality.
+  int math = 0;
 };
 
 struct TuneResult {

@@ -219,3 +219,37 @@ def test_gconv_tc_paper_shape_sampled(env):
     err = max_rel(ref, got.reshape(-1)[idx])
     record("gconv paper shape sampled", "3xtf32", 144, err, None, None)
     assert err <= tol("3xtf32", 144)
+
+
+@pytest.mark.parametrize("math", ["tf32", "3xtf32"])
+def test_tc_tuner_and_cache_replay(env, tmp_path, math):
+    """The genetic tuner over the tcgen05 genes (tile N, K splits): every
+    candidate is held to the mode's tolerance against the default plan, the
+    cache records entries under the ' math=<mode>' target, and a later
+    tensor-core compile replays the best plan while the FFMA compile of the
+    same shapes does not see it."""
+    import paper_1802_04730_b200 as tcb
+    ee, orc = env
+    tcb.cache_purge()
+    rng = orc.rng(8)
+    A, B, Cin = rng.f32((128, 1024)), rng.f32((1000, 1024)), rng.f32((128, 1000))
+    ref = orc.c3(A, B, Cin)
+    dA, dB = dev(A), dev(B)
+    dC = dev(Cin)
+    log = tmp_path / "tc_session.jsonl"
+    best = ee.tune("C3", [dA, dB], [dC], population=10, generations=2, seed=3, timing_iters=3, math=math,
+                   session_log=str(log))
+    assert best["tile_sizes"][1] in (16, 32, 64, 128, 256) and best["block_shape"][2] in (1, 2, 4, 8, 16)
+    ents = tcb.cache_entries()
+    assert len(ents) == 1 and ents[0]["target"].endswith(f" math={math}")
+    costs = [json.loads(x)["best_cost"] for x in log.read_text().splitlines()]
+    assert all(a >= b for a, b in zip(costs, costs[1:]))
+    h = ee.compile("C3", [dA, dB], [dC], math=math)
+    d = ee.describe(h)
+    assert d["options_source"] == "cache" and d["options"] == best
+    dC.copy_(torch.from_numpy(Cin))
+    ee.run(h, [dA, dB], [dC])
+    torch.cuda.synchronize()
+    assert max_rel(ref, dC.cpu().numpy()) <= tol(math, 1024)
+    assert ee.describe(ee.compile("C3", [dA, dB], [dC]))["options_source"] == "default"
+    tcb.cache_purge()
