@@ -34,6 +34,12 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+__device__ __forceinline__ float4 ldsV4(unsigned addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ float initValue(const GemmArgs& a, const float* C, int m, int n) {
   if (a.init == kInitInout) return C[(int64_t)m * a.ldc + n];
   if (a.init == kInitBias) return a.bias[n];
@@ -114,11 +120,15 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
     const int st = t % S;
     const float* Ast = &As[st][ty][0];
     const float* Bst = &Bs[st][tx][0];
+    // volatile shared loads: the compiler keeps them where they are written
+    // (it otherwise sinks them next to their FFMAs, exposing the latency)
+    const unsigned aS = static_cast<unsigned>(__cvta_generic_to_shared(Ast));
+    const unsigned bS = static_cast<unsigned>(__cvta_generic_to_shared(Bst));
     auto loadGroup = [&](int kk, float4* av, float4* bv) {
 #pragma unroll
-      for (int i = 0; i < RM; ++i) av[i] = *reinterpret_cast<const float4*>(Ast + i * TY * LD + kk);
+      for (int i = 0; i < RM; ++i) av[i] = ldsV4(aS + (i * TY * LD + kk) * 4);
 #pragma unroll
-      for (int j = 0; j < RN; ++j) bv[j] = *reinterpret_cast<const float4*>(Bst + j * TX * LD + kk);
+      for (int j = 0; j < RN; ++j) bv[j] = ldsV4(bS + (j * TX * LD + kk) * 4);
     };
     auto fmaGroup = [&](const float4* av, const float4* bv) {  // one 4-k step of every chain
 #pragma unroll
@@ -145,16 +155,16 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN))
     };
     const int klim = min(TK, a.K - t * TK);
     if (klim == TK) {
-      // full tile: register double buffer — group g+1's shared loads are
-      // issued before group g's FFMAs, so their latency hides behind them
-      float4 a0[RM], b0[RN], a1[RM], b1[RN];
-      loadGroup(0, a0, b0);
+      // full tile: register ring of 3 groups — group g+2's shared loads are
+      // issued before group g's FFMAs, so their latency hides behind two
+      // groups of FFMAs
+      float4 ra[3][RM], rb[3][RN];
+      loadGroup(0, ra[0], rb[0]);
+      if (TK > 4) loadGroup(4, ra[1], rb[1]);
 #pragma unroll
-      for (int kk = 0; kk < TK; kk += 8) {
-        if (kk + 4 < TK) loadGroup(kk + 4, a1, b1);
-        fmaGroup(a0, b0);
-        if (kk + 8 < TK) loadGroup(kk + 8, a0, b0);
-        if (kk + 4 < TK) fmaGroup(a1, b1);
+      for (int g = 0; g < TK / 4; ++g) {
+        if (g + 2 < TK / 4) loadGroup((g + 2) * 4, ra[(g + 2) % 3], rb[(g + 2) % 3]);
+        fmaGroup(ra[g % 3], rb[g % 3]);
       }
     } else {
       const int k4 = klim & ~3;
@@ -387,6 +397,13 @@ const GemmVariant kGemmVariants[] = {
     {20, 1, 1, 1, 1, 0, "batched_r1x1", 0},
     {21, 1, 1, 2, 1, 0, "batched_r2x1", 0},
     {22, 1, 1, 1, 2, 0, "batched_r1x2", 0},
+    // deeper k stages for long reductions (more bytes in flight per CTA)
+    {23, 32, 32, 2, 2, 64, "t32x32_r2x2_k64_s8", 8},
+    {24, 32, 32, 2, 2, 128, "t32x32_r2x2_k128", 4},
+    {25, 32, 64, 2, 4, 64, "t32x64_r2x4_k64", 4},
+    {26, 16, 64, 2, 4, 64, "t16x64_r2x4_k64", 4},
+    {27, 16, 32, 2, 2, 64, "t16x32_r2x2_k64_s8", 8},
+    {28, 32, 16, 2, 2, 64, "t32x16_r2x2_k64", 4},
 };
 
 template <int RM, int RN>
@@ -469,6 +486,12 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
     case 16: return launchTiled<32, 32, 2, 2, 32, 8>(a, vec, s);
     case 17: return launchTiled<16, 32, 2, 2, 32, 8>(a, vec, s);
     case 18: return launchTiled<16, 16, 1, 1, 64>(a, vec, s);
+    case 23: return launchTiled<32, 32, 2, 2, 64, 8>(a, vec, s);
+    case 24: return launchTiled<32, 32, 2, 2, 128, 4>(a, vec, s);
+    case 25: return launchTiled<32, 64, 2, 4, 64, 4>(a, vec, s);
+    case 26: return launchTiled<16, 64, 2, 4, 64, 4>(a, vec, s);
+    case 27: return launchTiled<16, 32, 2, 2, 64, 8>(a, vec, s);
+    case 28: return launchTiled<32, 16, 2, 2, 64, 4>(a, vec, s);
     case 19:
     case 20:
     case 21:
