@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(1024)
     for (int b = 0; b < 2 * layers; ++b) mbarInit(&bars[b], 1);
     // the pushed activations of every later layer: R rows x all columns
     // (armed before any peer can push: see the cluster arrive below)
-    for (int l = 1; l < layers; ++l) mbarExpectTx(&bars[l], (unsigned)(R * a.L[l - 1].out * 4));
+    if (cn > 1)
+      for (int l = 1; l < layers; ++l) mbarExpectTx(&bars[l], (unsigned)(R * a.L[l - 1].out * 4));
     FC_STAMP(1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     FC_STAMP(5);
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(1024)
     const bool last = l + 1 == layers;
     const int ald = p.ald[l];
     const unsigned actBase = smemAddr(sm + p.offAct[l]), wBase = smemAddr(sm + p.offW[l]);
-    if (l > 0 || p.bulk) mbarWait(&bars[l], 0, l);
+    if ((l > 0 && cn > 1) || (l == 0 && p.bulk)) mbarWait(&bars[l], 0, l);
     if (p.bulk) mbarWait(&bars[layers + l], 0, layers + l);
     FC_STAMP(3 + 3 * l);
     if (!last && l == 0 && cn > 1) asm volatile("barrier.cluster.wait;" ::: "memory");
@@ -316,12 +317,17 @@ __global__ void __launch_bounds__(1024)
         const float v = fmaxf(acc, 0.0f);
         if (r < rows) L.O[(int64_t)(row0 + r) * L.out + c0 + c] = v;
         if (!last) {  // push into the next layer's input buffer of every cluster CTA
-          const float* dst = sm + p.offAct[l + 1] + r * p.ald[l + 1] + c0 + c;
-          for (int q = 0; q < cn; ++q) stAsyncCluster(dst, &bars[l + 1], q, v);
+          float* dst = sm + p.offAct[l + 1] + r * p.ald[l + 1] + c0 + c;
+          if (cn > 1) {
+            for (int q = 0; q < cn; ++q) stAsyncCluster(dst, &bars[l + 1], q, v);
+          } else {
+            *dst = v;  // a lone CTA: plain store, published by the barrier below
+          }
         }
       }
     }
     FC_STAMP(4 + 3 * l);
+    if (!last && cn == 1) __syncthreads();
   }
   if (cn > 1 && layers == 1) asm volatile("barrier.cluster.wait;" ::: "memory");  // pair the arrive
   FC_STAMP(15);
