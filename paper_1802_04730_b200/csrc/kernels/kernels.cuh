@@ -54,6 +54,7 @@ enum MathMode : int { kMathFfma = 0, kMathTf32 = 1, kMath3xTf32 = 3 };
 struct TcPlan {
   int bn = 128;     // output columns per CTA (UMMA N, multiple of 16 in [16, 256])
   int splits = 1;   // K splits = cluster size along z (power of two <= 16)
+  int packP = 0;    // > 1: block-diagonal packing of packP small batches per 128-row tile
 };
 bool tcGemmSupported(const GemmArgs& a, const char** why);
 TcPlan tcGemmPlan(int batch, int M, int N, int K, int sms);

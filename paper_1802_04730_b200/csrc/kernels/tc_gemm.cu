@@ -49,6 +49,10 @@ struct TcParams {
   int init, relu;
   int splits, kbPerSplit, nkb;
   int aBatched, bBatched;
+  // block-diagonal packing of many small batches (TBMM): CTA tile t holds
+  // batches [t*packP, t*packP + packP) stacked along M (rows of M each) and
+  // along N; only the diagonal blocks are stored. 0 = no packing.
+  int packP, batch;
 };
 
 template <int BN, bool X3>
@@ -113,13 +117,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       const int ba = p.aBatched ? b : 0, bb = p.bBatched ? b : 0;
+      // packed: the maps view A, B as [batch * M][K] and [batch * N][K]
+      const int arow = p.packP ? mt * p.packP * p.M : mt * kBM;
+      const int brow = p.packP ? mt * p.packP * p.N : nt * BN;
       for (int i = 0; i < nk; ++i) {
         const int s = i % S;
         if (i >= S) mbarWait(&empty[s], ((i / S) - 1) & 1, 1);
         mbarExpectTx(&full[s], Cfg::kABytes + Cfg::kBBytes);
         const int kc = (kb0 + i) * kBK;
-        tmaLoad3d(aBig(s), &tmA, kc, mt * kBM, ba, &full[s]);
-        tmaLoad3d(bBig(s), &tmB, kc, nt * BN, bb, &full[s]);
+        tmaLoad3d(aBig(s), &tmA, kc, arow, ba, &full[s]);
+        tmaLoad3d(bBig(s), &tmB, kc, brow, bb, &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -212,8 +219,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int R = kBM / p.splits;
     const uint32_t base = smem(sm);
     const int64_t cb = static_cast<int64_t>(b) * p.sC;
+    if (p.packP) {
+      // diagonal blocks only: row r = (batch i, m), column c = (batch j, n), i == j
+      for (int idx = threadIdx.x; idx < kBM * BN; idx += kThreads) {
+        const int row = idx / BN, col = idx % BN;
+        const int i = row / p.M, j = col / p.N;
+        const int bq = mt * p.packP + i;
+        if (i != j || i >= p.packP || bq >= p.batch) continue;
+        const int m = row - i * p.M, n = col - j * p.N;
+        float v = *reinterpret_cast<const float*>(sm + (row * Cfg::kPartLd + col) * 4);
+        float* cp = p.C + static_cast<int64_t>(bq) * p.sC + static_cast<int64_t>(m) * p.ldc + n;
+        if (p.init == kInitInout) v = *cp + v;
+        else if (p.init == kInitBias) v = p.bias[n] + v;
+        if (p.relu) v = fmaxf(v, 0.f);
+        *cp = v;
+      }
+    }
     constexpr int Q = BN / 4;  // float4 column groups per row
-    for (int idx = threadIdx.x; idx < R * Q; idx += kThreads) {
+    for (int idx = threadIdx.x; !p.packP && idx < R * Q; idx += kThreads) {
       const int row = split * R + idx / Q, col = (idx % Q) * 4;
       const int m = mt * kBM + row, n0 = nt * BN + col;
       if (m >= p.M || n0 >= p.N) continue;
@@ -360,6 +383,19 @@ TcPlan tcGemmPlan(int batch, int M, int N, int K, int sms) {
     while (s < 8 && ctas(b) * s * 5 < sms * 4 && s * 4 <= nkb) s *= 2;  // >= 2 k-blocks per split
     return s;
   };
+  if (batch > 1 && M <= 64 && N <= 128) {
+    // many small batches: stack P of them per 128-row tile, block-diagonally
+    int P = std::min(kBM / M, 256 / N);
+    int bn = 16;
+    while (bn < P * N) bn *= 2;
+    if (P > 1 && bn <= 256) {
+      TcPlan pl;
+      pl.bn = bn;
+      pl.splits = 1;
+      pl.packP = P;
+      return pl;
+    }
+  }
   int bn = 16;
   while (bn < 128 && bn < N) bn *= 2;
   while (bn > 32 && ctas(bn) * splitsFor(bn) * 4 < sms) bn /= 2;
@@ -399,7 +435,24 @@ cudaError_t launchTcGemm(const GemmArgs& a, int math, const TcPlan& pl, cudaStre
   }
   p.aBatched = a.sA != 0 && a.batch > 1;
   p.bBatched = a.sB != 0 && a.batch > 1;
-  const int tilesN = (a.N + bn - 1) / bn, tilesM = (a.M + kBM - 1) / kBM;
+  p.packP = 0;
+  p.batch = a.batch;
+  int tilesN = (a.N + bn - 1) / bn, tilesM = (a.M + kBM - 1) / kBM;
+  const bool contiguous = a.batch > 1 && a.sA == (int64_t)a.M * a.lda && a.sB == (int64_t)a.N * a.ldb &&
+                          a.lda == a.K && a.ldb == a.K;
+  if (pl.packP > 1 && contiguous) {
+    // block-diagonal packing: 2-D views of the contiguous batches
+    p.packP = pl.packP;
+    p.splits = 1;
+    p.kbPerSplit = p.nkb;
+    p.aBatched = p.bBatched = 0;
+    if (!makeMap(&ta, a.A, a.K, a.batch * a.M, 1, a.lda, 0, kBM)) return cudaErrorInvalidValue;
+    if (!makeMap(&tb, a.B, a.K, a.batch * a.N, 1, a.ldb, 0, bn)) return cudaErrorInvalidValue;
+    tilesN = 1;
+    tilesM = (a.batch + p.packP - 1) / p.packP;
+    return math == kMath3xTf32 ? dispatchBn<true>(bn, ta, tb, p, tilesN, tilesM, 1, s)
+                               : dispatchBn<false>(bn, ta, tb, p, tilesN, tilesM, 1, s);
+  }
   return math == kMath3xTf32 ? dispatchBn<true>(bn, ta, tb, p, tilesN, tilesM, a.batch, s)
                              : dispatchBn<false>(bn, ta, tb, p, tilesN, tilesM, a.batch, s);
 }

@@ -496,16 +496,10 @@ MappingOptions defaultOptions(const Problem& p, int math) {
     return o;
   }
   if (math != k::kMathFfma && (p.family == Family::Gemm || p.family == Family::FcChain)) {
-    // tensor-core plan for the (first) contraction; FC layers replan per layer
-    int batch = 1, M = 0, N = 0, K = 0;
-    if (p.family == Family::Gemm) {
-      batch = p.gemm.batch, M = p.gemm.M, N = p.gemm.N, K = p.gemm.K;
-    } else {
-      M = p.fc.batch, N = p.fc.layers[0].out, K = p.fc.layers[0].kred;
-    }
-    k::TcPlan pl = k::tcGemmPlan(batch, M, N, K, smCount());
-    o.tileSizes = {128, p.family == Family::Gemm ? pl.bn : 1, 32};
-    o.blockShape = {{1, 1, p.family == Family::Gemm ? pl.splits : 1}};
+    // tile N = 1: plan tile, K splits and batch packing from the shape at
+    // launch (k::tcGemmPlan); the tuner explores explicit values
+    o.tileSizes = {128, 1, 32};
+    o.blockShape = {{1, 1, 1}};
     o.threadShape = {{256, 1, 1}};
     o.useShared = true;
     o.fusion = Fusion::Min;
@@ -629,8 +623,7 @@ GenePools genePools(const Problem& p, int math) {
       g.bz = {1};
     } else {
       g.tile0 = {128};
-      g.tile1 = {16, 32, 64, 128, 256};
-      if (p.family == Family::FcChain) g.tile1.push_back(1);  // 1 = plan each layer
+      g.tile1 = {1, 16, 32, 64, 128, 256};  // 1 = plan at launch (per layer for the FC chains)
       g.tile2 = {32};
       g.bz = {1, 2, 4, 8, 16};
     }

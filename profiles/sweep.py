@@ -35,6 +35,8 @@ def main():
     for v in [{}] + variants:
         o = dict(base)
         o.update(v)
+        if not v and math != "ffma":
+            o = None  # the tensor-core plan (no explicit options)
         try:
             h = ee.compile(name, sets[0][0], sets[0][1], o, math=math)
             desc = ee.describe(h)["kernel"]
