@@ -13,6 +13,8 @@
 // KW taps: RF·RW·KW FFMAs per (RW+KW-1) scalar + KW vector smem loads.
 // The chain order per output is exactly the reference's (i, kh, kw), and
 // the bias loop adds B[0..M-1] sequentially (__fadd_rn, no contraction).
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace tcb {
@@ -20,97 +22,130 @@ namespace k {
 
 namespace {
 
+__device__ __forceinline__ void cpAsync4(float* dst, const float* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(ok ? 4 : 0)
+               : "memory");
+}
+
+// One CTA per (n, g, run of RPB row blocks of TH output rows). The group's
+// filters are staged once; the halo of row block b+1 streams in by cp.async
+// while block b is computed (two halo buffers), so after the first block
+// the global-load latency is hidden.
 template <int RF, int RW, int KW>
-__global__ void __launch_bounds__(512) gconv_kernel(const GconvArgs a, const int TH, const int TW, const int TF) {
+__global__ void __launch_bounds__(512)
+    gconv_kernel(const GconvArgs a, const int TH, const int TW, const int TF, const int RPB) {
   extern __shared__ __align__(16) float sm[];
   const int C = a.C, KH = a.KH, F = a.F;
   const int Ho = a.H - KH + 1, Wo = a.W - KW + 1;
   const int rows = TH + KH - 1;
   const int WP = TW * RW + KW - 1;
   const int FP = TF * RF;
-  const int n = blockIdx.z, g = blockIdx.y, h0 = blockIdx.x * TH;
+  const int n = blockIdx.z, g = blockIdx.y;
+  const int nblk = (Ho + TH - 1) / TH;
+  const int b0 = blockIdx.x * RPB, b1 = min(nblk, b0 + RPB);
   const int tid = threadIdx.x, T = blockDim.x;
+  const int haloF = C * rows * WP;
 
-  float* In = sm;                      // [C][rows][WP]
-  float* Wt = In + C * rows * WP;      // [C][KH][KW][FP]
-  float* Bs = Wt + C * KH * KW * FP;   // [Mb]
+  float* Wt = sm;                      // [C][KH][KW][FP]
+  float* Bs = Wt + C * KH * KW * FP;   // [Mb] (padded to 4)
+  float* halo = Bs + ((a.Mb + 3) & ~3);  // [2][C][rows][WP]
 
   const float* Ig = a.I + ((int64_t)n * a.G + g) * C * a.H * a.W;
-  for (int e = tid; e < C * rows * WP; e += T) {
-    int w = e % WP, t = e / WP;
-    int r = t % rows, c = t / rows;
-    int h = h0 + r;
-    In[e] = (h < a.H && w < a.W) ? __ldg(Ig + ((int64_t)c * a.H + h) * a.W + w) : 0.0f;
-  }
+  auto loadHalo = [&](int blk, float* dst) {
+    const int h0 = blk * TH;
+    for (int e = tid; e < haloF; e += T) {
+      const int w = e % WP, t = e / WP;
+      const int r = t % rows, c = t / rows;
+      const int h = h0 + r;
+      const bool ok = h < a.H && w < a.W;
+      cpAsync4(dst + e, ok ? Ig + ((int64_t)c * a.H + h) * a.W + w : Ig, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (b0 < b1) loadHalo(b0, halo);
   const float* Wg = a.W1 + (int64_t)g * F * C * KH * KW;
   for (int e = tid; e < C * KH * KW * FP; e += T) {
     int f = e % FP, t = e / FP;  // t = (c*KH + kh)*KW + kw
     Wt[e] = f < F ? __ldg(Wg + (int64_t)f * C * KH * KW + t) : 0.0f;
   }
   for (int e = tid; e < a.Mb; e += T) Bs[e] = __ldg(a.B + e);
-  __syncthreads();
 
   const int wg = tid % TW;
   const int hl = (tid / TW) % TH;
   const int fg = tid / (TW * TH);
-  if (fg >= TF) return;
+  const bool active = fg < TF;
+  float* Og = a.O + ((int64_t)n * a.G + g) * F * Ho * Wo;
 
-  float acc[RF][RW];
+  for (int blk = b0; blk < b1; ++blk) {
+    const float* In = halo + ((blk - b0) & 1) * haloF;
+    if (blk + 1 < b1) {
+      loadHalo(blk + 1, halo + ((blk + 1 - b0) & 1) * haloF);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this block's halo landed (this thread)
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();  // ... for every thread (and the filters are staged)
+    if (active) {
+      float acc[RF][RW];
 #pragma unroll
-  for (int f = 0; f < RF; ++f)
+      for (int f = 0; f < RF; ++f)
 #pragma unroll
-    for (int j = 0; j < RW; ++j) acc[f][j] = 0.0f;
+        for (int j = 0; j < RW; ++j) acc[f][j] = 0.0f;
 
-  for (int c = 0; c < C; ++c) {
-    for (int kh = 0; kh < KH; ++kh) {
-      const float* row = In + (c * rows + hl + kh) * WP + wg * RW;
-      float x[RW + KW - 1];
+      for (int c = 0; c < C; ++c) {
+        for (int kh = 0; kh < KH; ++kh) {
+          const float* row = In + (c * rows + hl + kh) * WP + wg * RW;
+          float x[RW + KW - 1];
 #pragma unroll
-      for (int j = 0; j < RW + KW - 1; ++j) x[j] = row[j];
-      const float* wp = Wt + ((c * KH + kh) * KW) * FP + fg * RF;
+          for (int j = 0; j < RW + KW - 1; ++j) x[j] = row[j];
+          const float* wp = Wt + ((c * KH + kh) * KW) * FP + fg * RF;
 #pragma unroll
-      for (int kw = 0; kw < KW; ++kw) {
-        float wv[RF];
-        if constexpr (RF % 4 == 0) {
+          for (int kw = 0; kw < KW; ++kw) {
+            float wv[RF];
+            if constexpr (RF % 4 == 0) {
 #pragma unroll
-          for (int f = 0; f < RF; f += 4) {
-            float4 v = *reinterpret_cast<const float4*>(wp + kw * FP + f);
-            wv[f] = v.x;
-            wv[f + 1] = v.y;
-            wv[f + 2] = v.z;
-            wv[f + 3] = v.w;
+              for (int f = 0; f < RF; f += 4) {
+                float4 v = *reinterpret_cast<const float4*>(wp + kw * FP + f);
+                wv[f] = v.x;
+                wv[f + 1] = v.y;
+                wv[f + 2] = v.z;
+                wv[f + 3] = v.w;
+              }
+            } else {
+#pragma unroll
+              for (int f = 0; f < RF; ++f) wv[f] = wp[kw * FP + f];
+            }
+#pragma unroll
+            for (int f = 0; f < RF; ++f)
+#pragma unroll
+              for (int j = 0; j < RW; ++j) acc[f][j] = __fmaf_rn(x[j + kw], wv[f], acc[f][j]);
           }
-        } else {
+        }
+      }
+
+      const int h = blk * TH + hl;
+      if (h < Ho) {
+        for (int m = 0; m < a.Mb; ++m) {
+          const float bm = Bs[m];
 #pragma unroll
-          for (int f = 0; f < RF; ++f) wv[f] = wp[kw * FP + f];
+          for (int f = 0; f < RF; ++f)
+#pragma unroll
+            for (int j = 0; j < RW; ++j) acc[f][j] = __fadd_rn(acc[f][j], bm);
         }
 #pragma unroll
-        for (int f = 0; f < RF; ++f)
+        for (int f = 0; f < RF; ++f) {
+          int o = fg * RF + f;
+          if (o >= F) continue;
 #pragma unroll
-          for (int j = 0; j < RW; ++j) acc[f][j] = __fmaf_rn(x[j + kw], wv[f], acc[f][j]);
+          for (int j = 0; j < RW; ++j) {
+            int w = wg * RW + j;
+            if (w < Wo) Og[((int64_t)o * Ho + h) * Wo + w] = acc[f][j];
+          }
+        }
       }
     }
-  }
-
-  const int h = h0 + hl;
-  if (h >= Ho) return;
-  for (int m = 0; m < a.Mb; ++m) {
-    const float bm = Bs[m];
-#pragma unroll
-    for (int f = 0; f < RF; ++f)
-#pragma unroll
-      for (int j = 0; j < RW; ++j) acc[f][j] = __fadd_rn(acc[f][j], bm);
-  }
-  float* Og = a.O + ((int64_t)n * a.G + g) * F * Ho * Wo;
-#pragma unroll
-  for (int f = 0; f < RF; ++f) {
-    int o = fg * RF + f;
-    if (o >= F) continue;
-#pragma unroll
-    for (int j = 0; j < RW; ++j) {
-      int w = wg * RW + j;
-      if (w < Wo) Og[((int64_t)o * Ho + h) * Wo + w] = acc[f][j];
-    }
+    __syncthreads();  // the halo buffer of this block is free for block + 2
   }
 }
 
@@ -129,10 +164,19 @@ cudaError_t launchV(const GconvArgs& a, int th, cudaStream_t s) {
   size_t smem = gconvSmem(a, th, RW);
   smem += (size_t)a.C * a.KH * KW * (TF * RF - a.F) * sizeof(float);  // filter padding
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  // row blocks per CTA: enough CTAs for ~2 waves of 148 SMs, the rest
+  // become a pipelined loop inside the CTA
+  const int nblk = (Ho + th - 1) / th;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t pairs = (int64_t)a.G * a.N;
+  const int want = static_cast<int>(std::max<int64_t>(1, (4 * sms + pairs - 1) / pairs));
+  const int rpb = std::max(1, (nblk + want - 1) / want);
   auto kfn = gconv_kernel<RF, RW, KW>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((Ho + th - 1) / th, a.G, a.N);
-  kfn<<<grid, threads, smem, s>>>(a, th, TW, TF);
+  dim3 grid((nblk + rpb - 1) / rpb, a.G, a.N);
+  kfn<<<grid, threads, smem, s>>>(a, th, TW, TF, rpb);
   return cudaGetLastError();
 }
 
@@ -145,7 +189,9 @@ size_t gconvSmem(const GconvArgs& a, int th, int rw) {
   const int Wo = a.W - a.KW + 1;
   const int TW = (Wo + rw - 1) / rw;
   const int WP = TW * rw + a.KW - 1;
-  return ((size_t)a.C * (th + a.KH - 1) * WP + (size_t)a.C * a.KH * a.KW * a.F + a.Mb) * sizeof(float);
+  // two halo buffers (double-buffered row blocks) + filters + bias
+  return (2 * (size_t)a.C * (th + a.KH - 1) * WP + (size_t)a.C * a.KH * a.KW * a.F + ((a.Mb + 3) & ~3)) *
+         sizeof(float);
 }
 
 int gconvThreads(const GconvArgs& a, int variant, int th) {
