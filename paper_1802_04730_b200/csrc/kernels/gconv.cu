@@ -45,21 +45,47 @@ __global__ void __launch_bounds__(512)
   const int nblk = (Ho + TH - 1) / TH;
   const int b0 = blockIdx.x * RPB, b1 = min(nblk, b0 + RPB);
   const int tid = threadIdx.x, T = blockDim.x;
-  const int haloF = C * rows * WP;
+  const int haloF = C * rows * WP + (C * rows * WP) % 2;  // keep the second buffer 8-byte aligned
 
   float* Wt = sm;                      // [C][KH][KW][FP]
   float* Bs = Wt + C * KH * KW * FP;   // [Mb] (padded to 4)
   float* halo = Bs + ((a.Mb + 3) & ~3);  // [2][C][rows][WP]
 
   const float* Ig = a.I + ((int64_t)n * a.G + g) * C * a.H * a.W;
+  // one halo row (c, r) per warp and pass, lanes along w: 8-byte copies when
+  // the rows allow it (W and WP even: every pair is inside or outside the
+  // image row, and 8-byte aligned on both sides), else 4-byte copies
+  const bool pairs = (a.W % 2 == 0) && (WP % 2 == 0);
+  const int lane = tid & 31, nw = T >> 5, wid = tid >> 5;
   auto loadHalo = [&](int blk, float* dst) {
     const int h0 = blk * TH;
-    for (int e = tid; e < haloF; e += T) {
-      const int w = e % WP, t = e / WP;
-      const int r = t % rows, c = t / rows;
-      const int h = h0 + r;
-      const bool ok = h < a.H && w < a.W;
-      cpAsync4(dst + e, ok ? Ig + ((int64_t)c * a.H + h) * a.W + w : Ig, ok);
+    if (T % 32) {  // partial warps (tiny problems): one element per thread and pass
+      for (int e = tid; e < C * rows * WP; e += T) {
+        const int w = e % WP, t = e / WP, r = t % rows, c = t / rows, h = h0 + r;
+        const bool ok = h < a.H && w < a.W;
+        cpAsync4(dst + e, ok ? Ig + ((int64_t)c * a.H + h) * a.W + w : Ig, ok);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      return;
+    }
+    for (int row = wid; row < C * rows; row += nw) {
+      const int c = row / rows, r = row - c * rows, h = h0 + r;
+      const float* src = Ig + ((int64_t)c * a.H + (h < a.H ? h : 0)) * a.W;
+      float* d = dst + row * WP;
+      if (pairs) {
+        for (int w = 2 * lane; w < WP; w += 64) {
+          const bool ok = h < a.H && w < a.W;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                           static_cast<unsigned>(__cvta_generic_to_shared(d + w))),
+                       "l"(ok ? src + w : Ig), "r"(ok ? 8 : 0)
+                       : "memory");
+        }
+      } else {
+        for (int w = lane; w < WP; w += 32) {
+          const bool ok = h < a.H && w < a.W;
+          cpAsync4(d + w, ok ? src + w : Ig, ok);
+        }
+      }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
