@@ -60,7 +60,8 @@ TC_OPS = [("tmm 128x1024x1024", "3xtf32"), ("tmm 128x1024x1024", "tf32"),
           ("tmm 128x4096x16384", "3xtf32"), ("tmm 128x4096x16384", "tf32"),
           ("C3 128x1024->1000", "3xtf32"), ("C3 128x1024->1000", "tf32"),
           ("tbmm 500,26,72,26", "3xtf32"), ("MLP1 128x1128->128", "3xtf32"),
-          ("2FCRelu 128x1128->128->64", "3xtf32"), ("MLP3 128->64->32->2", "3xtf32")]
+          ("2FCRelu 128x1128->128->64", "3xtf32"), ("MLP3 128->64->32->2", "3xtf32"),
+          ("gconv 32,32,16,16,58x58,3x3", "3xtf32"), ("gconv 32,32,16,16,58x58,3x3", "tf32")]
 INT_PARAMS = {"2LUT": {1, 3}, "1LUT": {1}}
 
 
@@ -656,7 +657,7 @@ def paper_op_table(ee, torch, dev, stream, peaks):
     todo += [(*byl[lab][:1], f"{lab} [{m}]", *byl[lab][1:], m) for lab, m in TC_OPS]
     for name, label, shapes, seeded, math in todo:
         try:
-            big = name in ("2LUT", "gconv") or label.startswith("tmm 128x4096x16384")
+            big = name in ("2LUT", "gconv") or label.startswith(("tmm 128x4096x16384", "gconv"))
             one = OpInstance(ee, torch, name, shapes, seeded, 1, dev, 3, math=math)
             nsets = 1 if big else max(2, int(np.ceil(2 * L2_BYTES / max(1, one.set_bytes()))))
             nsets = min(nsets, 64)
