@@ -90,6 +90,10 @@ extern "C" {
 /* run flags */
 #define TCB_RUN_PROFILE 1  /* time the launch with CUDA events (synchronises) */
 #define TCB_RUN_NOCHECK 2  /* skip the post-launch device error check (graph capture) */
+#define TCB_RUN_ASYNC 4    /* host tensors: return once the H2D copies, the launch and the D2H copies
+                            * are enqueued on `stream`; the caller synchronises the stream before
+                            * reading outputs or reusing inputs (pinned buffers make the copies
+                            * asynchronous). Two async host runs of one handle must share a stream. */
 
 typedef struct tcb_tensor {
   void* data;
@@ -135,7 +139,7 @@ int tcb_compile(tcb_engine* e, const char* name, const tcb_tensor* inputs, int n
                 const tcb_tensor* outputs, int n_outputs, const char* options_json, uint64_t* handle);
 
 /* compile with an explicit arithmetic (TCB_MATH_*). Tensor-core modes exist
- * for tmm, tbmm, C3, MLP1, 2FCRelu, MLP3; other defs fail with
+ * for tmm, tbmm, C3, MLP1, 2FCRelu, MLP3 and gconv; other defs fail with
  * TCB_ERR_MAPPING_INVALID. Their cache entries carry the target suffix
  * " math=<mode>" and never mix with the exact ones. */
 int tcb_compile_ex(tcb_engine* e, const char* name, const tcb_tensor* inputs, int n_inputs,

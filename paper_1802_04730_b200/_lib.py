@@ -11,7 +11,7 @@ LIB_PATH = os.path.join(_HERE, "libtcb.so")
 
 TCB_F32, TCB_I32 = 0, 1
 TCB_DEVICE, TCB_HOST = 0, 1
-TCB_RUN_PROFILE, TCB_RUN_NOCHECK = 1, 2
+TCB_RUN_PROFILE, TCB_RUN_NOCHECK, TCB_RUN_ASYNC = 1, 2, 4
 MATH_MODES = {"ffma": 0, "tf32": 1, "3xtf32": 3}
 
 # ErrorKind order of proj/include/tc/support/diagnostics.h:36-68 (+2 additions)

@@ -300,6 +300,70 @@ int tcb_describe(tcb_engine* e, uint64_t h, char* buf, int len) {
   });
 }
 
+namespace {
+
+// largest host tensor moved by the segment-copy kernel instead of a DMA
+// (TCB_ZEROCOPY_MAX bytes; 0 disables it)
+int64_t zeroCopyMax() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("TCB_ZEROCOPY_MAX");
+    return e ? std::atoll(e) : static_cast<int64_t>(1) << 20;
+  }();
+  return v;
+}
+
+// the device address of a pinned (page-locked, UVA-mapped) host buffer, or
+// null for pageable memory
+const void* mappedHost(const void* p) {
+  if (zeroCopyMax() <= 0) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
+int deviceSms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+}  // namespace
+
+namespace {
+
+// device staging buffers of a handle run on host tensors
+void ensureStaging(Compiled& c) {
+  const auto& params = c.spec.v.def.params;
+  const auto& rets = c.spec.v.def.rets;
+  const int nin = static_cast<int>(params.size()), nout = static_cast<int>(rets.size());
+  if (c.dIn.empty()) {
+    auto inout = sem::inoutReturns(c.spec.v);
+    for (int i = 0; i < nin; ++i) {
+      size_t b = 4;
+      if (!params[i].scalar())
+        for (auto x : c.spec.shapes.at(params[i].name)) b *= static_cast<size_t>(x);
+      void* p = nullptr;
+      cudaOk(cudaMalloc(&p, b), "cudaMalloc");
+      c.dIn.push_back(p);
+      c.inBytes.push_back(b);
+    }
+    for (int i = 0; i < nout; ++i) {
+      size_t b = 4;
+      for (auto x : c.spec.shapes.at(rets[i])) b *= static_cast<size_t>(x);
+      void* p = nullptr;
+      cudaOk(cudaMalloc(&p, b), "cudaMalloc");
+      c.dOut.push_back(p);
+      c.outBytes.push_back(b);
+      c.outInout.push_back(std::find(inout.begin(), inout.end(), rets[i]) != inout.end());
+    }
+  }
+}
+
+}  // namespace
+
 int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_tensor* out, int nout, void* stream,
             int flags, int64_t* duration_ns) {
   return guarded([&] {
@@ -334,43 +398,40 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
     }
     c.lastStream = s;
     std::vector<void*> din(nin), dout(nout);
+    bool profile = (flags & TCB_RUN_PROFILE) != 0;
+    // host tensors: mapped pinned buffers up to zeroCopyMax() move in one
+    // segment-copy launch per direction; the rest (pageable or large) by DMA
+    k::SegCopyArgs up{}, down{};
+    std::vector<const void*> outMapped(nout, nullptr);
     if (host) {
-      if (c.dIn.empty()) {
-        auto inout = sem::inoutReturns(c.spec.v);
-        for (int i = 0; i < nin; ++i) {
-          size_t b = 4;
-          if (!params[i].scalar())
-            for (auto x : c.spec.shapes.at(params[i].name)) b *= static_cast<size_t>(x);
-          void* p = nullptr;
-          cudaOk(cudaMalloc(&p, b), "cudaMalloc");
-          c.dIn.push_back(p);
-          c.inBytes.push_back(b);
+      ensureStaging(c);
+      auto stage = [&](k::SegCopyArgs& a, void* dst, const void* src, const void* mapped, size_t bytes,
+                       cudaMemcpyKind kind) {
+        if (mapped && a.n < k::kMaxSeg && static_cast<int64_t>(bytes) <= zeroCopyMax() && bytes % 4 == 0) {
+          if (kind == cudaMemcpyHostToDevice)
+            k::segCopyAdd(a, dst, mapped, static_cast<int64_t>(bytes));
+          else
+            k::segCopyAdd(a, const_cast<void*>(mapped), src, static_cast<int64_t>(bytes));
+        } else {
+          cudaOk(cudaMemcpyAsync(dst, src, bytes, kind, s), kind == cudaMemcpyHostToDevice ? "H2D" : "D2H");
         }
-        for (int i = 0; i < nout; ++i) {
-          size_t b = 4;
-          for (auto x : c.spec.shapes.at(rets[i])) b *= static_cast<size_t>(x);
-          void* p = nullptr;
-          cudaOk(cudaMalloc(&p, b), "cudaMalloc");
-          c.dOut.push_back(p);
-          c.outBytes.push_back(b);
-          c.outInout.push_back(std::find(inout.begin(), inout.end(), rets[i]) != inout.end());
-        }
-      }
+      };
       for (int i = 0; i < nin; ++i) {
         din[i] = c.dIn[i];
         if (!params[i].scalar())
-          cudaOk(cudaMemcpyAsync(din[i], in[i].data, c.inBytes[i], cudaMemcpyHostToDevice, s), "H2D");
+          stage(up, din[i], in[i].data, mappedHost(in[i].data), c.inBytes[i], cudaMemcpyHostToDevice);
       }
       for (int i = 0; i < nout; ++i) {
         dout[i] = c.dOut[i];
-        if (c.outInout[i]) cudaOk(cudaMemcpyAsync(dout[i], out[i].data, c.outBytes[i], cudaMemcpyHostToDevice, s), "H2D");
+        outMapped[i] = mappedHost(out[i].data);
+        if (c.outInout[i]) stage(up, dout[i], out[i].data, outMapped[i], c.outBytes[i], cudaMemcpyHostToDevice);
       }
+      cudaOk(k::launchSegCopy(up, deviceSms(), s), "host copy");
     } else {
       for (int i = 0; i < nin; ++i) din[i] = in[i].data;
       for (int i = 0; i < nout; ++i) dout[i] = out[i].data;
     }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    bool profile = (flags & TCB_RUN_PROFILE) != 0;
     if (profile) {
       cudaOk(cudaEventCreate(&ev0), "event");
       cudaOk(cudaEventCreate(&ev1), "event");
@@ -379,9 +440,14 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
     ops::launch(c.prob, c.map, din.data(), dout.data(), c.dErr, s);
     if (profile) cudaOk(cudaEventRecord(ev1, s), "record");
     if (host) {
-      for (int i = 0; i < nout; ++i)
-        cudaOk(cudaMemcpyAsync(out[i].data, dout[i], c.outBytes[i], cudaMemcpyDeviceToHost, s), "D2H");
-      cudaOk(cudaStreamSynchronize(s), "sync");
+      for (int i = 0; i < nout; ++i) {
+        if (outMapped[i] && down.n < k::kMaxSeg && static_cast<int64_t>(c.outBytes[i]) <= zeroCopyMax())
+          k::segCopyAdd(down, const_cast<void*>(outMapped[i]), dout[i], static_cast<int64_t>(c.outBytes[i]));
+        else
+          cudaOk(cudaMemcpyAsync(out[i].data, dout[i], c.outBytes[i], cudaMemcpyDeviceToHost, s), "D2H");
+      }
+      cudaOk(k::launchSegCopy(down, deviceSms(), s), "host copy");
+      if (!(flags & TCB_RUN_ASYNC)) cudaOk(cudaStreamSynchronize(s), "sync");
     }
     if (profile) {
       cudaOk(cudaEventSynchronize(ev1), "sync");
@@ -391,7 +457,7 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
       cudaEventDestroy(ev0);
       cudaEventDestroy(ev1);
     }
-    if (c.prob.family == ops::Family::Lut && !(flags & TCB_RUN_NOCHECK)) {
+    if (c.prob.family == ops::Family::Lut && !(flags & (TCB_RUN_NOCHECK | TCB_RUN_ASYNC))) {
       int flag = 0;
       cudaOk(cudaMemcpyAsync(&flag, c.dErr, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
       cudaOk(cudaStreamSynchronize(s), "sync");

@@ -139,6 +139,21 @@ struct ConcatArgs {
 };
 cudaError_t launchConcat(const ConcatArgs& a, cudaStream_t s);
 
+// ------------------------------------------------------ host transfers
+// Up to kMaxSeg copies (4-byte multiples) in one launch; host sides are
+// mapped pinned pointers. Segments whose pointers and size are 16-byte
+// aligned move as int4.
+constexpr int kMaxSeg = 16;
+struct SegCopyArgs {
+  const void* src[kMaxSeg];
+  void* dst[kMaxSeg];
+  int64_t start[kMaxSeg + 1];  // prefix of per-segment units (16 B or 4 B)
+  bool vec16[kMaxSeg];
+  int n;
+};
+void segCopyAdd(SegCopyArgs& a, void* dst, const void* src, int64_t bytes);
+cudaError_t launchSegCopy(const SegCopyArgs& a, int sms, cudaStream_t s);
+
 // ---------------------------------------------------------------- probes
 // fp32 FFMA throughput of the whole device (TFLOP/s, 2 flops per FMA)
 cudaError_t probeFfma(int sms, double* tflops, float* ms);

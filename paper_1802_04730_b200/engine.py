@@ -139,14 +139,19 @@ class ExecutionEngine:
         return json.loads(b.value.decode())
 
     # ---------------------------------------------------------------- run
-    def run(self, handle, inputs, outputs, stream=None, profile=False, check_errors=True):
-        """Runs a compiled handle. Returns the device time in ns when profiling."""
+    def run(self, handle, inputs, outputs, stream=None, profile=False, check_errors=True, sync=True):
+        """Runs a compiled handle. Returns the device time in ns when profiling.
+
+        sync=False with host tensors only enqueues the copies and the launch
+        on `stream` (TCB_RUN_ASYNC); synchronise the stream before reading
+        the outputs, then call check() for LUT index errors."""
         ins, nin = _arr(inputs)
         outs, nout = _arr(outputs)
         if stream is None and torch is not None and any(
                 isinstance(t, torch.Tensor) and t.is_cuda for t in list(inputs) + list(outputs)):
             stream = torch.cuda.current_stream().cuda_stream
-        flags = (_lib.TCB_RUN_PROFILE if profile else 0) | (0 if check_errors else _lib.TCB_RUN_NOCHECK)
+        flags = ((_lib.TCB_RUN_PROFILE if profile else 0) | (0 if check_errors else _lib.TCB_RUN_NOCHECK) |
+                 (0 if sync else _lib.TCB_RUN_ASYNC))
         dur = C.c_int64(0)
         check(lib.tcb_run(self._h, handle, ins, nin, outs, nout, C.c_void_p(stream or 0), flags,
                           C.byref(dur)))
@@ -154,6 +159,12 @@ class ExecutionEngine:
 
     def check(self, handle):
         check(lib.tcb_check(self._h, handle))
+
+    def prepare(self, handle, inputs, outputs) -> "PreparedRun":
+        """Binds tensors to a compiled handle once, like the reference's
+        caller building its DLTensor arrays once (execution_engine.h:93-101);
+        PreparedRun.run() then only crosses the C ABI."""
+        return PreparedRun(self, handle, inputs, outputs)
 
     # --------------------------------------------------------------- tune
     def tune(self, name, inputs, outputs=None, **opts) -> dict:
@@ -339,3 +350,25 @@ def device_info(dev=0):
     b = _lib.buf(1024)
     check(lib.tcb_device_info(dev, b, 1024))
     return b.value.decode()
+
+
+class PreparedRun:
+    """A handle bound to fixed tensors (their descriptors are built once).
+    The tensors are kept alive; writing new values into them between runs is
+    the intended use."""
+
+    def __init__(self, ee, handle, inputs, outputs):
+        self.ee, self.handle = ee, handle
+        self.tensors = (list(inputs), list(outputs))
+        self._ins, self._nin = _arr(inputs)
+        self._outs, self._nout = _arr(outputs)
+        self._cuda = torch is not None and any(isinstance(t, torch.Tensor) and t.is_cuda
+                                               for t in self.tensors[0] + self.tensors[1])
+
+    def run(self, stream=None, sync=True, check_errors=True):
+        """One call; see ExecutionEngine.run for `sync`."""
+        if stream is None and self._cuda:
+            stream = torch.cuda.current_stream().cuda_stream
+        flags = (0 if check_errors else _lib.TCB_RUN_NOCHECK) | (0 if sync else _lib.TCB_RUN_ASYNC)
+        check(lib.tcb_run(self.ee._h, self.handle, self._ins, self._nin, self._outs, self._nout,
+                          C.c_void_p(stream or 0), flags, None))

@@ -228,6 +228,88 @@ def test_host_buffers_equal_device(engine, oracle, golden, name):
         assert_exact(oracle, name + "/host", k, got_h[k], rec["fnv"])
 
 
+def _pinned(a, misalign=False):
+    """A pinned host tensor holding a; misalign: a view 4 bytes into its buffer."""
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if not misalign:
+        return t.pin_memory()
+    buf = torch.empty(t.numel() + 1, dtype=t.dtype).pin_memory()
+    v = buf[1:].view(t.shape)
+    v.copy_(t)
+    return v
+
+
+@pytest.mark.parametrize("misalign", [False, True])
+@pytest.mark.parametrize("name", ["tbmm_small", "mlp3_small", "2fcrelu_small", "2lut_small", "kru_small"])
+def test_pinned_host_buffers(engine, oracle, golden, name, misalign):
+    """Pinned host tensors move by the one-launch segment copy (aligned: int4,
+    misaligned: 4-byte units); sync, async and prepared runs give the
+    golden bits."""
+    case, ins, seeded = case_inputs(oracle, golden, name)
+    d = case["def"]
+    params = [_pinned(ins[n], misalign) for n in PARAM_ORDER[d]]
+    given = [seeded[r].shape if r in seeded else None for r in RETURN_ORDER[d]]
+    shapes = engine.infer_output_tensor_info(d, params, given)
+    outs = [_pinned(seeded[r] if r in seeded else np.zeros(s, np.float32), misalign)
+            for r, s in zip(RETURN_ORDER[d], shapes)]
+    h = engine.compile(d, params, outs)
+    engine.run(h, params, outs)
+    for r, o in zip(RETURN_ORDER[d], outs):
+        assert_exact(oracle, name + "/pinned", r, o.numpy(), case["outputs"][r]["fnv"])
+    if seeded:  # in-out returns accumulate: restore before rerunning
+        return
+    s = torch.cuda.Stream()
+    pr = engine.prepare(h, params, outs)
+    for o in outs:
+        o.zero_()
+    pr.run(stream=s.cuda_stream, sync=False)
+    s.synchronize()
+    engine.check(h)
+    for r, o in zip(RETURN_ORDER[d], outs):
+        assert_exact(oracle, name + "/pinned-async", r, o.numpy(), case["outputs"][r]["fnv"])
+
+
+def test_pinned_host_large_tensor_dma(engine, oracle):
+    """Host tensors above the segment-copy limit (1 MiB) take the DMA path in
+    the same call as small ones."""
+    rng = np.random.default_rng(7)
+    X = rng.uniform(-1, 1, (500, 26, 72)).astype(np.float32)  # 3.7 MB: DMA
+    Y = rng.uniform(-1, 1, (500, 26, 72)).astype(np.float32)
+    Xs, Ys = X[:4], Y[:4]  # small: segment copy
+    for a, b in ((X, Y), (Xs, Ys)):
+        pa, pb = _pinned(a), _pinned(b)
+        z = torch.zeros(a.shape[0], 26, 26).pin_memory()
+        engine.run(engine.compile("tbmm", [pa, pb], [z]), [pa, pb], [z])
+        np.testing.assert_array_equal(z.numpy(), oracle.tbmm(a, b))
+
+
+def test_host_calls_back_to_back(engine, oracle):
+    """Large host calls (DMA) on pageable and pinned buffers, and async
+    prepared calls of one handle queued back to back on one stream, give the
+    exact result (the handle's staging buffers are reused in stream order)."""
+    rng = np.random.default_rng(11)
+    X = rng.uniform(-1, 1, (500, 26, 72)).astype(np.float32)
+    Y = rng.uniform(-1, 1, (500, 26, 72)).astype(np.float32)
+    ref = oracle.tbmm(X, Y)
+    z = np.zeros((500, 26, 26), np.float32)  # pageable numpy
+    h = engine.compile("tbmm", [X, Y], [z])
+    engine.run(h, [X, Y], [z])
+    np.testing.assert_array_equal(z, ref)
+    pa, pb, pz = _pinned(X), _pinned(Y), torch.zeros(500, 26, 26).pin_memory()
+    X2 = rng.uniform(-1, 1, X.shape).astype(np.float32)
+    pa2, pz2 = _pinned(X2), torch.zeros(500, 26, 26).pin_memory()
+    s = torch.cuda.Stream()
+    r1, r2 = engine.prepare(h, [pa, pb], [pz]), engine.prepare(h, [pa2, pb], [pz2])
+    for _ in range(3):
+        pz.zero_()
+        pz2.zero_()
+        r1.run(stream=s.cuda_stream, sync=False)
+        r2.run(stream=s.cuda_stream, sync=False)
+        s.synchronize()
+        np.testing.assert_array_equal(pz.numpy(), ref)
+        np.testing.assert_array_equal(pz2.numpy(), oracle.tbmm(X2, Y))
+
+
 def test_lut_index_out_of_range(engine):
     from paper_1802_04730_b200 import TcError
     lut = to_dev(np.ones((5, 8), np.float32))
