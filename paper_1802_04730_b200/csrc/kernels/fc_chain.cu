@@ -169,7 +169,7 @@ __device__ __forceinline__ float chainSegment(unsigned xa, unsigned wa, int n, f
 
 #ifdef TCB_FC_TRACE
 // diagnostic build only (profiles/fc_trace.cu): per-CTA phase timestamps
-__device__ unsigned long long g_fc_trace[1024][16];
+__device__ unsigned long long g_fc_trace[1024][24];
 #define FC_STAMP(ev)                                                                       \
   do {                                                                                     \
     if (threadIdx.x == 0) g_fc_trace[blockIdx.y * gridDim.x + blockIdx.x][ev] = clock64(); \
@@ -191,13 +191,19 @@ __device__ unsigned long long g_fc_trace[1024][16];
 
 // __grid_constant__: the layer loop indexes a.L[l] / p.*[l] dynamically;
 // without it those reads go through a local-memory copy of the parameters
-__global__ void __launch_bounds__(1024)
+// NL = a.layers: every layer loop unrolls with static indices, so the
+// parameter reads are constant-bank operands the compiler can hoist and
+// overlap. (A runtime layer loop made each layer's reads dependent misses in
+// the cold constant cache; MLP3 6.8 -> 5.3 µs, profiles/fc_trace.cu.)
+template <int NL>
+__global__ void __launch_bounds__(kFcMaxThreads)
     fc_cluster_kernel(const __grid_constant__ FcChainArgs a, const __grid_constant__ FcPlan p) {
   FC_GSTAMP(13);
   FC_STAMP(0);
   extern __shared__ __align__(128) float sm[];
   const int tid = threadIdx.x, T = blockDim.x, R = p.R;
-  const int cn = p.cn, layers = a.layers;
+  const int cn = p.cn;
+  constexpr int layers = NL;
   const int rank = cn > 1 ? static_cast<int>(clusterRank()) : 0;
   const int row0 = blockIdx.y * R;
   const int rows = min(R, a.batch - row0);
@@ -213,10 +219,12 @@ __global__ void __launch_bounds__(1024)
     biasPre[l] = (l < layers && tid < R * p.cols[l] && c0 + c < a.L[l].out) ? __ldg(a.L[l].bias + c0 + c) : 0.0f;
   }
   if (tid == 0) {
+#pragma unroll
     for (int b = 0; b < 2 * layers; ++b) mbarInit(&bars[b], 1);
     // the pushed activations of every later layer: R rows x all columns
     // (armed before any peer can push: see the cluster arrive below)
     if (cn > 1)
+#pragma unroll
       for (int l = 1; l < layers; ++l) mbarExpectTx(&bars[l], (unsigned)(R * a.L[l - 1].out * 4));
     FC_STAMP(1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -239,6 +247,7 @@ __global__ void __launch_bounds__(1024)
     const unsigned rowBytes = (unsigned)a.L[0].kred * 4u;
     if (tid == 0) {
       mbarExpectTx(&bars[0], rowBytes * rows);
+#pragma unroll
       for (int l = 0; l < layers; ++l) {
         const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
         mbarExpectTx(&bars[layers + l], (unsigned)(a.L[l].kred * 4 * nc));
@@ -255,6 +264,7 @@ __global__ void __launch_bounds__(1024)
           if (j++ % nw == warp)
             bulkCopy(sm + p.offAct[0] + r * p.ald[0], a.I + (int64_t)(row0 + r) * a.ldi, rowBytes, &bars[0]);
       }
+#pragma unroll
       for (int l = 0; l < layers; ++l) {
         const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
         if (nc == 0) continue;
@@ -289,7 +299,7 @@ __global__ void __launch_bounds__(1024)
   }
   FC_STAMP(2);
 
-#pragma unroll 1
+#pragma unroll
   for (int l = 0; l < layers; ++l) {
     const FcLayer L = a.L[l];
     const int cols = p.cols[l], c0 = rank * cols;
@@ -313,6 +323,7 @@ __global__ void __launch_bounds__(1024)
         if (q == l) bpre = biasPre[q];  // static register indexing
       float acc = !live ? 0.0f : base == 0 ? bpre : __ldg(L.bias + c0 + c);
       acc = chainSegment(actBase + (unsigned)(r * ald) * 4u, wBase + (unsigned)(c * p.wld[l]) * 4u, L.kred, acc);
+      FC_STAMP(16 + l);  // chain done (thread 0's first pass), before its stores
       if (live) {
         const float v = fmaxf(acc, 0.0f);
         if (r < rows) L.O[(int64_t)(row0 + r) * L.out + c0 + c] = v;
@@ -398,7 +409,17 @@ int fcChainThreads(const FcChainArgs& a, int rows, int cn) {
   // block size that runs every layer in one pass (any multiple of 32 works;
   // smaller blocks take several passes)
   int t = ((need + 31) / 32) * 32;
-  return t > 1024 ? 1024 : (t < 32 ? 32 : t);
+  return t > kFcMaxThreads ? kFcMaxThreads : (t < 32 ? 32 : t);
+}
+
+static void (*fcKernel(int layers))(FcChainArgs, FcPlan) {
+  switch (layers) {
+    case 1: return fc_cluster_kernel<1>;
+    case 2: return fc_cluster_kernel<2>;
+    case 3: return fc_cluster_kernel<3>;
+    case 4: return fc_cluster_kernel<4>;
+    default: return nullptr;
+  }
 }
 
 cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s) {
@@ -406,9 +427,11 @@ cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, c
   FcPlan p;
   size_t smem = planFc(a, rows, cn, p);
   if (smem > 227 * 1024 || cn < 1 || cn > 16 || rows < 1) return cudaErrorInvalidConfiguration;
-  if (threads < 32 || threads > 1024 || threads % 32) return cudaErrorInvalidConfiguration;
-  cudaFuncSetAttribute(fc_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (cn > 8) cudaFuncSetAttribute(fc_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (threads < 32 || threads > kFcMaxThreads || threads % 32) return cudaErrorInvalidConfiguration;
+  void (*kern)(FcChainArgs, FcPlan) = fcKernel(a.layers);
+  if (!kern) return cudaErrorInvalidValue;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cn > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cn, (a.batch + rows - 1) / rows, 1);
   cfg.blockDim = dim3(threads, 1, 1);
@@ -421,7 +444,7 @@ cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, c
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fc_cluster_kernel, a, p);
+  return cudaLaunchKernelEx(&cfg, kern, a, p);
 }
 
 }  // namespace k

@@ -65,6 +65,7 @@ cudaError_t launchTcGemm(const GemmArgs& a, int math, const TcPlan& plan, cudaSt
 // per `rows` batch rows; output features split across the cluster,
 // activations exchanged over DSMEM between layers.
 constexpr int kMaxLayers = 4;
+constexpr int kFcMaxThreads = 256;  // fused chain block size bound (register budget, fc_chain.cu)
 struct FcLayer {
   const float* W;     // [out][ldw]
   const float* bias;  // [out]

@@ -426,7 +426,8 @@ Mapping decode(const Problem& p, const MappingOptions& o, int math) {
       if (m.rows < 1 || m.rows > 32) invalid("fused FC chain rows per cluster must be in [1, 32]");
       if (m.cn < 1 || m.cn > 16) invalid("fused FC chain cluster size must be in [1, 16]");
       m.threads = static_cast<int>(o.threads());
-      if (m.threads < 32 || m.threads % 32) invalid("fused FC chain needs a multiple of 32 threads");
+      if (m.threads < 32 || m.threads % 32 || m.threads > k::kFcMaxThreads)
+        invalid("fused FC chain needs a multiple of 32 threads, at most 256");
       k::FcChainArgs a{};
       a.layers = static_cast<int>(p.fc.layers.size());
       a.batch = p.fc.batch;

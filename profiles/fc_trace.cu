@@ -12,12 +12,13 @@
 using namespace tcb::k;
 
 static void run(const char* label, FcChainArgs a, int rows, int cn, int threads) {
-  static unsigned long long z[1024][16];
+  static unsigned long long z[1024][24];
   {
     FcPlan pl;
     size_t smem = planFc(a, rows, cn, pl);
-    cudaFuncSetAttribute(fc_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cn > 8) cudaFuncSetAttribute(fc_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    auto kern = fcKernel(a.layers);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cn > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cn, (a.batch + rows - 1) / rows, 1);
     cfg.blockDim = dim3(threads, 1, 1);
@@ -30,7 +31,7 @@ static void run(const char* label, FcChainArgs a, int rows, int cn, int threads)
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nc = -1;
-    cudaError_t e = cudaOccupancyMaxActiveClusters(&nc, fc_cluster_kernel, &cfg);
+    cudaError_t e = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
     printf("[%s] smem %zu B, grid %d clusters, max active clusters %d (%s)\n", label, smem,
            (a.batch + rows - 1) / rows, nc, cudaGetErrorString(e));
   }
@@ -46,12 +47,13 @@ static void run(const char* label, FcChainArgs a, int rows, int cn, int threads)
   cudaError_t err = cudaDeviceSynchronize();
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  static unsigned long long tr[1024][16];
+  static unsigned long long tr[1024][24];
   cudaMemcpyFromSymbol(tr, g_fc_trace, sizeof(tr));
   int nblk = cn * ((a.batch + rows - 1) / rows);
   printf("%s: %s  %.2f us  (%d CTAs)\n", label, cudaGetErrorString(err), ms * 1e3, nblk);
-  const char* names[16] = {"start", "bar_init", "copies_issued", "L0_data", "L0_done", "init_fence", "L1_data",
-                           "L1_done", "cta_sync", "L2_data", "L2_done", "cl_arrive", "expects", "-", "-", "end"};
+  const char* names[24] = {"start", "bar_init", "copies_issued", "L0_data", "L0_done", "init_fence", "L1_data",
+                           "L1_done", "cta_sync", "L2_data", "L2_done", "cl_arrive", "expects", "-", "-", "end",
+                           "L0_chain", "L1_chain", "L2_chain", "L3_chain", "-", "-", "-", "-"};
   unsigned long long g0 = ~0ull, g1 = 0;
   for (int b = 0; b < nblk; ++b) {
     if (tr[b][13]) g0 = std::min(g0, tr[b][13]);
@@ -62,7 +64,8 @@ static void run(const char* label, FcChainArgs a, int rows, int cn, int threads)
   std::sort(st.begin(), st.end());
   printf("  globaltimer: first CTA start -> last CTA end %.2f us; CTA start skew median %lld max %lld ns\n",
          (g1 - g0) * 1e-3, st[st.size() / 2], st.back());
-  for (int ev = 1; ev < 13; ++ev) {
+  const int order[] = {1, 5, 8, 11, 12, 2, 3, 16, 4, 6, 17, 7, 9, 18, 10, 19, 15};
+  for (int ev : order) {
     std::vector<long long> d;
     for (int b = 0; b < nblk; ++b)
       if (tr[b][ev] && tr[b][0]) d.push_back((long long)(tr[b][ev] - tr[b][0]));
@@ -86,10 +89,8 @@ int main() {
   f.layers = 2;
   f.L[0] = {alloc(128 * 1128), alloc(128), alloc(128 * 128), 128, 1128, 1128};
   f.L[1] = {alloc(64 * 128), alloc(64), alloc(128 * 64), 64, 128, 128};
-  run("2FCRelu rows=8 cn=8", f, 8, 8, 128);
   FcChainArgs one = f;
   one.layers = 1;
-  run("MLP1 rows=8 cn=8", one, 8, 8, 128);
   FcChainArgs m{};
   m.I = alloc(128 * 128);
   m.ldi = 128;
@@ -98,12 +99,11 @@ int main() {
   m.L[0] = {alloc(64 * 128), alloc(64), alloc(128 * 64), 64, 128, 128};
   m.L[1] = {alloc(32 * 64), alloc(32), alloc(128 * 32), 32, 64, 64};
   m.L[2] = {alloc(2 * 32), alloc(2), alloc(128 * 2), 2, 32, 32};
-  run("MLP3 rows=4 cn=4", m, 4, 4, 64);
-  run("MLP3 rows=8 cn=2", m, 8, 2, 128);
-  run("MLP3 rows=4 cn=1", m, 4, 1, 64);
-  run("2FCRelu rows=8 cn=4", f, 8, 4, 256);
+  // the default plans of the bench step (ops.cc defaultOptions)
   run("2FCRelu rows=4 cn=8", f, 4, 8, 64);
-  run("2FCRelu rows=8 cn=16", f, 8, 16, 64);
-  run("2FCRelu rows=16 cn=8", f, 16, 8, 256);
+  run("MLP1 rows=4 cn=8", one, 4, 8, 64);
+  run("MLP3 rows=2 cn=4", m, 2, 4, 64);
+  run("MLP3 rows=4 cn=4", m, 4, 4, 64);
+  run("MLP3 rows=1 cn=1", m, 1, 1, 64);
   return 0;
 }
