@@ -23,16 +23,6 @@ __device__ __forceinline__ int findSeg(const SegCopyArgs& a, int64_t u) {
   return s;
 }
 
-__device__ __forceinline__ void copyUnit(const SegCopyArgs& a, int s, int64_t j) {
-  if (a.vec16[s]) {
-    const int4* src = static_cast<const int4*>(a.src[s]);
-    int4* dst = static_cast<int4*>(a.dst[s]);
-    dst[j] = src[j];
-  } else {
-    static_cast<int*>(a.dst[s])[j] = static_cast<const int*>(a.src[s])[j];
-  }
-}
-
 __global__ void __launch_bounds__(256) seg_copy_kernel(const __grid_constant__ SegCopyArgs a) {
   const int64_t total = a.start[a.n];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;

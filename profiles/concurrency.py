@@ -75,6 +75,44 @@ def main():
             main_s.wait_stream(sd)
     print(f"forked   tbmm x2    {timeit(capture(tb2)):8.2f} us/replay")
 
+    def pair(i, j):
+        def f(k):
+            for sd in side[:2]:
+                sd.wait_stream(main_s)
+            with torch.cuda.stream(side[0]):
+                ops[i].run(k)
+            with torch.cuda.stream(side[1]):
+                ops[j].run(k)
+            for sd in side[:2]:
+                main_s.wait_stream(sd)
+        return f
+    for i, j in ((0, 1), (0, 2), (1, 2), (1, 0), (2, 0)):
+        print(f"forked   {ops[i].name}+{ops[j].name:8s} {timeit(capture(pair(i, j))):8.2f} us/replay")
+
+    # high-priority side streams for the FC chains (lower number = higher priority)
+    lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+    pside = [torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)]
+
+    def forked_prio(k):
+        for sd in pside:
+            sd.wait_stream(main_s)
+        for o, sd in zip(ops, pside):
+            with torch.cuda.stream(sd):
+                o.run(k)
+        for sd in pside:
+            main_s.wait_stream(sd)
+    print(f"forked   3 ops, FC high priority {timeit(capture(forked_prio)):8.2f} us/replay")
+
+    def forked_rev(k):
+        for sd in side:
+            sd.wait_stream(main_s)
+        for o, sd in list(zip(ops, side))[::-1]:
+            with torch.cuda.stream(sd):
+                o.run(k)
+        for sd in side:
+            main_s.wait_stream(sd)
+    print(f"forked   3 ops, reverse order   {timeit(capture(forked_rev)):8.2f} us/replay")
+
 
 if __name__ == "__main__":
     main()
