@@ -67,6 +67,10 @@ def main():
         print(f"{' || '.join(c):40s} {timeit(graph_of([ops[n] for n in c])):8.2f} us/step", flush=True)
     for n in ("tbmm", "2FCRelu", "MLP3"):
         print(f"{n + ' || ' + n:40s} {timeit(graph_of([ops[n], twin[n]])):8.2f} us/step", flush=True)
+    for c in (["2FCRelu", "tbmm", "MLP3"], ["2FCRelu", "MLP3", "tbmm"], ["MLP3", "tbmm", "2FCRelu"],
+              ["MLP3", "2FCRelu", "tbmm"]):
+        print(f"{' || '.join(c) + ' (launch order)':40s} {timeit(graph_of([ops[n] for n in c])):8.2f} us/step",
+              flush=True)
 
 
 if __name__ == "__main__":

@@ -25,7 +25,25 @@ def wall(fn, n=200, warm=20):
     return (time.perf_counter() - t0) / n * 1e6
 
 
+def gpu_local_cpus(index=0):
+    """CPUs on the GPU's NUMA node (NVML CPU affinity mask), or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        return cpus & os.sched_getaffinity(0) or None
+    except Exception:
+        return None
+
+
 def main():
+    if os.environ.get("E2E_PIN_LOCAL") == "1":
+        c = gpu_local_cpus()
+        print("gpu-local cpus:", sorted(c)[:4], "...", len(c) if c else None, "of", os.cpu_count(), flush=True)
+        if c:
+            os.sched_setaffinity(0, c)
     dev = torch.device("cuda", 0)
     ss = [torch.cuda.Stream() for _ in range(4)]
     for mb in (1.5, 7.5, 8.85, 64):
