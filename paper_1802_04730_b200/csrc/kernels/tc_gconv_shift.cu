@@ -1,0 +1,370 @@
+// tc_gconv_shift.cu — tensor-core (tcgen05, TF32 / 3xTF32) grouped
+// convolution (proj/kernels/gconv.tc:2-7) as an implicit GEMM per group g
+// with NO im2col: each tap is a shifted view of one halo tile.
+//
+//   D[p][f] = sum_{kh,kw,c} X[c][p + kh*W + kw] * W1[g][f][c][kh][kw]
+//   O(n,g,f,h,w) = D[h*W + w] + B(0) + ... + B(Mb-1)   (sequential, gconv.tc:6)
+//
+// Virtual pixels p = h*W + w run over the INPUT row pitch W, so tap (kh, kw)
+// of pixel p is input pixel p + kh*W + kw: a constant shift. An M tile is 128
+// consecutive virtual pixels; its halo is the HP = 128 + (KH-1)*W + (KW-1)
+// input pixels from p0, stored channel-block-major: [C/4][HP][4 channels],
+// 16 bytes per pixel per block. That is exactly a K-major, no-swizzle UMMA
+// operand (8-pixel x 16-byte core matrices: SBO = 128 B to the next 8
+// pixels, LBO = HP*16 B to the next 4 channels) for EVERY tap, starting
+// (kh*W + kw)*16 bytes further in: 9 taps x C/8 K steps read one tile that
+// was written once (vs 9x the bytes for an im2col A; tc_gconv.cu). Outputs
+// at w >= Wo (the row's last KW-1 virtual pixels) are computed and dropped.
+//
+// Roles (512 threads): warp 1 = MMA issuer (whole warp, elect.sync), warp 2 = TMEM
+// allocator, warps 4-7 = epilogue (TMEM lane quarter = warp % 4), warps 8-15
+// = builders: 4-byte cp.async of the tile's input pixels straight into the
+// transposed layout (lanes = 8 pixels x 4 channels: 128 contiguous shared
+// bytes, four 32-byte global segments), two tiles ahead; 3xTF32 then splits
+// each landed tile into hi/lo planes. Accumulators are double-buffered in
+// TMEM so tile t's epilogue overlaps tile t+1's MMAs. Not FFMA-exact:
+// selected by tensor-core math.
+#include <algorithm>
+
+#include "kernels.cuh"
+#include "sm100.cuh"
+
+namespace tcb {
+namespace k {
+
+namespace {
+
+using namespace sm100;
+
+constexpr int kThreadsSh = 512;
+constexpr int kBuildersSh = 256;
+constexpr int kStagesSh = 4;  // halo tiles in flight (ring)
+constexpr int kAheadSh = 2;   // tiles loaded ahead of the one being finalised
+// One accumulator per tile: a tcgen05.mma from shared memory costs ~40 cycles
+// at N = 16 whatever the accumulator dependence (it is bound by reading the
+// 4 KB A operand, profiles/umma_rate.cu), so partial accumulators would only
+// multiply the epilogue's TMEM reads.
+constexpr int kMaxBiasSh = 16;
+// TMEM accumulator ring: the MMA issuer runs up to kTmemBufs tiles ahead of
+// the epilogue, so the commit -> epilogue -> release round trip (~1-3k cycles)
+// is paid once per kTmemBufs tiles, not once per tile
+constexpr int kTmemBufs = 8;
+
+struct ShiftParams {
+  const float* I;
+  float* O;
+  const float* W1;
+  const float* bias;
+  int N, G, C, H, W, F, KH, KW, Mb;
+  int Ho, Wo, tilesPerImg, items;  // items = G * N * tilesPerImg, split evenly over the grid
+  int HP;  // halo pixels per tile (multiple of 8)
+};
+
+__device__ __forceinline__ bool elect() {
+  uint32_t pred;
+  asm volatile("{ .reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p; }" : "=r"(pred));
+  return pred != 0;
+}
+
+__device__ __forceinline__ uint64_t descKI(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>(lbo >> 4) << 16;
+  d |= static_cast<uint64_t>(sbo >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version; layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
+template <int F, bool X3>
+struct ShiftCfg {
+  // 3xTF32 stacks B as [b_hi | b_lo] (N = 2F): a_hi*[b_hi|b_lo] and
+  // a_lo*[b_hi|b_lo] are two MMAs per K step instead of three (an MMA from
+  // shared memory at small N costs its A read, not its N), and the lo*lo
+  // term comes for free; the epilogue adds the two column halves
+  static constexpr int kN = X3 ? 2 * F : F;
+  static constexpr int kTmemCols = kTmemBufs * kN <= 32    ? 32
+                                   : kTmemBufs * kN <= 64  ? 64
+                                   : kTmemBufs * kN <= 128 ? 128
+                                   : kTmemBufs * kN <= 256 ? 256
+                                                           : 512;
+  __host__ __device__ static int stageFloats(int C, int HP) { return C * HP * (X3 ? 2 : 1); }
+  __host__ __device__ static int bBytes(int KH, int KW, int C) { return KH * KW * (C / 8) * 32 * kN; }
+  __host__ __device__ static int smem(const ShiftParams& p) {
+    return 1024 + kStagesSh * stageFloats(p.C, p.HP) * 4 + 2 * bBytes(p.KH, p.KW, p.C) + 1024 +
+           8 * p.KH * p.KW * (p.C / 8) + 4 * p.Mb;
+  }
+};
+
+template <int F, bool X3>
+__global__ void __launch_bounds__(kThreadsSh, 1) tc_gconv_shift_kernel(const ShiftParams p) {
+  using Cfg = ShiftCfg<F, X3>;
+  constexpr int S = kStagesSh;
+  extern __shared__ uint8_t smraw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  const int C = p.C, HP = p.HP, taps = p.KH * p.KW, kcb = C / 8;
+  const int stF = Cfg::stageFloats(C, HP);
+  const int planeF = C * HP;  // hi (or raw fp32) plane of a stage; lo follows (3xTF32)
+  float* stages = reinterpret_cast<float*>(sm);
+  uint8_t* bBank = sm + S * stF * 4;  // [2 banks][hi (+ lo)] of the CTA's first and last group
+  constexpr int NB = Cfg::kN;
+  const int bStride = Cfg::bBytes(p.KH, p.KW, C);
+  uint64_t* full = reinterpret_cast<uint64_t*>(bBank + 2 * bStride);
+  uint64_t* empty = full + S;
+  uint64_t* tFull = empty + S;            // [kTmemBufs]
+  uint64_t* tEmpty = tFull + kTmemBufs;   // [kTmemBufs]
+  uint32_t* tmemSlot = reinterpret_cast<uint32_t*>(tEmpty + kTmemBufs);
+  uint32_t* aOff16 = tmemSlot + 4;              // [K steps] A descriptor start offset (16-byte units)
+  float* sBias = reinterpret_cast<float*>(aOff16 + taps * kcb);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // work items (g, n, tile), g-major, split evenly over the grid: a CTA's
+  // range spans at most two groups (items per CTA <= items per group)
+  const int tilesG = p.N * p.tilesPerImg;
+  const int t0 = static_cast<int>((int64_t)blockIdx.x * p.items / gridDim.x);
+  const int t1 = static_cast<int>((int64_t)(blockIdx.x + 1) * p.items / gridDim.x);
+  const int gFirst = t0 / tilesG;
+  const int HW = p.H * p.W;
+
+  // ---- B: the group's filters per (tap, 8-channel step), K-major no swizzle:
+  // NB-row x 16-byte core matrices (SBO 128 B per 8 rows), channel halves
+  // LBO = 16*NB B; 3xTF32 rows [0, F) = hi, [F, 2F) = lo
+  for (int bank = 0; bank < 2; ++bank) {
+    const int g = min(gFirst + bank, p.G - 1);
+    const float* Wg = p.W1 + (int64_t)g * F * C * taps;
+    uint8_t* bb = bBank + bank * bStride;
+    for (int e = threadIdx.x; e < F * C * taps; e += blockDim.x) {
+      const int f = e / (C * taps), rem = e - f * C * taps, c = rem / taps, tap = rem - c * taps;
+      const float v = __ldg(Wg + e);  // W1[g][f][c][kh][kw]
+      const int ks = tap * kcb + (c >> 3), half = (c >> 2) & 1, el = c & 3;
+      auto at = [&](int r) { return bb + ks * 32 * NB + half * 16 * NB + (r >> 3) * 128 + (r & 7) * 16 + el * 4; };
+      if constexpr (X3) {
+        const float h = toTf32(v);
+        *reinterpret_cast<float*>(at(f)) = h;
+        *reinterpret_cast<float*>(at(F + f)) = toTf32(v - h);
+      } else {
+        *reinterpret_cast<float*>(at(f)) = v;
+      }
+    }
+  }
+  // A start offset of K step ks = (tap, 8-channel block c8): channel block
+  // 2*c8's plane plus the tap's pixel shift
+  for (int ks = threadIdx.x; ks < taps * kcb; ks += blockDim.x) {
+    const int tap = ks / kcb, c8 = ks - tap * kcb, kh = tap / p.KW, kw = tap - kh * p.KW;
+    aOff16[ks] = (c8 * 2 * HP * 16 + (kh * p.W + kw) * 16) >> 4;
+  }
+  for (int e = threadIdx.x; e < p.Mb; e += blockDim.x) sBias[e] = __ldg(p.bias + e);
+  fenceProxyAsyncSmem();  // generic writes of B visible to the tensor core
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbarInit(&full[s], kBuildersSh / 32);  // one arrive per builder warp
+      mbarInit(&empty[s], 1);
+    }
+    for (int b = 0; b < kTmemBufs; ++b) {
+      mbarInit(&tFull[b], 1);
+      mbarInit(&tEmpty[b], 4);  // one arrive per epilogue warp
+    }
+    fenceBarrierInit();
+  }
+  if (warp == 2) tmemAlloc<Cfg::kTmemCols>(tmemSlot);
+  tcFenceBefore();
+  __syncthreads();
+  tcFenceAfter();
+  const uint32_t tmem = *tmemSlot;
+
+  if (warp >= 8) {
+    // ---- builders
+    const int b = threadIdx.x - 256, el = b & 3, qq = b >> 2;  // 64 pixels x 4 channels per pass
+    auto load = [&](int t, int s) {
+      const int g = t / tilesG, tt = t - g * tilesG, n = tt / p.tilesPerImg, p0 = (tt - n * p.tilesPerImg) * 128;
+      const float* In = p.I + ((int64_t)n * p.G + g) * C * HW;
+      const uint32_t base = smem(stages + s * stF);
+      for (int cb = 0; cb < C / 4; ++cb) {
+        const float* src = In + (int64_t)(cb * 4 + el) * HW;
+        for (int q = qq; q < HP; q += 64) {
+          const int px = p0 + q;
+          const bool ok = px < HW;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(base + ((cb * HP + q) * 4 + el) * 4),
+                       "l"(src + (ok ? px : 0)), "r"(ok ? 4 : 0)
+                       : "memory");
+        }
+      }
+    };
+    auto finalise = [&](int lt) {  // tile lt's copies landed (this thread's): split (3x), publish
+      const int s = lt % S;
+      if constexpr (X3) {
+        asm volatile("bar.sync 1, %0;" ::"n"(kBuildersSh) : "memory");  // every builder's copies landed
+        float4* hi = reinterpret_cast<float4*>(stages + s * stF);
+        float4* lo = hi + planeF / 4;
+        for (int e = b; e < planeF / 4; e += kBuildersSh) {
+          const float4 x = hi[e];
+          float4 h, l;
+          h.x = toTf32(x.x); h.y = toTf32(x.y); h.z = toTf32(x.z); h.w = toTf32(x.w);
+          l.x = toTf32(x.x - h.x); l.y = toTf32(x.y - h.y); l.z = toTf32(x.z - h.z); l.w = toTf32(x.w - h.w);
+          hi[e] = h;
+          lo[e] = l;
+        }
+      }
+      fenceProxyAsyncSmem();  // this lane's landed copies -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) mbarArrive(&full[s]);  // (256 single-thread arrives per tile serialise)
+    };
+    const int nt = t1 - t0;
+    for (int lt = 0; lt < nt + kAheadSh; ++lt) {
+      if (lt < nt) {
+        const int s = lt % S;
+        if (lt >= S) mbarWait(&empty[s], ((lt / S) - 1) & 1, 1);  // MMAs of tile lt - S done
+        load(t0 + lt, s);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count uniform)
+      if (lt >= kAheadSh) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(kAheadSh) : "memory");
+        finalise(lt - kAheadSh);
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issue: the whole warp runs the loop (operands stay warp-uniform);
+    // elect.sync picks the issuing lane. Descriptors are per-tile bases plus
+    // a per-K-step start offset (the start field is the low 14 bits: adding
+    // a 16-byte-unit offset to a valid address cannot carry out of it).
+    constexpr uint32_t idesc = idescTf32(128, NB);  // both operands K-major
+    const uint32_t lboA = HP * 16, lboB = 16 * NB;
+    const int nks = taps * kcb;
+    for (int lt = 0; lt < t1 - t0; ++lt) {
+      const int s = lt % S, buf = lt % kTmemBufs, bank = (t0 + lt) / tilesG - gFirst;
+      if (lt >= kTmemBufs) mbarWait(&tEmpty[buf], ((lt / kTmemBufs) - 1) & 1, 2);
+      mbarWait(&full[s], (lt / S) & 1, 3);
+      tcFenceAfter();
+      const uint32_t aHi = smem(stages + s * stF);
+      const uint64_t ah0 = descKI(aHi, lboA, 128), al0 = descKI(aHi + planeF * 4, lboA, 128);
+      const uint64_t b0 = descKI(smem(bBank + bank * bStride), lboB, 128);
+      const uint32_t d = tmem + buf * NB;
+#pragma unroll 2
+      for (int ks = 0; ks < nks; ++ks) {
+        const uint64_t ao = aOff16[ks], bd = b0 + static_cast<uint64_t>(ks * 2 * NB);  // 32*NB bytes per step
+        if (elect()) {
+          mmaTf32(d, ah0 + ao, bd, idesc, ks > 0);
+          if constexpr (X3) mmaTf32(d, al0 + ao, bd, idesc, 1);
+        }
+      }
+      if (elect()) {
+        mmaCommit(&empty[s]);
+        mmaCommit(&tFull[buf]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ---- epilogue: TMEM -> registers -> partial sums in fixed order -> bias chain -> stores
+    const int q = warp - 4, pix = q * 32 + lane;
+    float bR[kMaxBiasSh];
+#pragma unroll
+    for (int m = 0; m < kMaxBiasSh; ++m) bR[m] = m < p.Mb ? sBias[m] : 0.0f;
+    for (int lt = 0; lt < t1 - t0; ++lt) {
+      const int t = t0 + lt, buf = lt % kTmemBufs;
+      mbarWait(&tFull[buf], (lt / kTmemBufs) & 1, 4);
+      __syncwarp();
+      tcFenceAfter();
+      float v[NB];
+      const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16) + buf * NB;
+#pragma unroll
+      for (int c = 0; c < NB; c += 16) tmemLoad16(trow + c, v + c);
+      tmemLoadWait();
+      if constexpr (X3) {
+#pragma unroll
+        for (int f = 0; f < F; ++f) v[f] += v[F + f];  // (hi*hi + lo*hi) + (hi*lo + lo*lo)
+      }
+      tcFenceBefore();
+      __syncwarp();
+      if (lane == 0) mbarArrive(&tEmpty[buf]);
+      const int g = t / tilesG, tt = t - g * tilesG, n = tt / p.tilesPerImg;
+      const int vp = (tt - n * p.tilesPerImg) * 128 + pix;
+      const int h = vp / p.W, w = vp - h * p.W;
+      if (w < p.Wo && h < p.Ho) {
+        float* o = p.O + (((int64_t)n * p.G + g) * F) * p.Ho * p.Wo + (int64_t)h * p.Wo + w;
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          float x = v[f];
+#pragma unroll
+          for (int m = 0; m < kMaxBiasSh; ++m)
+            if (m < p.Mb) x = __fadd_rn(x, bR[m]);  // B(0), B(1), ... in order (gconv.tc:6)
+          for (int m = kMaxBiasSh; m < p.Mb; ++m) x = __fadd_rn(x, sBias[m]);
+          o[(int64_t)f * p.Ho * p.Wo] = x;
+        }
+      }
+    }
+  }
+  tcFenceBefore();
+  __syncthreads();
+  if (warp == 2) {
+    tcFenceAfter();
+    tmemFree<Cfg::kTmemCols>(tmem);
+  }
+}
+
+template <int F, bool X3>
+cudaError_t launchShift(const ShiftParams& p, cudaStream_t s) {
+  using Cfg = ShiftCfg<F, X3>;
+  auto kern = tc_gconv_shift_kernel<F, X3>;
+  const int smemBytes = Cfg::smem(p);
+  if (smemBytes > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smemBytes);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // one CTA per SM (one wave); a CTA's items must not span more than 2 groups
+  const int tilesG = p.N * p.tilesPerImg;
+  const int grid = std::max(std::min(sms, p.items), (p.items + tilesG - 1) / tilesG);
+  kern<<<grid, kThreadsSh, smemBytes, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool tcGconvShiftSupported(const GconvArgs& a, const char** why) {
+  auto no = [&](const char* w) {
+    if (why) *why = w;
+    return false;
+  };
+  if (a.C % 8) return no("tensor-core gconv needs input channels per group that are a multiple of 8");
+  if (a.F != 16 && a.F != 32 && a.F != 64) return no("tensor-core gconv needs 16, 32 or 64 filters per group");
+  const int HP = ((128 + (a.KH - 1) * a.W + (a.KW - 1)) + 7) / 8 * 8;
+  const bool x3 = true;  // size for the larger (3xTF32) footprint
+  const int64_t bytes = 1024 + (int64_t)kStagesSh * a.C * HP * 4 * (x3 ? 2 : 1) +
+                        (int64_t)a.KH * a.KW * (a.C / 8) * 32 * (2 * a.F) * 2 + 1024 + 8 * a.KH * a.KW * (a.C / 8) +
+                        4 * a.Mb;
+  if (bytes > 227 * 1024) return no("tensor-core gconv (shifted halo): the halo ring exceeds shared memory");
+  return true;
+}
+
+cudaError_t launchTcGconvShift(const GconvArgs& a, int math, cudaStream_t s) {
+  if (!tcGconvShiftSupported(a, nullptr)) return cudaErrorInvalidValue;
+  ShiftParams p{};
+  p.I = a.I;
+  p.O = a.O;
+  p.W1 = a.W1;
+  p.bias = a.B;
+  p.N = a.N;
+  p.G = a.G;
+  p.C = a.C;
+  p.H = a.H;
+  p.W = a.W;
+  p.F = a.F;
+  p.KH = a.KH;
+  p.KW = a.KW;
+  p.Mb = a.Mb;
+  p.Ho = a.H - a.KH + 1;
+  p.Wo = a.W - a.KW + 1;
+  p.tilesPerImg = (p.Ho * p.W + 127) / 128;
+  p.HP = ((128 + (a.KH - 1) * a.W + (a.KW - 1)) + 7) / 8 * 8;
+  p.items = a.G * a.N * p.tilesPerImg;
+  const bool x3 = math == kMath3xTf32;
+  switch (a.F) {
+    case 16: return x3 ? launchShift<16, true>(p, s) : launchShift<16, false>(p, s);
+    case 32: return x3 ? launchShift<32, true>(p, s) : launchShift<32, false>(p, s);
+    case 64: return x3 ? launchShift<64, true>(p, s) : launchShift<64, false>(p, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace k
+}  // namespace tcb

@@ -74,11 +74,17 @@ void decodeTc(const Problem& p, const MappingOptions& o, Mapping& m) {
     a.F = p.gconv.F;
     a.KH = p.gconv.KH;
     a.KW = p.gconv.KW;
+    a.Mb = p.gconv.Mb;
     const char* why = nullptr;
+    // tile_sizes[2]: 2 = NHWC staging, 3 = shifted halo, else on-chip im2col
+    const int sel = o.tileSizes.size() > 2 ? static_cast<int>(o.tileSizes[2]) : 0;
+    if (sel == 3) {
+      if (!k::tcGconvShiftSupported(a, &why)) invalid(why);
+      m.gconvVariant = 2;
+      return;
+    }
     if (!k::tcGconvSupported(a, &why)) invalid(why);
-    // tile_sizes[2] == 2 selects the NHWC-staging variant; otherwise the
-    // on-chip im2col kernel (the faster of the two on B200, profiles/README.md)
-    m.gconvVariant = (o.tileSizes.size() > 2 && o.tileSizes[2] == 2) ? 0 : 1;
+    m.gconvVariant = sel == 2 ? 0 : 1;
     return;
   }
   if (p.family != Family::Gemm && p.family != Family::FcChain)
@@ -221,7 +227,9 @@ std::string Mapping::describe() const {
   if (math != k::kMathFfma) {
     os << "tcgen05 " << mathName(math);
     if (family == Family::Gconv)
-      return os.str() + (gconvVariant == 1 ? " implicit-GEMM (on-chip im2col)" : " implicit-GEMM (NHWC staging)");
+      return os.str() + (gconvVariant == 1   ? " implicit-GEMM (on-chip im2col)"
+                         : gconvVariant == 2 ? " implicit-GEMM (shifted halo)"
+                                             : " implicit-GEMM (NHWC staging)");
     if (tcAuto) os << " planned";
     else os << " bn=" << tc.bn << " splits=" << tc.splits;
     if (family == Family::FcChain) os << " per-layer";
@@ -776,9 +784,14 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
       a.Mb = d.Mb;
       if (m.math != k::kMathFfma) {
         const char* why = nullptr;
-        if (!k::tcGconvSupported(a, &why)) fail(ErrorKind::MappingInvalid, why);
-        check(m.gconvVariant == 1 ? k::launchTcGconv(a, m.math, s) : k::launchTcGconvTma(a, m.math, s),
-              "tensor-core gconv");
+        if (m.gconvVariant == 2) {
+          if (!k::tcGconvShiftSupported(a, &why)) fail(ErrorKind::MappingInvalid, why);
+          check(k::launchTcGconvShift(a, m.math, s), "tensor-core gconv");
+        } else {
+          if (!k::tcGconvSupported(a, &why)) fail(ErrorKind::MappingInvalid, why);
+          check(m.gconvVariant == 1 ? k::launchTcGconv(a, m.math, s) : k::launchTcGconvTma(a, m.math, s),
+                "tensor-core gconv");
+        }
       } else {
         check(k::launchGconv(a, m.gconvVariant, m.th, s), "gconv");
       }

@@ -1,0 +1,115 @@
+// Diagnostic: tcgen05.mma kind::tf32 rate, M=128, K=8 per instruction, for
+// N = 16/64/256, issued by one thread into 1 or 4 accumulators, operands in
+// shared memory with K-major no-swizzle (small LBO vs a 4 KB LBO) or SW128.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1802_04730_b200/csrc/kernels profiles/umma_rate.cu -o /tmp/ur && /tmp/ur
+#include <cstdio>
+#include "sm100.cuh"
+using namespace tcb::k::sm100;
+
+__device__ __forceinline__ uint64_t dKI(uint32_t s, uint32_t lbo, uint32_t sbo) {
+  return ((uint64_t)((s & 0x3FFFF) >> 4)) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+
+template <int N>
+__global__ void __launch_bounds__(128, 1) rate(int iters, int nacc, int layout, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  fenceProxyAsyncSmem();
+  if (threadIdx.x == 0) {
+    mbarInit(&bar, 1);
+    fenceBarrierInit();
+  }
+  if (threadIdx.x < 32) tmemAlloc<512>(&slot);
+  tcFenceBefore();
+  __syncthreads();
+  tcFenceAfter();
+  const uint32_t tmem = slot;
+  if (layout == 3 && threadIdx.x < 32) {  // whole warp, elect.sync picks the issuing lane
+    const uint32_t a = smem(sm), b = smem(sm + 64 * 1024);
+    const uint64_t ad0 = dKI(a, 128, 256), bd0 = dKI(b, 128, 256);
+    constexpr uint32_t id = idescTf32(128, N);
+    long long t0 = clock64();
+    for (int i = 0; i < iters; i += 4) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t pred;
+        asm volatile("{ .reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p; }" : "=r"(pred));
+        // per-MMA operands vary (as in a real K loop): descriptor start + 32 B per step, accumulator j
+        const uint64_t ad = ad0 + (uint64_t)(((i + j) & 7) * 2), bd = bd0 + (uint64_t)(((i + j) & 7) * 2);
+        if (pred) mmaTf32(tmem + (nacc > 1 ? j * N : 0), ad, bd, id, 1);
+      }
+    }
+    if (threadIdx.x == 0) mmaCommit(&bar);
+    __syncwarp();
+    long long t1 = clock64();
+    if (threadIdx.x == 0) {
+      unsigned done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(smem(&bar)) : "memory");
+      long long t2 = clock64();
+      if (blockIdx.x == 0) { out[0] = t1 - t0; out[1] = t2 - t0; }
+    }
+  } else if (layout != 3 && threadIdx.x == 0) {
+    const uint32_t a = smem(sm), b = smem(sm + 64 * 1024);
+    uint64_t ad, bd;
+    if (layout == 0) { ad = dKI(a, 128, 256); bd = dKI(b, 128, 256); }
+    else if (layout == 1) { ad = dKI(a, 4096, 128); bd = dKI(b, 16 * N, 128); }
+    else { ad = descSw128(a); bd = descSw128(b); }
+    constexpr uint32_t id = idescTf32(128, N);
+    long long t0 = clock64();
+    if (nacc == 0) {  // loop-invariant operands: same accumulator, descriptors, accumulate flag
+      for (int i = 0; i < iters; ++i) mmaTf32(tmem, ad, bd, id, 1);
+    } else if (nacc < 0) {  // 4 accumulators, unrolled: every operand a loop invariant
+      for (int i = 0; i < iters; i += 4) {
+        mmaTf32(tmem, ad, bd, id, 1);
+        mmaTf32(tmem + N, ad, bd, id, 1);
+        mmaTf32(tmem + 2 * N, ad, bd, id, 1);
+        mmaTf32(tmem + 3 * N, ad, bd, id, 1);
+      }
+    } else {
+      for (int i = 0; i < iters; ++i) mmaTf32(tmem + (i % nacc) * N, ad, bd, id, i >= nacc);
+    }
+    mmaCommit(&bar);
+    long long t1 = clock64();
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(smem(&bar)) : "memory");
+    long long t2 = clock64();
+    if (blockIdx.x == 0) { out[0] = t1 - t0; out[1] = t2 - t0; }
+  }
+  tcFenceBefore();
+  __syncthreads();
+  if (threadIdx.x < 32) { tcFenceAfter(); tmemFree<512>(tmem); }
+}
+
+template <int N>
+void runN(long long* d) {
+  cudaFuncSetAttribute(rate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  for (int layout : {0, 2, 3})
+    for (int nacc : {1, 4, 0, -4}) {
+      if (layout == 3 && nacc < 1) continue;
+      if (nacc * N > 512 || -nacc * N > 512) continue;
+      const int iters = 2048;
+      rate<N><<<148, 128, 100 * 1024>>>(iters, nacc, layout, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      long long h[2];
+      cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+      printf("N=%3d layout=%s acc=%d: issue %.1f, complete %.1f cycles/MMA (%.0f MAC/cycle) %s\n", N,
+             layout == 0 ? "KI lbo128" : layout == 1 ? "KI lbo4K " : layout == 2 ? "SW128    " : "warp+elect", nacc, (double)h[0] / iters,
+             (double)h[1] / iters, 128.0 * N * 8 * iters / h[1], cudaGetErrorString(e));
+    }
+}
+
+int main() {
+  long long* d;
+  cudaMalloc(&d, 64);
+  runN<16>(d);
+  runN<64>(d);
+  runN<256>(d);
+  return 0;
+}

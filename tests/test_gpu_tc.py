@@ -184,36 +184,43 @@ GCONV_CASES = [  # (N, G, C, H, W, F, KH, KW, Mb)
 ]
 
 
-@pytest.mark.parametrize("variant", ["nhwc", "im2col"])
+@pytest.mark.parametrize("variant", ["nhwc", "im2col", "shift"])
 @pytest.mark.parametrize("math", ["3xtf32", "tf32"])
 @pytest.mark.parametrize("case", GCONV_CASES)
 def test_gconv_tc(env, case, math, variant):
-    """variant: the on-chip im2col kernel (default) or the NHWC-staging
-    kernel (tile_sizes[2] == 2)."""
+    """variant: the on-chip im2col kernel, the NHWC-staging kernel
+    (tile_sizes[2] == 2) or the shifted-halo kernel (tile_sizes[2] == 3)."""
     from paper_1802_04730_b200 import options_baseline
     ee, orc = env
     N, G, C, H, W, F, KH, KW, Mb = case
     rng = orc.rng(31 + H + F)
     I, W1, Bv = rng.f32((N, G, C, H, W)), rng.f32((G, F, C, KH, KW)), rng.f32((Mb,))
     ref = orc.gconv(I, W1, Bv)
-    opts = None
-    if variant == "nhwc":
-        opts = json.loads(options_baseline(0))
-        opts.update({"tile_sizes": [128, F, 2], "thread_shape": [512, 1, 1]})
+    opts = json.loads(options_baseline(0))
+    opts.update({"tile_sizes": [128, F, {"nhwc": 2, "im2col": 1, "shift": 3}[variant]],
+                 "thread_shape": [512, 1, 1]})
     (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros(ref.shape, np.float32)], math, opts)
-    assert "tcgen05" in desc["kernel"] and ("im2col" in desc["kernel"]) == (variant == "im2col")
+    assert "tcgen05" in desc["kernel"]
+    assert {"nhwc": "NHWC", "im2col": "im2col", "shift": "shifted halo"}[variant] in desc["kernel"]
     K = C * KH * KW
     err = max_rel(ref, got)
     record(f"gconv {case} {variant}", math, K, err, None, None)
     assert err <= tol(math, K), f"gconv {case} {math}: maxRel {err:.3g} > {tol(math, K):.3g}"
 
 
-def test_gconv_tc_paper_shape_sampled(env):
-    """tcgen05 gconv at the BASELINE shape, 200k sampled points vs the oracle."""
+@pytest.mark.parametrize("variant", [None, 3])
+def test_gconv_tc_paper_shape_sampled(env, variant):
+    """tcgen05 gconv at the BASELINE shape, 200k sampled points vs the oracle
+    (default plan, and the shifted-halo kernel)."""
+    from paper_1802_04730_b200 import options_baseline
     ee, orc = env
     rng = orc.rng(11)
     I, W1, Bv = rng.f32((32, 32, 16, 58, 58)), rng.f32((32, 16, 16, 3, 3)), rng.f32((16,))
-    (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros((32, 32, 16, 56, 56), np.float32)], "3xtf32")
+    opts = None
+    if variant is not None:
+        opts = json.loads(options_baseline(0))
+        opts.update({"tile_sizes": [128, 16, variant], "thread_shape": [512, 1, 1]})
+    (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros((32, 32, 16, 56, 56), np.float32)], "3xtf32", opts)
     idx = np.random.default_rng(0).integers(0, got.size, 200_000)
     ref = orc.gconv_points(I, W1, Bv, idx)
     err = max_rel(ref, got.reshape(-1)[idx])
