@@ -208,6 +208,27 @@ def test_gconv_tc(env, case, math, variant):
     assert err <= tol(math, K), f"gconv {case} {math}: maxRel {err:.3g} > {tol(math, K):.3g}"
 
 
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("case", [(1, 2, 8, 11, 13, 16, 3, 3, 2), (2, 1, 16, 9, 7, 32, 2, 2, 1)])
+def test_gconv_tc_shift_odd_planes(env, case, math):
+    """Shifted-halo kernel on planes with H*W % 4 != 0 (its 4-byte cp.async
+    builders; the 4x4 vector builders need whole 16-byte pixel quads)."""
+    from paper_1802_04730_b200 import options_baseline
+    ee, orc = env
+    N, G, C, H, W, F, KH, KW, Mb = case
+    rng = orc.rng(7 + H * W)
+    I, W1, Bv = rng.f32((N, G, C, H, W)), rng.f32((G, F, C, KH, KW)), rng.f32((Mb,))
+    ref = orc.gconv(I, W1, Bv)
+    opts = json.loads(options_baseline(0))
+    opts.update({"tile_sizes": [128, F, 3], "thread_shape": [512, 1, 1]})
+    (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros(ref.shape, np.float32)], math, opts)
+    assert "shifted halo" in desc["kernel"]
+    K = C * KH * KW
+    err = max_rel(ref, got)
+    record(f"gconv {case} shift-odd", math, K, err, None, None)
+    assert err <= tol(math, K), f"gconv {case} {math}: maxRel {err:.3g} > {tol(math, K):.3g}"
+
+
 @pytest.mark.parametrize("variant", [None, 3])
 def test_gconv_tc_paper_shape_sampled(env, variant):
     """tcgen05 gconv at the BASELINE shape, 200k sampled points vs the oracle
