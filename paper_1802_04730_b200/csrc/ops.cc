@@ -499,8 +499,20 @@ Mapping decode(const Problem& p, const MappingOptions& o, int math) {
 MappingOptions defaultOptions(const Problem& p, int math) {
   MappingOptions o;
   if (math != k::kMathFfma && p.family == Family::Gconv) {
-    o.tileSizes = {128, static_cast<int64_t>(p.gconv.F), 1};  // 128 pixels x F filters; 1 = on-chip im2col
-    o.threadShape = {{384, 1, 1}};
+    // 128 pixels x F filters; variant 3 = shifted halo (the fastest at the
+    // paper shape, profiles/experiments/r01_gconv_shift_tuning.txt), else 1 =
+    // on-chip im2col where the halo ring does not fit
+    k::GconvArgs a{};
+    a.C = p.gconv.C;
+    a.H = p.gconv.H;
+    a.W = p.gconv.W;
+    a.F = p.gconv.F;
+    a.KH = p.gconv.KH;
+    a.KW = p.gconv.KW;
+    a.Mb = p.gconv.Mb;
+    const int variant = k::tcGconvShiftSupported(a, nullptr) ? 3 : 1;
+    o.tileSizes = {128, static_cast<int64_t>(p.gconv.F), variant};
+    o.threadShape = {{512, 1, 1}};
     o.useShared = true;
     return o;
   }
@@ -628,7 +640,7 @@ GenePools genePools(const Problem& p, int math) {
     if (p.family == Family::Gconv) {
       g.tile0 = {128};
       g.tile1 = {static_cast<int64_t>(p.gconv.F)};
-      g.tile2 = {1, 2};  // on-chip im2col | NHWC staging
+      g.tile2 = {1, 2, 3};  // on-chip im2col | NHWC staging | shifted halo
       g.bz = {1};
     } else {
       g.tile0 = {128};
