@@ -198,6 +198,8 @@ def time_device(torch, fn, iters, stream):
     for i in range(iters):
         fn(i)
     e.record(stream)
+    while not e.query():  # wait without holding the GIL: the clock sampler thread keeps polling
+        time.sleep(0.0002)
     e.synchronize()
     return s.elapsed_time(e) * 1e-3  # seconds
 
