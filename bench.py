@@ -391,7 +391,7 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     # the step's three operators are independent: inside the graph they fork
     # onto their own streams and join back (concurrent kernels share the SMs)
-    side = [torch.cuda.Stream(device=dev) for _ in ops[1:]]
+    side = [torch.cuda.Stream(device=dev) for _ in ops]
 
     with torch.cuda.stream(stream):
         def step(i):
@@ -399,10 +399,12 @@ def main():
                 for o in ops:
                     o.run(i)
                 return
+            # every operator on its own side stream; the main stream only
+            # forks and joins (profiles/r01_concurrency.txt: ~2 us/step better
+            # than running the first operator on the joining stream)
             for sd in side:
                 sd.wait_stream(stream)
-            ops[0].run(i)
-            for o, sd in zip(ops[1:], side):
+            for o, sd in zip(ops, side):
                 with torch.cuda.stream(sd):
                     o.run(i)
             for sd in side:
@@ -522,7 +524,9 @@ def main():
             for st in e2e_streams:
                 st.synchronize()
 
-        for i in range(args.warmup):
+        # untimed warm-up: the first ~150 host calls run slow (pinned-page and
+        # IOMMU mappings warming up: blocks of 50 measured 474, 341, 270, 234, 232 us)
+        for i in range(max(args.warmup, 200)):
             e2e_step(i)
         # host wall clock (each step ends with its outputs on the host), in 5
         # blocks of kb steps; the median block is reported (one-off host

@@ -13,7 +13,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_1802_04730_b200 import ExecutionEngine  # noqa: E402
 
-NSTEP = 8
+NSTEP = int(os.environ.get("NSTEP", "8"))
 
 
 def main():
@@ -67,6 +67,31 @@ def main():
         print(f"{' || '.join(c):40s} {timeit(graph_of([ops[n] for n in c])):8.2f} us/step", flush=True)
     for n in ("tbmm", "2FCRelu", "MLP3"):
         print(f"{n + ' || ' + n:40s} {timeit(graph_of([ops[n], twin[n]])):8.2f} us/step", flush=True)
+    def staged(first, then):  # fork `first` onto side streams, join, then `then` serially
+        def body():
+            for k in range(NSTEP):
+                for sd in side[:len(first)]:
+                    sd.wait_stream(main_s)
+                for o, sd in zip(first, side):
+                    with torch.cuda.stream(sd):
+                        o.run(k)
+                for sd in side[:len(first)]:
+                    main_s.wait_stream(sd)
+                for o in then:
+                    o.run(k)
+        with torch.cuda.stream(main_s):
+            body()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=main_s):
+                body()
+        return g
+    print(f"{'(tbmm || MLP3) -> 2FCRelu':40s} {timeit(staged([ops['tbmm'], ops['MLP3']], [ops['2FCRelu']])):8.2f} us/step",
+          flush=True)
+    print(f"{'2FCRelu -> (tbmm || MLP3)':40s} {timeit(staged([ops['2FCRelu']], [])) :8.2f} (2FCRelu alone, staged form)",
+          flush=True)
+    print(f"{'serial tbmm, MLP3, 2FCRelu':40s} {timeit(staged([], [ops['tbmm'], ops['MLP3'], ops['2FCRelu']])):8.2f} us/step",
+          flush=True)
     for c in (["2FCRelu", "tbmm", "MLP3"], ["2FCRelu", "MLP3", "tbmm"], ["MLP3", "tbmm", "2FCRelu"],
               ["MLP3", "2FCRelu", "tbmm"]):
         print(f"{' || '.join(c) + ' (launch order)':40s} {timeit(graph_of([ops[n] for n in c])):8.2f} us/step",
