@@ -61,7 +61,8 @@ TC_OPS = [("tmm 128x1024x1024", "3xtf32"), ("tmm 128x1024x1024", "tf32"),
           ("C3 128x1024->1000", "3xtf32"), ("C3 128x1024->1000", "tf32"),
           ("tbmm 500,26,72,26", "3xtf32"), ("MLP1 128x1128->128", "3xtf32"),
           ("2FCRelu 128x1128->128->64", "3xtf32"), ("MLP3 128->64->32->2", "3xtf32"),
-          ("gconv 32,32,16,16,58x58,3x3", "3xtf32"), ("gconv 32,32,16,16,58x58,3x3", "tf32")]
+          ("gconv 32,32,16,16,58x58,3x3", "3xtf32"), ("gconv 32,32,16,16,58x58,3x3", "tf32"),
+          ("3KRU M=256 16^3->32^3", "3xtf32"), ("3KRU M=256 16^3->32^3", "tf32")]
 INT_PARAMS = {"2LUT": {1, 3}, "1LUT": {1}}
 
 

@@ -92,6 +92,9 @@ struct KruArgs {
 };
 cudaError_t launchKru3(const KruArgs& a, int dchunk, int threads, cudaStream_t s);
 size_t kru3Smem(const KruArgs& a, int dchunk);
+// tensor-core 3-KRU (tc_kru.cu): N0 = N1 = N2 = 16, D0 = D1 in {16, 32}, D2 % 16 == 0
+bool tcKru3Supported(const KruArgs& a, const char** why);
+cudaError_t launchTcKru3(const KruArgs& a, int math, cudaStream_t s);
 
 // ---------------------------------------------------------------- gconv
 struct GconvArgs {

@@ -87,9 +87,21 @@ void decodeTc(const Problem& p, const MappingOptions& o, Mapping& m) {
     m.gconvVariant = sel == 2 ? 0 : 1;
     return;
   }
+  if (p.family == Family::Kru3) {
+    k::KruArgs a{};
+    a.N0 = p.kru.N0;
+    a.N1 = p.kru.N1;
+    a.N2 = p.kru.N2;
+    a.D0 = p.kru.D0;
+    a.D1 = p.kru.D1;
+    a.D2 = p.kru.D2;
+    const char* why = nullptr;
+    if (!k::tcKru3Supported(a, &why)) invalid(why);  // (null pointers pass the alignment check)
+    return;
+  }
   if (p.family != Family::Gemm && p.family != Family::FcChain)
     invalid(std::string("no tensor-core kernel for the ") + familyName(p.family) +
-            " family (tensor-core math covers TMM, TBMM, C3, the FC chains and gconv)");
+            " family (tensor-core math covers TMM, TBMM, C3, the FC chains, gconv and 3-KRU)");
   auto ok4 = [](int64_t v) { return v % 4 == 0; };
   if (p.family == Family::Gemm) {
     const GemmDesc& g = p.gemm;
@@ -226,6 +238,7 @@ std::string Mapping::describe() const {
   os << familyName(family) << ":";
   if (math != k::kMathFfma) {
     os << "tcgen05 " << mathName(math);
+    if (family == Family::Kru3) return os.str() + " fused 3-step (TMEM -> next step's A in smem)";
     if (family == Family::Gconv)
       return os.str() + (gconvVariant == 1   ? " implicit-GEMM (on-chip im2col)"
                          : gconvVariant == 2 ? " implicit-GEMM (shifted halo)"
@@ -622,6 +635,7 @@ double tcTolerance(const Problem& p, int math) {
       for (const auto& L : p.fc.layers) K = std::max<int64_t>(K, L.kred);
       break;
     case Family::Gconv: K = (int64_t)p.gconv.C * p.gconv.KH * p.gconv.KW; break;
+    case Family::Kru3: K = (int64_t)p.kru.N0 + p.kru.N1 + p.kru.N2; break;  // three chained K = 16 steps
     default: break;
   }
   // between two tensor-core plans both errors count: twice the per-mode bound
@@ -775,6 +789,12 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
       a.D0 = d.D0;
       a.D1 = d.D1;
       a.D2 = d.D2;
+      if (m.math != k::kMathFfma) {
+        const char* why = nullptr;
+        if (!k::tcKru3Supported(a, &why)) fail(ErrorKind::MappingInvalid, why);
+        check(k::launchTcKru3(a, m.math, s), "tensor-core 3-KRU");
+        return;
+      }
       check(k::launchKru3(a, m.dchunk, m.threads, s), "3-KRU");
       return;
     }

@@ -167,11 +167,11 @@ def test_tc_explicit_plan_and_errors(env):
     with pytest.raises(TcError) as ei:
         run(ee, "tmm", [A2, B2], [np.zeros((16, 16), np.float32)], "tf32")
     assert ei.value.kind == "MappingInvalid"
-    # families without a tensor-core kernel say so
+    # shapes the tensor-core 3-KRU does not take say so (D0 != D1)
     X = rng.f32((4, 16, 16, 16))
-    Ws = [rng.f32((32, 16)) for _ in range(3)]
+    Ws = [rng.f32((32, 16)), rng.f32((16, 16)), rng.f32((32, 16))]
     with pytest.raises(TcError) as ei:
-        run(ee, "3KRU", Ws + [X], [np.zeros((4, 32, 32, 32), np.float32), np.zeros((4, 16, 32, 32), np.float32),
+        run(ee, "3KRU", Ws + [X], [np.zeros((4, 32, 16, 32), np.float32), np.zeros((4, 16, 16, 32), np.float32),
                                    np.zeros((4, 16, 16, 32), np.float32)], "tf32")
     assert ei.value.kind == "MappingInvalid"
 
@@ -247,6 +247,29 @@ def test_gconv_tc_paper_shape_sampled(env, variant):
     err = max_rel(ref, got.reshape(-1)[idx])
     record("gconv paper shape sampled", "3xtf32", 144, err, None, None)
     assert err <= tol("3xtf32", 144)
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("shape", [(3, 32, 48), (2, 16, 16), (8, 32, 32)])  # (M, D0 = D1, D2)
+def test_kru_tc(env, shape, math):
+    """tcgen05 3-KRU (tc_kru.cu): three chained K = 16 contractions, each
+    return within the stated bound for its depth in the chain (the K of every
+    contraction feeding it), scaled by the operand magnitudes."""
+    ee, orc = env
+    M, D, D2 = shape
+    rng = orc.rng(5 + M + D + D2)
+    W0, W1, W2 = rng.f32((D, 16)), rng.f32((D, 16)), rng.f32((D2, 16))
+    X = rng.f32((M, 16, 16, 16))
+    Y, XW1, XW2 = orc.kru3(W0, W1, W2, X)
+    outs = [np.zeros(Y.shape, np.float32), np.zeros(XW1.shape, np.float32), np.zeros(XW2.shape, np.float32)]
+    (gY, gXW1, gXW2), desc = run(ee, "3KRU", [W0, W1, W2, X], outs, math)
+    assert "tcgen05" in desc["kernel"] and "3-step" in desc["kernel"]
+    for name, got, ref, K, scale in (("XW2", gXW2, XW2, 16, opscale(X, W2)),
+                                     ("XW1", gXW1, XW1, 32, opscale(XW2, W1)),
+                                     ("Y", gY, Y, 48, opscale(XW1, W0))):
+        err = max_rel(ref, got)
+        record(f"3KRU {shape} {name}", math, K, err, None, None)
+        assert err <= tol(math, K, scale), f"3KRU {shape} {name} {math}: maxRel {err:.3g} > {tol(math, K, scale):.3g}"
 
 
 @pytest.mark.parametrize("math", ["tf32", "3xtf32"])
