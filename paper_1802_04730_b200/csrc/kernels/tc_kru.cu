@@ -124,7 +124,10 @@ __global__ void __launch_bounds__(kThreadsKru) tc_kru3_kernel(const KruArgs a) {
     mbarInit(bar, 1);
     fenceBarrierInit();
   }
-  if (warp == 0) tmemAlloc<256>(tmemSlot);
+  // TMEM: step 1 (2 x nb1) then step 2 (2 x nb2) columns, step 3 reuses both
+  // (4 x nb3): 128 columns for TF32, so four CTAs' worth fit an SM
+  constexpr int kCols = X3 ? 256 : 128;
+  if (warp == 0) tmemAlloc<kCols>(tmemSlot);
   tcFenceBefore();
   __syncthreads();
   tcFenceAfter();
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(kThreadsKru) tc_kru3_kernel(const KruArgs a) {
   __syncthreads();
   if (warp == 0) {
     tcFenceAfter();
-    tmemFree<256>(tmem);
+    tmemFree<kCols>(tmem);
   }
 }
 
