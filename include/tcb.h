@@ -84,7 +84,7 @@ extern "C" {
 
 /* arithmetic of a compiled handle (tcb_compile_ex) */
 #define TCB_MATH_FFMA 0   /* default: FFMA-exact kernels, bit-identical to the reference interpreter */
-#define TCB_MATH_TF32 1   /* tcgen05 .kind::tf32 tensor cores (GEMM-NT family, FC chains); tolerance DESIGN.md §2 */
+#define TCB_MATH_TF32 1   /* tcgen05 .kind::tf32 tensor cores (GEMM-NT, FC chains, gconv, 3KRU); tolerance DESIGN.md §2 */
 #define TCB_MATH_3XTF32 3 /* tcgen05 TF32 with hi/lo operand split (3 MMAs): near-fp32 accuracy */
 
 /* run flags */
@@ -139,7 +139,7 @@ int tcb_compile(tcb_engine* e, const char* name, const tcb_tensor* inputs, int n
                 const tcb_tensor* outputs, int n_outputs, const char* options_json, uint64_t* handle);
 
 /* compile with an explicit arithmetic (TCB_MATH_*). Tensor-core modes exist
- * for tmm, tbmm, C3, MLP1, 2FCRelu, MLP3 and gconv; other defs fail with
+ * for tmm, tbmm, C3, MLP1, 2FCRelu, MLP3, gconv and 3KRU; other defs fail with
  * TCB_ERR_MAPPING_INVALID. Their cache entries carry the target suffix
  * " math=<mode>" and never mix with the exact ones. */
 int tcb_compile_ex(tcb_engine* e, const char* name, const tcb_tensor* inputs, int n_inputs,
