@@ -103,8 +103,8 @@ std::string formOf(const std::string& canonicalTc);  // "" if unregistered
 
 Problem match(const sem::Specialized& s, const std::string& canonicalTc);  // Error(NoKernel)
 // math: k::MathMode. Tensor-core modes exist for the GEMM-NT family
-// (TMM, TBMM, C3) and the FC chains (per-layer GEMMs); other families
-// raise MappingInvalid for them.
+// (TMM, TBMM, C3), the FC chains (per-layer GEMMs), gconv (implicit GEMM)
+// and 3-KRU (three chained GEMMs); the LUT family raises MappingInvalid.
 Mapping decode(const Problem& p, const MappingOptions& o, int math = k::kMathFfma);  // Error(MappingInvalid)
 MappingOptions defaultOptions(const Problem& p, int math = k::kMathFfma);
 const char* mathName(int math);
