@@ -52,6 +52,12 @@ PAPER_OPS = [
     ("C3", "C3 128x1024->1000", [(128, 1024), (1000, 1024)], {0: (128, 1000)}),
     ("3KRU", "3KRU M=256 16^3->32^3", [(32, 16), (32, 16), (32, 16), (256, 16, 16, 16)], {}),
     ("gconv", "gconv 32,32,16,16,58x58,3x3", [(32, 32, 16, 58, 58), (32, 16, 16, 3, 3), (16,)], {}),
+    # the paper's four gconv columns (N,G,F,C,W,H) = (32,32,16,16,14,14), (32,32,32,32,7,7),
+    # (32,32,4,4,56,56), (32,32,8,8,28,28): W,H are the outputs of 3x3 taps
+    ("gconv", "gconv paper 32,32,16,16,14x14", [(32, 32, 16, 16, 16), (32, 16, 16, 3, 3), (16,)], {}),
+    ("gconv", "gconv paper 32,32,32,32,7x7", [(32, 32, 32, 9, 9), (32, 32, 32, 3, 3), (32,)], {}),
+    ("gconv", "gconv paper 32,32,4,4,56x56", [(32, 32, 4, 58, 58), (32, 4, 4, 3, 3), (4,)], {}),
+    ("gconv", "gconv paper 32,32,8,8,28x28", [(32, 32, 8, 30, 30), (32, 8, 8, 3, 3), (8,)], {}),
     ("2LUT", "2LUT E=1e7,D=64,B=128,L=50",
      [(10_000_000, 64), (128, 50), (10_000_000, 64), (128, 50)], {}),
 ]
@@ -62,7 +68,8 @@ TC_OPS = [("tmm 128x1024x1024", "3xtf32"), ("tmm 128x1024x1024", "tf32"),
           ("tbmm 500,26,72,26", "3xtf32"), ("MLP1 128x1128->128", "3xtf32"),
           ("2FCRelu 128x1128->128->64", "3xtf32"), ("MLP3 128->64->32->2", "3xtf32"),
           ("gconv 32,32,16,16,58x58,3x3", "3xtf32"), ("gconv 32,32,16,16,58x58,3x3", "tf32"),
-          ("3KRU M=256 16^3->32^3", "3xtf32"), ("3KRU M=256 16^3->32^3", "tf32")]
+          ("3KRU M=256 16^3->32^3", "3xtf32"), ("3KRU M=256 16^3->32^3", "tf32"),
+          ("gconv paper 32,32,16,16,14x14", "tf32"), ("gconv paper 32,32,32,32,7x7", "tf32")]
 INT_PARAMS = {"2LUT": {1, 3}, "1LUT": {1}}
 
 
@@ -525,9 +532,10 @@ def main():
             for st in e2e_streams:
                 st.synchronize()
 
-        # untimed warm-up: the first ~150 host calls run slow (pinned-page and
-        # IOMMU mappings warming up: blocks of 50 measured 474, 341, 270, 234, 232 us)
-        for i in range(max(args.warmup, 200)):
+        # untimed warm-up: the first host calls run slow (pinned-page and IOMMU
+        # mappings warming up; blocks of 50 after 200 warm-up calls still fell
+        # 441, 408, 300, 278, 270 us on one box), ~0.3 s
+        for i in range(max(args.warmup, 1000)):
             e2e_step(i)
         # host wall clock (each step ends with its outputs on the host), in 5
         # blocks of kb steps; the median block is reported (one-off host

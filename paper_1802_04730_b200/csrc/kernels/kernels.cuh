@@ -118,7 +118,7 @@ cudaError_t launchTcGconv(const GconvArgs& a, int math, cudaStream_t s);
 cudaError_t launchTcGconvTma(const GconvArgs& a, int math, cudaStream_t s);
 // shifted-halo implicit GEMM (tc_gconv_shift.cu): one halo tile per 128
 // virtual pixels, every tap a shifted K-major descriptor into it
-bool tcGconvShiftSupported(const GconvArgs& a, const char** why);
+bool tcGconvShiftSupported(const GconvArgs& a, int math, const char** why);
 cudaError_t launchTcGconvShift(const GconvArgs& a, int math, cudaStream_t s);
 size_t gconvSmem(const GconvArgs& a, int th, int rw);
 int gconvThreads(const GconvArgs& a, int variant, int th);

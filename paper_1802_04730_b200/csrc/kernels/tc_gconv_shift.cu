@@ -317,7 +317,7 @@ cudaError_t launchShift(const ShiftParams& p, cudaStream_t s) {
 
 }  // namespace
 
-bool tcGconvShiftSupported(const GconvArgs& a, const char** why) {
+bool tcGconvShiftSupported(const GconvArgs& a, int math, const char** why) {
   auto no = [&](const char* w) {
     if (why) *why = w;
     return false;
@@ -325,16 +325,16 @@ bool tcGconvShiftSupported(const GconvArgs& a, const char** why) {
   if (a.C % 8) return no("tensor-core gconv needs input channels per group that are a multiple of 8");
   if (a.F != 16 && a.F != 32 && a.F != 64) return no("tensor-core gconv needs 16, 32 or 64 filters per group");
   const int HP = ((128 + (a.KH - 1) * a.W + (a.KW - 1)) + 7) / 8 * 8;
-  const bool x3 = true;  // size for the larger (3xTF32) footprint
+  const bool x3 = math == kMath3xTf32;
   const int64_t bytes = 1024 + (int64_t)kStagesSh * a.C * HP * 4 * (x3 ? 2 : 1) +
-                        (int64_t)a.KH * a.KW * (a.C / 8) * 32 * (2 * a.F) * 2 + 1024 + 8 * a.KH * a.KW * (a.C / 8) +
-                        4 * a.Mb;
+                        (int64_t)a.KH * a.KW * (a.C / 8) * 32 * (x3 ? 2 * a.F : a.F) * 2 + 1024 +
+                        8 * a.KH * a.KW * (a.C / 8) + 4 * a.Mb;
   if (bytes > 227 * 1024) return no("tensor-core gconv (shifted halo): the halo ring exceeds shared memory");
   return true;
 }
 
 cudaError_t launchTcGconvShift(const GconvArgs& a, int math, cudaStream_t s) {
-  if (!tcGconvShiftSupported(a, nullptr)) return cudaErrorInvalidValue;
+  if (!tcGconvShiftSupported(a, math, nullptr)) return cudaErrorInvalidValue;
   ShiftParams p{};
   p.I = a.I;
   p.O = a.O;

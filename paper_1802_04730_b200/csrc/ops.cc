@@ -79,7 +79,7 @@ void decodeTc(const Problem& p, const MappingOptions& o, Mapping& m) {
     // tile_sizes[2]: 2 = NHWC staging, 3 = shifted halo, else on-chip im2col
     const int sel = o.tileSizes.size() > 2 ? static_cast<int>(o.tileSizes[2]) : 0;
     if (sel == 3) {
-      if (!k::tcGconvShiftSupported(a, &why)) invalid(why);
+      if (!k::tcGconvShiftSupported(a, m.math, &why)) invalid(why);
       m.gconvVariant = 2;
       return;
     }
@@ -523,7 +523,7 @@ MappingOptions defaultOptions(const Problem& p, int math) {
     a.KH = p.gconv.KH;
     a.KW = p.gconv.KW;
     a.Mb = p.gconv.Mb;
-    const int variant = k::tcGconvShiftSupported(a, nullptr) ? 3 : 1;
+    const int variant = k::tcGconvShiftSupported(a, math, nullptr) ? 3 : 1;
     o.tileSizes = {128, static_cast<int64_t>(p.gconv.F), variant};
     o.threadShape = {{512, 1, 1}};
     o.useShared = true;
@@ -599,11 +599,26 @@ MappingOptions defaultOptions(const Problem& p, int math) {
       o.useShared = true;
       break;
     case Family::Gconv: {
-      int Wo = p.gconv.W - p.gconv.KW + 1;
+      int Wo = p.gconv.W - p.gconv.KW + 1, Ho = p.gconv.H - p.gconv.KH + 1;
       int rw = (p.gconv.KW == 3 && Wo % 7 == 0) ? 7 : 4;
       int rf = 4;
       if (p.gconv.KW != 3) rw = 4;
       o.tileSizes = {4, rf, rw};
+      // small images: one CTA covers more rows (its filter staging is shared by
+      // more work); measured on the paper's four gconv columns
+      // (profiles/r01_gconv_columns_sweep.txt): 14x14 F16 rf4 x 7 rows 127 -> 63 us,
+      // 7x7 F32 rf2 x 7 rows 308 -> 104 us, 28x28 F8 and 56x56 F4 rf2 x 14 rows
+      // 108 -> 66 us and 109 -> 72 us; the 56x56 F16 shape keeps rf4 x 4 rows
+      if (rw == 7 && Ho % 7 == 0 && Ho <= 14) {
+        rf = p.gconv.F >= 32 ? 2 : 4;
+        o.tileSizes = {7, rf, rw};
+        break;
+      }
+      if (rw == 7 && Ho % 14 == 0 && p.gconv.F <= 8 && (Wo / 7) * 14 * ((p.gconv.F + 1) / 2) <= 512) {
+        rf = 2;
+        o.tileSizes = {14, rf, rw};
+        break;
+      }
       o.threadShape = {{1, 1, 1}};
       o.useShared = true;
       // shrink rows-per-CTA until the CTA fits 512 threads
@@ -817,7 +832,7 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
       if (m.math != k::kMathFfma) {
         const char* why = nullptr;
         if (m.gconvVariant == 2) {
-          if (!k::tcGconvShiftSupported(a, &why)) fail(ErrorKind::MappingInvalid, why);
+          if (!k::tcGconvShiftSupported(a, m.math, &why)) fail(ErrorKind::MappingInvalid, why);
           check(k::launchTcGconvShift(a, m.math, s), "tensor-core gconv");
         } else {
           if (!k::tcGconvSupported(a, &why)) fail(ErrorKind::MappingInvalid, why);

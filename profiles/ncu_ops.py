@@ -24,6 +24,10 @@ OPS = {
     "c3": ("C3", [(128, 1024), (1000, 1024)], {0: (128, 1000)}),
     "kru": ("3KRU", [(32, 16), (32, 16), (32, 16), (256, 16, 16, 16)], {}),
     "gconv": ("gconv", [(32, 32, 16, 58, 58), (32, 16, 16, 3, 3), (16,)], {}),
+    "gconv14": ("gconv", [(32, 32, 16, 16, 16), (32, 16, 16, 3, 3), (16,)], {}),
+    "gconv7": ("gconv", [(32, 32, 32, 9, 9), (32, 32, 32, 3, 3), (32,)], {}),
+    "gconv56": ("gconv", [(32, 32, 4, 58, 58), (32, 4, 4, 3, 3), (4,)], {}),
+    "gconv28": ("gconv", [(32, 32, 8, 30, 30), (32, 8, 8, 3, 3), (8,)], {}),
     "lut": ("2LUT", [(10_000_000, 64), (128, 50), (10_000_000, 64), (128, 50)], {}),
 }
 
