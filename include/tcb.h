@@ -162,7 +162,8 @@ int tcb_describe(tcb_engine* e, uint64_t handle, char* buf, int len);
 
 /* tuner::tune on the GPU. tune_options_json keys (all optional):
  * population (100), generations (25), mutation_rate (0.05), seed (0),
- * timing_iters (10), session_log (path), use_baselines (true),
+ * timing_iters (10), cold_l2 (true: a 2x-L2 buffer is rewritten before each
+ * timed launch), session_log (path), use_baselines (true),
  * math ("ffma" | "tf32" | "3xtf32": tune the tcgen05 tile/split genes; a
  * candidate must then agree with the mode's default plan within the stated
  * tolerance instead of bit-for-bit). Writes the best MappingOptions JSON.

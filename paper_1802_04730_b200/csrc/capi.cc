@@ -510,6 +510,7 @@ int tcb_tune(tcb_engine* e, const char* name, const tcb_tensor* in, int nin, con
       }
       if (j.has("seed")) o.seed = j.at("seed").asUInt();
       if (j.has("timing_iters")) o.timingIters = static_cast<int>(j.at("timing_iters").asInt());
+      if (j.has("cold_l2")) o.coldL2 = j.at("cold_l2").asBool();
       if (j.has("session_log")) o.sessionLog = j.at("session_log").asStr();
       if (j.has("use_baselines")) o.useBaselines = j.at("use_baselines").asBool();
       if (j.has("math")) o.math = ops::mathFromName(j.at("math").asStr());

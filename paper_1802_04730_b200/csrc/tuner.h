@@ -30,6 +30,7 @@ struct TuneOptions {
   double mutationRate = 0.05;
   uint64_t seed = 0;
   int timingIters = 10;
+  bool coldL2 = true;  // rewrite a 2x-L2 buffer before each timed launch
   std::string sessionLog;
   bool useBaselines = true;
   std::vector<MappingOptions> extraStarting;
