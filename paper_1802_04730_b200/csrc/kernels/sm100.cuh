@@ -168,6 +168,15 @@ __device__ __forceinline__ void mmaTf32(uint32_t tmemD, uint64_t a, uint64_t b, 
       "l"(a), "l"(b), "r"(idesc), "r"(accum)
       : "memory");
 }
+// one lane of the (converged) warp: issue tcgen05.mma from a warp-uniform
+// branch (elect.sync) instead of `lane == 0`, so the operands stay in uniform
+// registers and each MMA issues without a per-lane waterfall (~40 vs ~100
+// cycles per MMA at small N, profiles/umma_rate.cu)
+__device__ __forceinline__ bool electSync() {
+  uint32_t pred;
+  asm volatile("{ .reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p; }" : "=r"(pred));
+  return pred != 0;
+}
 // arrives on `bar` when every previously issued tcgen05.mma of this thread completes
 __device__ __forceinline__ void mmaCommit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem(bar))
