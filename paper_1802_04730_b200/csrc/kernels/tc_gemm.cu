@@ -130,19 +130,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // the whole warp runs the issue loop (warp-uniform operands); elect.sync
-    // picks the lane that issues each MMA
-    constexpr uint32_t idesc = idescTf32(kBM, BN);
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % S;
-      mbarWait(X3 ? &conv[s] : &full[s], (i / S) & 1, 2);
-      tcFenceAfter();
-      const uint32_t ab = smem(aBig(s)), bbg = smem(bBig(s));
+    if (lane == 0) {
+      constexpr uint32_t idesc = idescTf32(kBM, BN);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % S;
+        mbarWait(X3 ? &conv[s] : &full[s], (i / S) & 1, 2);
+        tcFenceAfter();
+        const uint32_t ab = smem(aBig(s)), bbg = smem(bBig(s));
 #pragma unroll
-      for (int kk = 0; kk < kBK / 8; ++kk) {
-        const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
-        const uint32_t acc = (i | kk) != 0;
-        if (electSync()) {
+        for (int kk = 0; kk < kBK / 8; ++kk) {
+          const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
+          const uint32_t acc = (i | kk) != 0;
           if constexpr (X3) {
             const uint32_t al = smem(aLo(s)), bl = smem(bLo(s));
             mmaTf32(tmem, descSw128(al + off), descSw128(bbg + off), idesc, acc);
@@ -152,12 +150,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mmaTf32(tmem, descSw128(ab + off), descSw128(bbg + off), idesc, acc);
           }
         }
+        mmaCommit(&empty[s]);
       }
-      if (electSync()) mmaCommit(&empty[s]);
-      __syncwarp();
+      mmaCommit(tmemFull);
     }
-    if (electSync()) mmaCommit(tmemFull);
-    __syncwarp();
   } else if (warp >= 4) {
     const int et = threadIdx.x - 128;
     if constexpr (X3) {

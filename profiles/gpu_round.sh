@@ -21,4 +21,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_
     -o $OUT/tc python profiles/ncu_ops.py math=tf32 reps=1 c3 tmm_huge > $OUT/ncu_tc.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_gconv" -c 2 \
     -o $OUT/tcgconv python profiles/ncu_ops.py math=tf32 reps=1 gconv > $OUT/ncu_tcgconv.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_kru" -c 1 \
+    -o $OUT/tckru python profiles/ncu_ops.py math=tf32 reps=1 kru > $OUT/ncu_tckru.log 2>&1
 ls -la $OUT
