@@ -153,6 +153,17 @@ __device__ __forceinline__ uint64_t descSw128(uint32_t saddr) {
   d |= static_cast<uint64_t>(2) << 61;            // SWIZZLE_128B
   return d;
 }
+// K-major operand without swizzle (CuTe INTERLEAVE): 8-row x 16-byte core
+// matrices; LBO = byte distance to the next core matrix along K, SBO = to the
+// next 8-row group
+__device__ __forceinline__ uint64_t descKInterleave(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>(lbo >> 4) << 16;
+  d |= static_cast<uint64_t>(sbo >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version; layout type 0 = SWIZZLE_NONE
+  return d;
+}
 // .kind::tf32, fp32 accumulate, both operands K-major
 __host__ __device__ constexpr uint32_t idescTf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |

@@ -65,21 +65,10 @@ struct TcConvParams {
   int kc;      // K steps per pipeline stage (a stage holds kc x 4 KB of A)
 };
 
-// K-major operand without swizzle (CuTe INTERLEAVE): 8-row x 16-byte core
-// matrices; LBO = next core matrix along K, SBO = next 8-row group
 __device__ __forceinline__ void sts4(uint32_t addr, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
-__device__ __forceinline__ uint64_t descKInterleave(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
-  d |= static_cast<uint64_t>(lbo >> 4) << 16;
-  d |= static_cast<uint64_t>(sbo >> 4) << 32;
-  d |= static_cast<uint64_t>(1) << 46;  // version; layout type 0 = SWIZZLE_NONE
-  return d;
-}
-
 template <int F, bool X3>
 struct ConvCfg {
   // 2 accumulator buffers x kAcc independent partial accumulators of F columns

@@ -59,21 +59,6 @@ struct ShiftParams {
   int HP;  // halo pixels per tile (multiple of 8)
 };
 
-__device__ __forceinline__ bool elect() {
-  uint32_t pred;
-  asm volatile("{ .reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p; }" : "=r"(pred));
-  return pred != 0;
-}
-
-__device__ __forceinline__ uint64_t descKI(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
-  d |= static_cast<uint64_t>(lbo >> 4) << 16;
-  d |= static_cast<uint64_t>(sbo >> 4) << 32;
-  d |= static_cast<uint64_t>(1) << 46;  // version; layout type 0 = SWIZZLE_NONE
-  return d;
-}
-
 template <int F, bool X3>
 struct ShiftCfg {
   // 3xTF32 stacks B as [b_hi | b_lo] (N = 2F): a_hi*[b_hi|b_lo] and
@@ -234,18 +219,18 @@ __global__ void __launch_bounds__(kThreadsSh, 1) tc_gconv_shift_kernel(const Shi
       mbarWait(&full[s], (lt / S) & 1, 3);
       tcFenceAfter();
       const uint32_t aHi = smem(stages + s * stF);
-      const uint64_t ah0 = descKI(aHi, lboA, 128), al0 = descKI(aHi + planeF * 4, lboA, 128);
-      const uint64_t b0 = descKI(smem(bBank + bank * bStride), lboB, 128);
+      const uint64_t ah0 = descKInterleave(aHi, lboA, 128), al0 = descKInterleave(aHi + planeF * 4, lboA, 128);
+      const uint64_t b0 = descKInterleave(smem(bBank + bank * bStride), lboB, 128);
       const uint32_t d = tmem + buf * NB;
 #pragma unroll 2
       for (int ks = 0; ks < nks; ++ks) {
         const uint64_t ao = aOff16[ks], bd = b0 + static_cast<uint64_t>(ks * 2 * NB);  // 32*NB bytes per step
-        if (elect()) {
+        if (electSync()) {
           mmaTf32(d, ah0 + ao, bd, idesc, ks > 0);
           if constexpr (X3) mmaTf32(d, al0 + ao, bd, idesc, 1);
         }
       }
-      if (elect()) {
+      if (electSync()) {
         mmaCommit(&empty[s]);
         mmaCommit(&tFull[buf]);
       }

@@ -38,21 +38,6 @@ constexpr int kR = 16;   // N0 = N1 = N2: the reduction extent of every step
 // memory of the step-2/3 operands so more CTAs share an SM
 constexpr int kThreadsKru = 128;
 
-__device__ __forceinline__ bool electOne() {
-  uint32_t pred;
-  asm volatile("{ .reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p; }" : "=r"(pred));
-  return pred != 0;
-}
-
-__device__ __forceinline__ uint64_t descKI(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
-  d |= static_cast<uint64_t>(lbo >> 4) << 16;
-  d |= static_cast<uint64_t>(sbo >> 4) << 32;
-  d |= static_cast<uint64_t>(1) << 46;  // version; layout type 0 = SWIZZLE_NONE
-  return d;
-}
-
 // [k/4][rows][4] operand: element (row, k)
 __device__ __forceinline__ int kmIdx(int row, int k, int rows) { return ((k >> 2) * rows + row) * 4 + (k & 3); }
 
@@ -142,17 +127,17 @@ __global__ void __launch_bounds__(kThreadsKru) tc_kru3_kernel(const KruArgs a) {
       for (int rb = 0; rb < rows / 128; ++rb)
         for (int ks = 0; ks < 2; ++ks) {
           const uint32_t aoff = (2 * ks * rows + rb * 128) * 16, boff = 2 * ks * n * 16;
-          const uint64_t ah = descKI(smem(A) + aoff, rows * 16, 128), bd = descKI(smem(B) + boff, n * 16, 128);
-          if (electOne()) {
+          const uint64_t ah = descKInterleave(smem(A) + aoff, rows * 16, 128), bd = descKInterleave(smem(B) + boff, n * 16, 128);
+          if (electSync()) {
             mmaTf32(tmem + col0 + rb * n, ah, bd, idesc, ks > 0);
             if constexpr (X3) {
-              const uint64_t al = descKI(smem(A + rows * kR) + aoff, rows * 16, 128);
+              const uint64_t al = descKInterleave(smem(A + rows * kR) + aoff, rows * 16, 128);
               mmaTf32(tmem + col0 + rb * n, al, bd, idesc, 1);
             }
           }
           __syncwarp();
         }
-      if (electOne()) mmaCommit(bar);
+      if (electSync()) mmaCommit(bar);
       __syncwarp();
     }
     mbarWait(bar, parity, 0);
