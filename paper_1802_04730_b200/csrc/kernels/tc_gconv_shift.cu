@@ -79,11 +79,7 @@ struct ShiftCfg {
   }
 };
 
-// KWT / KCBT: compile-time taps per row and 8-channel steps (0 = runtime):
-// with both known the MMA loop unrolls over (kw, c8) and its descriptor
-// offsets are uniform-register arithmetic, ~40 instead of ~76-117 cycles per
-// MMA issue (profiles/umma_rate.cu, "gconv-like" variants)
-template <int F, bool X3, int KWT = 0, int KCBT = 0>
+template <int F, bool X3>
 __global__ void __launch_bounds__(kThreadsSh, 1) tc_gconv_shift_kernel(const ShiftParams p) {
   using Cfg = ShiftCfg<F, X3>;
   constexpr int S = kStagesSh;
@@ -226,29 +222,12 @@ __global__ void __launch_bounds__(kThreadsSh, 1) tc_gconv_shift_kernel(const Shi
       const uint64_t ah0 = descKInterleave(aHi, lboA, 128), al0 = descKInterleave(aHi + planeF * 4, lboA, 128);
       const uint64_t b0 = descKInterleave(smem(bBank + bank * bStride), lboB, 128);
       const uint32_t d = tmem + buf * NB;
-      if constexpr (KWT > 0 && KCBT > 0) {
-        // A start (16-byte units) of step (kh, kw, c8): c8 * 2*HP + kh * W + kw
-        const uint32_t hp2 = 2 * HP, w = p.W;
-        uint32_t ks = 0;
-        for (uint32_t kh = 0; kh < (uint32_t)p.KH; ++kh)
-#pragma unroll
-          for (uint32_t kw = 0; kw < (uint32_t)KWT; ++kw)
-#pragma unroll
-            for (uint32_t c8 = 0; c8 < (uint32_t)KCBT; ++c8, ++ks) {
-              const uint64_t ao = c8 * hp2 + kh * w + kw, bd = b0 + static_cast<uint64_t>(ks * 2 * NB);
-              if (electSync()) {
-                mmaTf32(d, ah0 + ao, bd, idesc, ks > 0);
-                if constexpr (X3) mmaTf32(d, al0 + ao, bd, idesc, 1);
-              }
-            }
-      } else {
 #pragma unroll 2
-        for (int ks = 0; ks < nks; ++ks) {
-          const uint64_t ao = aOff16[ks], bd = b0 + static_cast<uint64_t>(ks * 2 * NB);  // 32*NB bytes per step
-          if (electSync()) {
-            mmaTf32(d, ah0 + ao, bd, idesc, ks > 0);
-            if constexpr (X3) mmaTf32(d, al0 + ao, bd, idesc, 1);
-          }
+      for (int ks = 0; ks < nks; ++ks) {
+        const uint64_t ao = aOff16[ks], bd = b0 + static_cast<uint64_t>(ks * 2 * NB);  // 32*NB bytes per step
+        if (electSync()) {
+          mmaTf32(d, ah0 + ao, bd, idesc, ks > 0);
+          if constexpr (X3) mmaTf32(d, al0 + ao, bd, idesc, 1);
         }
       }
       if (electSync()) {
@@ -306,11 +285,7 @@ __global__ void __launch_bounds__(kThreadsSh, 1) tc_gconv_shift_kernel(const Shi
 template <int F, bool X3>
 cudaError_t launchShift(const ShiftParams& p, cudaStream_t s) {
   using Cfg = ShiftCfg<F, X3>;
-  // the unrolled loop is measured faster on the paper's 58x58 planes (TF32
-  // 347 -> 322 us) and slower on the small paper columns (14x14: 29 -> 33 us,
-  // 7x7 with C = 32: 37 -> 41 us), so it is used for large planes only
-  auto kern = (p.KW == 3 && p.C == 16 && p.H * p.W >= 1024) ? tc_gconv_shift_kernel<F, X3, 3, 2>
-                                                           : tc_gconv_shift_kernel<F, X3>;
+  auto kern = tc_gconv_shift_kernel<F, X3>;
   const int smemBytes = Cfg::smem(p);
   if (smemBytes > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smemBytes);
