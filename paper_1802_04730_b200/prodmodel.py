@@ -2,7 +2,8 @@
 CUDA graph over the tc-b200 kernels:
 
     (C1, C2) = 2LUT(LUT1, I1, LUT2, I2)           # embeddings, B x D each
-    C3       = C3(I3, W)                           # += onto zeros (a fresh return)
+    C3       = C3(I3, W)                           # += onto zeros (a fresh return): run as the
+                                                   # tmm def (zero-init chain, same bits, no memset)
     I        = concat(C1, C2, C3)                  # B x (2D + WY); not expressible in TC
     O1       = MLP1(I, W1, B1)
     O2..O4   = MLP3(O1, W2, B2, W3, B3, W4, B4)
@@ -47,7 +48,10 @@ class ProductionModel:
                         O3=z(B, P), O4=z(B, Q))
         o = self.out
         self.h_lut = ee.compile("2LUT", [p["LUT1"], p["I1"], p["LUT2"], p["I2"]], [o["C1"], o["C2"]])
-        self.h_c3 = ee.compile("C3", [p["I3"], p["W"]], [o["C3"]], math=math)
+        # C3 from zeros: the `tmm` def's chain starts from 0.0 exactly as C3's
+        # `+=` onto a zeroed return does (fma(a, b, 0) == a*b), so the zero
+        # fill drops out of the critical path with identical bits
+        self.h_c3 = ee.compile("tmm", [p["I3"], p["W"]], [o["C3"]], math=math)
         self.h_mlp1 = ee.compile("MLP1", [o["I"], p["W1"], p["B1"]], [o["O1"]], math=math)
         self.h_mlp3 = ee.compile("MLP3", [o["O1"], p["W2"], p["B2"], p["W3"], p["B3"], p["W4"], p["B4"]],
                                  [o["O1"], o["O2"], o["O3"], o["O4"]], math=math)
@@ -70,8 +74,7 @@ class ProductionModel:
         torch, ee, p, o = self.torch, self.ee, self.p, self.out
         s = self.stream
         self.side.wait_stream(s)
-        with torch.cuda.stream(self.side):  # C3 += onto a fresh zero return
-            o["C3"].zero_()
+        with torch.cuda.stream(self.side):  # C3 onto a fresh zero return (the tmm def: zero-init chain)
             ee.run(self.h_c3, [p["I3"], p["W"]], [o["C3"]], stream=self.side.cuda_stream, check_errors=False)
         ee.run(self.h_lut, [p["LUT1"], p["I1"], p["LUT2"], p["I2"]], [o["C1"], o["C2"]], stream=s.cuda_stream,
                check_errors=check_errors)

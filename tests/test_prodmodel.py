@@ -45,7 +45,7 @@ def test_prodmodel_graph_small_bit_exact():
     for v in m.out.values():
         v.fill_(123.0)
     m.capture()
-    for _ in range(3):  # replays are idempotent (C3 is re-zeroed inside the graph)
+    for _ in range(3):  # replays are idempotent (every output is rewritten from scratch)
         m.replay()
     m.check()
     for k in ref:
