@@ -189,6 +189,15 @@ class OpInstance:
         return t
 
 
+DOM_NOTES = {
+    "2FCRelu": "Bound by its sequential FFMA chain (1128 dependent steps per output), see chain_floor_us.",
+    "tbmm": "500 batches of 26x26 outputs, 72-step chains: one wave of CTAs whose time is load latency + "
+            "chain + store; its plan (two 64-deep k stages) is picked for overlap with the FC chains of the "
+            "forked step, not for its time alone (DESIGN.md section 8).",
+    "MLP3": "Three short dependent layers (128, 64, 32 steps): latency bound, see chain_floor_us.",
+}
+
+
 def chain_floor_us(op, fma_latency_cycles=4, mhz=1965.0):
     """Latency floor of an FFMA-exact operator: every output is one
     sequential chain of fused multiply-adds (the reference's reduction order),
@@ -581,8 +590,7 @@ def main():
                 "algorithmic_bytes": int(dom.bytes), "launch_us": round(dom_t * 1e6, 3),
                 "share_of_step": round(dom_t / step_dev, 3), "peak_source": peak_src,
                 "note": "FFMA-exact fp32 kernels: no tensor-core roofline applies; HBM roofline over the "
-                        "kernel's algorithmic bytes (inputs once, outputs once). The step's kernels are bound by "
-                        "their sequential FFMA chains (2FCRelu: 1128 dependent steps), see chain_floor_us",
+                        "kernel's algorithmic bytes (inputs once, outputs once). " + DOM_NOTES.get(dom.name, ""),
                 "chain_floor_us": round(chain_floor_us(dom), 3)}
     tbmm = [x for x in per_op if x[0].name == "tbmm"][0]
     roofline_ops = {
@@ -635,7 +643,7 @@ def main():
 def prod_model_line(ee, torch, dev):
     """The production model chain (2LUT -> C3 -> concat ->
     MLP1 -> MLP3) at the paper's sizes, one CUDA graph per forward pass:
-    device µs per forward (200 back-to-back replays) and the paper-protocol
+    device µs per forward (median of 5 blocks of 100 back-to-back replays) and the paper-protocol
     synchronised latency."""
     try:
         from paper_1802_04730_b200.prodmodel import PAPER_SIZES as S
@@ -653,15 +661,19 @@ def prod_model_line(ee, torch, dev):
         for _ in range(5):
             m.replay()
         m.check()
-        n = 200
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record(m.stream)
-        for _ in range(n):
+        for _ in range(50):
             m.replay()
-        e1.record(m.stream)
-        e1.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / n
+        n, blocks = 100, []
+        for _ in range(5):  # median of 5 blocks: graph replays are host-launched
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(m.stream)
+            for _ in range(n):
+                m.replay()
+            e1.record(m.stream)
+            e1.synchronize()
+            blocks.append(e0.elapsed_time(e1) * 1e3 / n)
+        us = sorted(blocks)[2]
         lat = []
         for _ in range(100):
             torch.cuda.synchronize()
@@ -670,7 +682,8 @@ def prod_model_line(ee, torch, dev):
             m.stream.synchronize()
             lat.append(time.perf_counter() - t0)
         lat.sort()
-        out = {"us_per_forward": round(us, 3), "gflops": round(m.flops / us / 1e3, 1),
+        out = {"us_per_forward": round(us, 3), "blocks_us_per_forward": [round(b, 2) for b in blocks],
+               "gflops": round(m.flops / us / 1e3, 1),
                "us_p0_p50_p90_sync": [round(lat[0] * 1e6, 1), round(lat[50] * 1e6, 1), round(lat[90] * 1e6, 1)],
                "kernels": m.kernels, "graph": "2LUT || C3 (tmm def, from zeros) -> concat -> MLP1 -> MLP3, one CUDA graph",
                "sizes": S}

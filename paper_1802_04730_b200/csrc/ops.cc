@@ -550,6 +550,16 @@ MappingOptions defaultOptions(const Problem& p, int math) {
 
       auto ctas = [&](int tm, int tn) { return (double)g.batch * ((g.M + tm - 1) / tm) * ((g.N + tn - 1) / tn); };
       o.unrollCopyShared = g.K > 128;
+      if (g.K > 32 && g.K <= 128 && ctas(32, 32) >= 2 * 148) {
+        // short reductions over many tiles (TBMM 500 x 26x26x72): two k
+        // stages instead of three. Slower alone (8.4 -> 9.6 us) but its CTAs
+        // overlap the FC chains of the bench step far better (step 19.5 ->
+        // 18.0 us, profiles/r01_step_variants.txt)
+        o.tileSizes = {32, 32, 64};
+        o.threadShape = {{16, 16, 1}};
+        o.unrollCopyShared = false;
+        break;
+      }
       if (g.K > 128 && ctas(32, 32) >= 96) {
         // long reductions with enough 32x32 tiles: 64-deep k stages (measured
         // best of the 19 variants for C3 / TMM 128x1024x1024 on B200)
@@ -575,15 +585,23 @@ MappingOptions defaultOptions(const Problem& p, int math) {
       int outMax = 0;
       for (const auto& L : p.fc.layers) outMax = std::max(outMax, L.out);
       int cn = std::min(8, std::max(1, (outMax + 15) / 16));
-      // aim at ~2 co-resident CTAs per SM (>= 200 CTAs): a wave of 1-CTA/SM
-      // 8-clusters does not fit the GPCs (max 15 active of 16 on B200)
-      int rows = 1;
-      while (rows < 16 && (int64_t)((p.fc.batch + rows * 2 - 1) / (rows * 2)) * cn >= 200) rows *= 2;
       k::FcChainArgs a{};
       a.layers = static_cast<int>(p.fc.layers.size());
       for (int l = 0; l < a.layers; ++l) {
         a.L[l].out = p.fc.layers[l].out;
         a.L[l].kred = p.fc.layers[l].kred;
+      }
+      // aim at ~2 co-resident CTAs per SM (>= 200 CTAs): a wave of 1-CTA/SM
+      // 8-clusters does not fit the GPCs (max 15 active of 16 on B200).
+      // Chains with small slices (<= 32 KB per CTA) go to >= 128 fatter CTAs:
+      // MLP3 rows 2 -> 4 is as fast alone and overlaps better in the bench
+      // step (profiles/r01_step_variants.txt)
+      int rows = 1;
+      while (rows < 16) {
+        const int nr = rows * 2;
+        const int64_t ctas = (int64_t)((p.fc.batch + nr - 1) / nr) * cn;
+        if (ctas < (k::fcChainSmem(a, nr, cn) <= 32 * 1024 ? 128 : 200)) break;
+        rows = nr;
       }
       while (rows > 1 && k::fcChainSmem(a, rows, cn) > 110 * 1024) rows /= 2;
       int t = std::max(64, k::fcChainThreads(a, rows, cn));  // one pass per layer

@@ -1,0 +1,112 @@
+"""The bench step (TBMM || 2FCRelu || MLP3, forked onto side streams) with
+alternative plans per operator: does a plan that is slower alone overlap
+better? Device µs per step over graphs of NSTEP consecutive steps, plus each
+variant alone. Usage: python profiles/step_variants.py"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1802_04730_b200 import ExecutionEngine  # noqa: E402
+
+NSTEP = int(os.environ.get("NSTEP", "26"))
+
+COMBOS = [
+    {"tbmm": {"tile_sizes": [32, 32, 64]}, "MLP3": {"tile_sizes": [4, 4, 1]}},
+    {"tbmm": {"tile_sizes": [32, 32, 64]}, "MLP3": {"tile_sizes": [2, 2, 1]}},
+    {"tbmm": {"tile_sizes": [16, 32, 64], "thread_shape": [16, 8, 1]}, "MLP3": {"tile_sizes": [4, 4, 1]}},
+    {"tbmm": {"tile_sizes": [32, 32, 64], "thread_shape": [8, 16, 1]}, "MLP3": {"tile_sizes": [4, 4, 1]}},
+    {"tbmm": {"tile_sizes": [32, 32, 72]}, "MLP3": {"tile_sizes": [4, 4, 1]}},
+    {"tbmm": {"tile_sizes": [32, 32, 64], "unroll_copy_shared": True}, "MLP3": {"tile_sizes": [4, 4, 1]}},
+]
+
+VARIANTS = {
+    "2FCRelu": [None, {"tile_sizes": [8, 8, 1], "block_shape": [128, 1, 1]}, {"tile_sizes": [8, 16, 1]},
+                {"tile_sizes": [16, 16, 1], "block_shape": [128, 1, 1]}, {"tile_sizes": [8, 4, 1], "block_shape": [256, 1, 1]}],
+    "tbmm": [None, {"tile_sizes": [32, 32, 64]}, {"tile_sizes": [16, 32, 32], "thread_shape": [16, 8, 1]},
+             {"tile_sizes": [32, 32, 32], "thread_shape": [8, 16, 1]}],
+    "MLP3": [None, {"tile_sizes": [4, 4, 1]}, {"tile_sizes": [2, 2, 1]}],
+}
+
+
+def main():
+    ee = ExecutionEngine()
+    dev = torch.device("cuda", 0)
+    ops = {n: bench.OpInstance(ee, torch, n, s, sd, NSTEP, dev, 1 + i) for i, (n, s, sd) in enumerate(bench.STEP_OPS)}
+    main_s = torch.cuda.Stream()
+    side = [torch.cuda.Stream() for _ in range(3)]
+
+    def graph_of(group):
+        def body():
+            for k in range(NSTEP):
+                for sd in side[:len(group)]:
+                    sd.wait_stream(main_s)
+                for o, sd in zip(group, side):
+                    with torch.cuda.stream(sd):
+                        o.run(k)
+                for sd in side[:len(group)]:
+                    main_s.wait_stream(sd)
+        with torch.cuda.stream(main_s):
+            body()
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=main_s):
+                body()
+        return g
+
+    def timeit(g, n=40):
+        with torch.cuda.stream(main_s):
+            for _ in range(3):
+                g.replay()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(main_s)
+            for _ in range(n):
+                g.replay()
+            e1.record(main_s)
+            e1.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / (n * NSTEP)
+
+    base = {n: o.handle for n, o in ops.items()}
+    g0 = graph_of(list(ops.values()))
+    print(f"default step {min(timeit(g0) for _ in range(8)):.2f} us", flush=True)
+    for combo in COMBOS:
+        try:
+            for name, v in combo.items():
+                o = ops[name]
+                o.handle = ee.compile(name, o.sets[0][0], o.sets[0][1],
+                                      dict(ee.default_options(name, o.sets[0][0], o.sets[0][1]), **v))
+            gs = graph_of(list(ops.values()))
+            step = min(timeit(gs) for _ in range(8))
+            print(json.dumps({"combo": combo, "kernels": {n: ee.describe(o.handle)["kernel"] for n, o in ops.items()},
+                              "step_us": round(step, 3)}), flush=True)
+        except Exception as e:
+            print(json.dumps({"combo": combo, "error": f"{type(e).__name__}: {e}"[:120]}), flush=True)
+        for n, o in ops.items():
+            o.handle = base[n]
+    if os.environ.get("COMBOS_ONLY"):
+        return
+    for name, vs in VARIANTS.items():
+        o = ops[name]
+        for v in vs:
+            try:
+                o.handle = base[name] if v is None else ee.compile(
+                    name, o.sets[0][0], o.sets[0][1], dict(ee.default_options(name, o.sets[0][0], o.sets[0][1]), **v))
+                kern = ee.describe(o.handle)["kernel"]
+                ga, gs = graph_of([o]), graph_of(list(ops.values()))
+                alone = min(timeit(ga) for _ in range(3))
+                step = min(timeit(gs) for _ in range(5))
+                print(json.dumps({"op": name, "opts": v, "kernel": kern, "alone_us": round(alone, 3),
+                                  "step_us": round(step, 3)}), flush=True)
+            except Exception as e:  # a plan the op rejects
+                print(json.dumps({"op": name, "opts": v, "error": f"{type(e).__name__}: {e}"[:120]}), flush=True)
+        o.handle = base[name]
+
+
+if __name__ == "__main__":
+    main()
