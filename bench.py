@@ -685,7 +685,7 @@ def prod_model_line(ee, torch, dev):
         out = {"us_per_forward": round(us, 3), "blocks_us_per_forward": [round(b, 2) for b in blocks],
                "gflops": round(m.flops / us / 1e3, 1),
                "us_p0_p50_p90_sync": [round(lat[0] * 1e6, 1), round(lat[50] * 1e6, 1), round(lat[90] * 1e6, 1)],
-               "kernels": m.kernels, "graph": "2LUT || C3 (tmm def, from zeros) -> concat -> MLP1 -> MLP3, one CUDA graph",
+               "kernels": m.kernels, "graph": "C3 (tmm def, from zeros) -> 2LUT -> concat -> MLP1 -> MLP3, one CUDA graph on one stream",
                "sizes": S}
         del m, p
         torch.cuda.empty_cache()

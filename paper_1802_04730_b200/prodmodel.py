@@ -11,8 +11,9 @@ CUDA graph over the tc-b200 kernels:
 At the paper's sizes (E=1e7, D=64, L=50, B=128, WX=1024, WY=1000) the concat
 width is 64+64+1000 = 1128, MLP1's input (mlp1.tc). The paper's motivation
 for fusing is launch overhead in this low-latency
-regime; here every launch of the chain is captured once and replayed: 2LUT
-and C3 fork onto two streams, the C3 zero-fill, concat, MLP1 and MLP3 follow.
+regime; here every launch of the chain is captured once and replayed: C3
+(from zeros, as the tmm def), 2LUT, concat, MLP1 and MLP3 on one stream
+(`fork=True` puts C3 beside 2LUT on a side stream; see __init__).
 Each operator is the FFMA-exact kernel of its TC definition, so the chain's
 outputs are bit-identical to evaluating the defs one after another on the
 reference interpreter (tests/test_prodmodel.py).
@@ -35,9 +36,14 @@ class ProductionModel:
     Outputs (allocated here): C1, C2, C3, I, O1, O2, O3, O4.
     """
 
-    def __init__(self, ee, params: dict, math: str = "ffma"):
+    def __init__(self, ee, params: dict, math: str = "ffma", fork: bool = False):
         import torch
         self.torch, self.ee = torch, ee
+        # fork=True puts C3 on a side stream beside 2LUT. Measured on B200 the
+        # forked graph is bimodal per block of replays (41.5 or 67.6 us per
+        # forward: C3's CTAs placed beside 2LUT's run slow); one stream is a
+        # steady 41.0 us (profiles/r01_prodmodel_probe.txt), so it is the default
+        self.fork = fork
         p = self.p = params
         dev = p["I3"].device
         B, D = p["I1"].shape[0], p["LUT1"].shape[1]
@@ -73,12 +79,14 @@ class ProductionModel:
         """Every launch of one forward pass on self.stream (+ the side stream)."""
         torch, ee, p, o = self.torch, self.ee, self.p, self.out
         s = self.stream
-        self.side.wait_stream(s)
-        with torch.cuda.stream(self.side):  # C3 onto a fresh zero return (the tmm def: zero-init chain)
-            ee.run(self.h_c3, [p["I3"], p["W"]], [o["C3"]], stream=self.side.cuda_stream, check_errors=False)
+        c3s = self.side if self.fork else s
+        c3s.wait_stream(s)
+        with torch.cuda.stream(c3s):  # C3 onto a fresh zero return (the tmm def: zero-init chain)
+            ee.run(self.h_c3, [p["I3"], p["W"]], [o["C3"]], stream=c3s.cuda_stream, check_errors=False)
         ee.run(self.h_lut, [p["LUT1"], p["I1"], p["LUT2"], p["I2"]], [o["C1"], o["C2"]], stream=s.cuda_stream,
                check_errors=check_errors)
-        s.wait_stream(self.side)
+        if self.fork:
+            s.wait_stream(self.side)
         self._concat(s)
         ee.run(self.h_mlp1, [o["I"], p["W1"], p["B1"]], [o["O1"]], stream=s.cuda_stream, check_errors=False)
         ee.run(self.h_mlp3, [o["O1"], p["W2"], p["B2"], p["W3"], p["B3"], p["W4"], p["B4"]],

@@ -30,7 +30,7 @@ def main():
              I3=r(S["B"], S["WX"]), W=r(S["WY"], S["WX"]), W1=r(S["N"], 2 * S["D"] + S["WY"]), B1=r(S["N"]),
              W2=r(S["O"], S["N"]), B2=r(S["O"]), W3=r(S["P"], S["O"]), B3=r(S["P"]), W4=r(S["Q"], S["P"]),
              B4=r(S["Q"]))
-    m = ProductionModel(ee, p)
+    m = ProductionModel(ee, p, fork=bool(os.environ.get("PM_FORK")))
     print({k: v for k, v in m.kernels.items()}, flush=True)
     if os.environ.get("EAGER"):
         for _ in range(5):
