@@ -16,13 +16,15 @@ from paper_1802_04730_b200 import ExecutionEngine  # noqa: E402
 
 NSTEP = int(os.environ.get("NSTEP", "26"))
 
-COMBOS = [
-    {"tbmm": {"tile_sizes": [32, 32, 64]}, "MLP3": {"tile_sizes": [4, 4, 1]}},
-    {"tbmm": {"tile_sizes": [32, 32, 64]}, "MLP3": {"tile_sizes": [2, 2, 1]}},
-    {"tbmm": {"tile_sizes": [16, 32, 64], "thread_shape": [16, 8, 1]}, "MLP3": {"tile_sizes": [4, 4, 1]}},
-    {"tbmm": {"tile_sizes": [32, 32, 64], "thread_shape": [8, 16, 1]}, "MLP3": {"tile_sizes": [4, 4, 1]}},
-    {"tbmm": {"tile_sizes": [32, 32, 72]}, "MLP3": {"tile_sizes": [4, 4, 1]}},
-    {"tbmm": {"tile_sizes": [32, 32, 64], "unroll_copy_shared": True}, "MLP3": {"tile_sizes": [4, 4, 1]}},
+COMBOS = [  # (round-1 second pass: TBMM plans beside the current defaults)
+    {"tbmm": {"tile_sizes": [2, 2, 1]}},
+    {"tbmm": {"tile_sizes": [1, 1, 1]}},
+    {"tbmm": {"tile_sizes": [2, 1, 1]}},
+    {"tbmm": {"tile_sizes": [2, 2, 1], "block_shape": [296, 1, 1]}},
+    {"tbmm": {"tile_sizes": [2, 2, 1], "block_shape": [500, 1, 1]}},
+    {"tbmm": {"tile_sizes": [16, 32, 64], "thread_shape": [16, 8, 1], "unroll_copy_shared": True}},
+    {"tbmm": {"tile_sizes": [32, 16, 64], "thread_shape": [8, 16, 1]}},
+    {"tbmm": {"tile_sizes": [32, 32, 128]}},
 ]
 
 VARIANTS = {
