@@ -366,6 +366,86 @@ __global__ void __launch_bounds__(512) gemm_nt_batched(const GemmArgs a, const i
   }
 }
 
+// "Slab" GEMM for many small batches (TBMM: 500 x (26x72 · 72x26)). One CTA
+// owns one batch (or a row/column tile of it). Lane j of a warp owns output
+// column n = n0 + j and holds B row n (K floats, up to 4*KR4) in registers,
+// read once straight from global; warp g owns CH output rows and streams
+// their A rows from shared memory, where every lane reads the same address
+// (a broadcast: one wavefront per 4 reduction steps for the whole warp).
+// So each A value fetched from shared memory feeds 32 FFMAs, and the kernel
+// is bound by the FFMA pipe rather than by shared-memory wavefronts (the
+// tiled kernel's 2x2 micro-tiles need one wavefront per 4 FFMAs). A whole
+// batch is ~15 KB, so every CTA of the paper shape is resident in one wave
+// (the tiled kernel's 69.6 KB stages left a 56-CTA second wave).
+// Each output is one thread's sequential FFMA chain in ascending k from its
+// init value, as in gemm_nt_tiled.
+template <int KR4, int CH>
+__global__ void __launch_bounds__(256) gemm_nt_slab(const GemmArgs a, const int ng) {
+  extern __shared__ __align__(16) float smem[];  // A rows of the tile: [ng*CH][K]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = warp % ng, lb = warp / ng;
+  const int MT = ng * CH;
+  const int m0 = blockIdx.y * MT, b = blockIdx.x;
+  const int n = blockIdx.z * (blockDim.x / ng) + lb * 32 + lane;
+  const int K4 = a.K >> 2;
+  const float* A = a.A + (int64_t)b * a.sA;
+  const float* B = a.B + (int64_t)b * a.sB;
+  float* C = a.C + (int64_t)b * a.sC;
+  const int rowsA = min(MT, a.M - m0);
+
+  // A tile -> shared memory (16-byte cp.async by every thread)
+  for (int e = tid; e < rowsA * K4; e += blockDim.x) {
+    const int r = e / K4, c = e - r * K4;
+    cp_async16(smem + r * a.K + 4 * c, A + (int64_t)(m0 + r) * a.lda + 4 * c, 16);
+  }
+  cp_async_commit();
+  // B row n -> registers (clamped row for lanes past N: computed, not stored)
+  const float4* Brow = reinterpret_cast<const float4*>(B + (int64_t)min(n, a.N - 1) * a.ldb);
+  float4 br[KR4];
+#pragma unroll
+  for (int q = 0; q < KR4; ++q) br[q] = q < K4 ? __ldg(Brow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int m = m0 + g * CH + c;
+    acc[c] = (m < a.M && n < a.N) ? initValue(a, C, m, n) : 0.0f;
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+
+  const unsigned aS = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  unsigned rowAddr[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) rowAddr[c] = aS + (unsigned)(min(g * CH + c, rowsA - 1) * a.K) * 4u;
+#pragma unroll
+  for (int q = 0; q < KR4; ++q) {
+    if (q < K4) {  // warp-uniform
+      float4 av[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) av[c] = ldsV4(rowAddr[c] + q * 16);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].x, br[q].x, acc[c]);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].y, br[q].y, acc[c]);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].z, br[q].z, acc[c]);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].w, br[q].w, acc[c]);
+    }
+  }
+  if (n < a.N) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int m = m0 + g * CH + c;
+      if (m < a.M) {
+        float v = acc[c];
+        if (a.relu) v = fmaxf(v, 0.0f);
+        C[(int64_t)m * a.ldc + n] = v;
+      }
+    }
+  }
+}
+
 int batchedLd(int K) {
   int l = (K + 3) & ~3;
   while (l % 32 != 4) l += 4;
@@ -404,6 +484,11 @@ const GemmVariant kGemmVariants[] = {
     {26, 16, 64, 2, 4, 64, "t16x64_r2x4_k64", 4},
     {27, 16, 32, 2, 2, 64, "t16x32_r2x2_k64_s8", 8},
     {28, 32, 16, 2, 2, 64, "t32x16_r2x2_k64", 4},
+    // slab: one CTA per batch, B rows in registers, A rows broadcast from
+    // shared memory (tk = -1; rm = output rows per warp)
+    {29, 0, 0, 4, 1, -1, "slab_c4", 0},
+    {30, 0, 0, 7, 1, -1, "slab_c7", 0},
+    {31, 0, 0, 13, 1, -1, "slab_c13", 0},
 };
 
 template <int RM, int RN>
@@ -431,15 +516,40 @@ cudaError_t launchBatched(const GemmArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+
+// slab kernel dispatch: KR4 = register float4s per B row (K <= 4*KR4)
+template <int CH>
+cudaError_t launchSlabCh(const GemmArgs& a, cudaStream_t s) {
+  // warps per lane block: enough row groups to cover M (<= 8), then as many
+  // 32-column lane blocks as fit in 256 threads
+  int ng = std::min(8, (a.M + CH - 1) / CH);
+  int nbMax = std::max(1, 8 / ng);
+  int nb = std::min(nbMax, (a.N + 31) / 32);
+  dim3 grid(a.batch, (a.M + ng * CH - 1) / (ng * CH), (a.N + 32 * nb - 1) / (32 * nb));
+  const int threads = ng * nb * 32;
+  const size_t smem = (size_t)ng * CH * a.K * 4;
+  void (*kfn)(GemmArgs, int);
+  if (a.K <= 32) kfn = gemm_nt_slab<8, CH>;
+  else if (a.K <= 72) kfn = gemm_nt_slab<18, CH>;
+  else kfn = gemm_nt_slab<32, CH>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kfn<<<grid, threads, smem, s>>>(a, ng);
+  return cudaGetLastError();
+}
+
 template <int TM, int TN, int RM, int RN, int TK, int S = 4>
 cudaError_t launchTiled(const GemmArgs& a, int vec, cudaStream_t s) {
   dim3 grid((a.N + TN - 1) / TN, (a.M + TM - 1) / TM, a.batch);
   const size_t smem = (size_t)S * (TM + TN) * (TK + 4) * sizeof(float);
   auto kfn = gemm_nt_tiled<TM, TN, RM, RN, TK, S>;
-  static bool attr = false;  // per instantiation
-  if (!attr) {
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  // set on every launch: the attribute is per device context, and a cached
+  // per-process flag would leave other devices at the 48 KB default
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
   }
   kfn<<<grid, (TM / RM) * (TN / RN), smem, s>>>(a, vec);
   return cudaGetLastError();
@@ -448,6 +558,12 @@ cudaError_t launchTiled(const GemmArgs& a, int vec, cudaStream_t s) {
 }  // namespace
 
 int gemmVariantCount() { return sizeof(kGemmVariants) / sizeof(kGemmVariants[0]); }
+
+bool slabOk(const GemmArgs& a) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return a.K > 0 && a.K % 4 == 0 && a.K <= 128 && a.lda % 4 == 0 && a.ldb % 4 == 0 && a.sA % 4 == 0 &&
+         a.sB % 4 == 0 && al16(a.A) && al16(a.B) && a.batch <= 65535 * 1024;
+}
 
 bool batchedOk(const GemmArgs& a) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -492,6 +608,14 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
     case 26: return launchTiled<16, 64, 2, 4, 64, 4>(a, vec, s);
     case 27: return launchTiled<16, 32, 2, 2, 64, 8>(a, vec, s);
     case 28: return launchTiled<32, 16, 2, 2, 64, 4>(a, vec, s);
+    case 29:
+    case 30:
+    case 31: {
+      if (!slabOk(a)) return cudaErrorInvalidValue;
+      if (variant == 29) return launchSlabCh<4>(a, s);
+      if (variant == 30) return launchSlabCh<7>(a, s);
+      return launchSlabCh<13>(a, s);
+    }
     case 19:
     case 20:
     case 21:

@@ -46,6 +46,9 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
 // whether the persistent batched variants can take this problem (16-byte
 // rows/strides/pointers, one batch's operands fit a shared-memory stage)
 bool batchedOk(const GemmArgs& a);
+// whether the slab variants (tk == -1) can take this problem: K % 4 == 0,
+// K <= 128 (a B row lives in registers), 16-byte rows/strides/pointers
+bool slabOk(const GemmArgs& a);
 
 // ------------------------------------------------- GEMM-NT, tensor cores
 // tcgen05 .kind::tf32 variant of the same contraction (tc_gemm.cu). Not

@@ -155,6 +155,21 @@ void decodeGemm(const MappingOptions& o, Mapping& m) {
     }
     invalid("persistent batched GEMM micro-tile must be 1x1, 1x2, 2x1 or 2x2");
   }
+  if (o.tileSizes[2] == 2) {
+    // reduction depth 2 = the slab kernel (one CTA per batch, B rows in
+    // registers, A rows broadcast from shared memory); tile_sizes[0] = output
+    // rows per warp
+    const int ch = static_cast<int>(o.tileSizes[0]);
+    for (int i = 1; i < k::gemmVariantCount(); ++i) {
+      const auto& v = k::gemmVariant(i);
+      if (v.tk == -1 && v.rm == ch) {
+        m.gemmVariant = i;
+        m.gemmThreads = 0;
+        return;
+      }
+    }
+    invalid("slab GEMM rows per warp must be 4, 7 or 13");
+  }
   if (o.threadShape[2] != 1) invalid("tiled GEMM uses a 2-D thread block");
   int64_t tm = o.tileSizes[0], tn = o.tileSizes[1], tk = o.tileSizes[2];
   int64_t tx = o.threadShape[0], ty = o.threadShape[1];
@@ -197,9 +212,11 @@ void launchGemmDesc(const GemmDesc& g, const Mapping& m, void* const* in, void* 
     if (!k::tcGemmSupported(a, &why)) fail(ErrorKind::MappingInvalid, why);
     k::TcPlan pl = m.tcAuto ? k::tcGemmPlan(g.batch, g.M, g.N, g.K, smCount()) : m.tc;
     e = k::launchTcGemm(a, m.math, pl, s);
-  } else if (k::gemmVariant(m.gemmVariant).tk == 0 && !k::batchedOk(a)) {
-    // the persistent batched kernel needs 16-byte aligned operands; the
-    // tiled kernel computes the same bit-exact chains without that need
+  } else if ((k::gemmVariant(m.gemmVariant).tk == 0 && !k::batchedOk(a)) ||
+             (k::gemmVariant(m.gemmVariant).tk == -1 && !k::slabOk(a))) {
+    // the persistent batched and slab kernels need 16-byte aligned operands
+    // (and the slab K <= 128); the tiled kernel computes the same bit-exact
+    // chains without that need
     e = k::launchGemm(a, 4, 256, s);
   } else {
     e = k::launchGemm(a, m.gemmVariant, m.gemmThreads, s);
@@ -250,7 +267,9 @@ std::string Mapping::describe() const {
   }
   switch (family) {
     case Family::Gemm:
-      if (k::gemmVariant(gemmVariant).tk == 0)
+      if (k::gemmVariant(gemmVariant).tk == -1)
+        os << k::gemmVariant(gemmVariant).name;
+      else if (k::gemmVariant(gemmVariant).tk == 0)
         os << k::gemmVariant(gemmVariant).name << " grid=" << (gemmThreads ? std::to_string(gemmThreads) : "auto");
       else
         os << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
@@ -550,13 +569,11 @@ MappingOptions defaultOptions(const Problem& p, int math) {
 
       auto ctas = [&](int tm, int tn) { return (double)g.batch * ((g.M + tm - 1) / tm) * ((g.N + tn - 1) / tn); };
       o.unrollCopyShared = g.K > 128;
-      if (g.K > 32 && g.K <= 128 && ctas(32, 32) >= 2 * 148) {
-        // short reductions over many tiles (TBMM 500 x 26x26x72): two k
-        // stages instead of three. Slower alone (8.4 -> 9.6 us) but its CTAs
-        // overlap the FC chains of the bench step far better (step 19.5 ->
-        // 18.0 us, profiles/r01_step_variants.txt)
-        o.tileSizes = {32, 32, 64};
-        o.threadShape = {{16, 16, 1}};
+      if (g.batch > 1 && g.K % 4 == 0 && g.K <= 128 && g.M <= 64 && g.N <= 256) {
+        // many small batches (TBMM 500 x 26x26x72): the slab kernel, one
+        // CTA per batch, 7 output rows per warp
+        o.tileSizes = {g.M <= 16 ? 4 : 7, 1, 2};
+        o.threadShape = {{32, 1, 1}};
         o.unrollCopyShared = false;
         break;
       }
@@ -704,9 +721,9 @@ GenePools genePools(const Problem& p, int math) {
       g.tile1 = {16, 32, 64};
       g.tile2 = {16, 32, 64};
       if (p.family == Family::Gemm && p.gemm.batch > 1) {  // + the persistent batched kernel
-        g.tile0 = {1, 2, 16, 32, 64};
+        g.tile0 = {1, 2, 4, 7, 13, 16, 32, 64};
         g.tile1 = {1, 2, 16, 32, 64};
-        g.tile2 = {1, 16, 32, 64};
+        g.tile2 = {1, 2, 16, 32, 64};  // 1 = persistent batched, 2 = slab
       }
       g.tx = {4, 8, 16, 32};
       g.ty = {4, 8, 16, 32};
