@@ -12,5 +12,19 @@ for n, dt in [(1 << 30, torch.bfloat16), (1 << 29, torch.float32), (53 << 20, to
         e0.record(); b.copy_(a); e1.record(); e1.synchronize(); best = min(best, e0.elapsed_time(e1))
     by = 2 * n * a.element_size()
     print("torch copy %s %d MB: %.1f us %.1f GB/s (single pair, back to back)" % (dt, by >> 20, best * 1e3, by / best / 1e6))
+    for nsets in (1, 2):
+        src = [a] + [torch.empty_like(a).uniform_() for _ in range(nsets - 1)]
+        dst = [b] + [torch.empty_like(b) for _ in range(nsets - 1)]
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for i in range(8):
+                    dst[i % nsets].copy_(src[i % nsets])
+            g.replay(); torch.cuda.synchronize()
+            e0.record(s); g.replay(); e1.record(s); e1.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / 8
+        print("   graph of 8 copies over %d pair(s): %.1f us %.1f GB/s" % (nsets, us, by / us / 1e3))
+        del src, dst, g
 PY
 cat $OUT/read_floor.txt
