@@ -90,6 +90,65 @@ __global__ void flat_k(const float4* X, const float4* Y, float* Z, int n4) {
   for (int e = tid; e < NB * OUTF; e += T) Z[e] = acc;
 }
 
+
+// the slab TBMM kernel (gemm.cu gemm_nt_slab<18,CH>) with stages switched
+// off: mode 0 = loads only, 1 = loads + chains, 2 = chains without the
+// B-row LDG (B from smem)
+template <int CH>
+__global__ void __launch_bounds__(256) slab_k(const float* X, const float* Y, float* Z, int mode) {
+  __shared__ __align__(16) float sA[26 * 72];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ng = blockDim.x / 32, g = warp;
+  const int b = blockIdx.x, n = lane, K4 = 18;
+  const float* A = X + (size_t)b * ROWF;
+  const float* B = Y + (size_t)b * ROWF;
+  for (int e = tid; e < 26 * K4; e += blockDim.x) {
+    unsigned d = (unsigned)__cvta_generic_to_shared(sA + 4 * e);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(A + 4 * e));
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  const float4* Brow = reinterpret_cast<const float4*>(B + (size_t)min(n, 25) * 72);
+  float4 br[18];
+#pragma unroll
+  for (int q = 0; q < 18; ++q) br[q] = __ldg(Brow + q);
+  float acc[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc[c] = 0.f;
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  if (mode == 1) {
+    const unsigned aS = (unsigned)__cvta_generic_to_shared(sA);
+    unsigned rowAddr[CH];
+#pragma unroll
+    for (int c = 0; c < CH; ++c) rowAddr[c] = aS + (unsigned)(min(g * CH + c, 25) * 72) * 4u;
+#pragma unroll
+    for (int q = 0; q < 18; ++q) {
+      float4 av[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(av[c].x), "=f"(av[c].y), "=f"(av[c].z), "=f"(av[c].w) : "r"(rowAddr[c] + q * 16));
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].x, br[q].x, acc[c]);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].y, br[q].y, acc[c]);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].z, br[q].z, acc[c]);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].w, br[q].w, acc[c]);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 18; ++q) acc[0] += br[q].x + br[q].y + br[q].z + br[q].w + sA[q * 4 + lane];
+  }
+  if (n < 26) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int m = g * CH + c;
+      if (m < 26) Z[(size_t)b * OUTF + m * 26 + n] = acc[c];
+    }
+  }
+}
+
 int main() {
   std::vector<float*> X(NSET), Y(NSET), Z(NSET);
   for (int i = 0; i < NSET; ++i) {
@@ -141,6 +200,11 @@ int main() {
   timeit("flat U4 592x256", [&](int i) { flat_k<4><<<592, 256, 0, s>>>((float4*)X[i], (float4*)Y[i], Z[i], n4); });
   timeit("flat U2 1184x256", [&](int i) { flat_k<2><<<1184, 256, 0, s>>>((float4*)X[i], (float4*)Y[i], Z[i], n4); });
   timeit("flat U1 2368x256", [&](int i) { flat_k<1><<<2368, 256, 0, s>>>((float4*)X[i], (float4*)Y[i], Z[i], n4); });
+  timeit("slab c7 loads only", [&](int i) { slab_k<7><<<NB, 128, 0, s>>>(X[i], Y[i], Z[i], 0); });
+  timeit("slab c7 full", [&](int i) { slab_k<7><<<NB, 128, 0, s>>>(X[i], Y[i], Z[i], 1); });
+  timeit("slab c13 full", [&](int i) { slab_k<13><<<NB, 64, 0, s>>>(X[i], Y[i], Z[i], 1); });
+  timeit("WARM slab c7 full", [&](int i) { slab_k<7><<<NB, 128, 0, s>>>(X[0], Y[0], Z[0], 1); });
+  timeit("WARM slab c7 loads only", [&](int i) { slab_k<7><<<NB, 128, 0, s>>>(X[0], Y[0], Z[0], 0); });
   // same, warm (one set repeated: L2 resident)
   timeit("WARM cp.async 1 CTA/batch x128", [&](int i) { cpasync_k<<<NB, 128, 0, s>>>(X[0], Y[0], Z[0]); });
   timeit("WARM flat U8 296x512", [&](int i) { flat_k<8><<<296, 512, 0, s>>>((float4*)X[0], (float4*)Y[0], Z[0], n4); });
