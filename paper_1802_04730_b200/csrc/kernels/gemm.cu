@@ -367,70 +367,99 @@ __global__ void __launch_bounds__(512) gemm_nt_batched(const GemmArgs a, const i
 }
 
 // "Slab" GEMM for many small batches (TBMM: 500 x (26x72 · 72x26)). One CTA
-// owns one batch (or a row/column tile of it). Lane j of a warp owns output
-// column n = n0 + j and holds B row n (K floats, up to 4*KR4) in registers,
-// read once straight from global; warp g owns CH output rows and streams
-// their A rows from shared memory, where every lane reads the same address
-// (a broadcast: one wavefront per 4 reduction steps for the whole warp).
-// So each A value fetched from shared memory feeds 32 FFMAs, and the kernel
-// is bound by the FFMA pipe rather than by shared-memory wavefronts (the
-// tiled kernel's 2x2 micro-tiles need one wavefront per 4 FFMAs). A whole
-// batch is ~15 KB, so every CTA of the paper shape is resident in one wave
-// (the tiled kernel's 69.6 KB stages left a 56-CTA second wave).
+// owns one batch (or a row/column tile of it); the whole tile's operands
+// are in flight from the first cycle, by 16-byte cp.async from every thread,
+// in NCH reduction chunks of CQ float4s, one commit group per chunk, so the
+// chains of chunk c run while chunks > c are still arriving. Lane j of a
+// warp owns output column n = n0 + j: it moves its B row's chunk from shared
+// memory into registers (rows padded to an odd number of 16-byte units, so
+// eight lanes' float4 reads hit eight bank groups). Warp g owns CH output
+// rows and streams their A rows from shared memory, where every lane reads
+// the same address (a broadcast: one wavefront per 4 reduction steps for the
+// whole warp), so each A value fetched feeds 32 FFMAs. A batch is ~15 KB:
+// every CTA of the paper shape is resident in one wave.
 // Each output is one thread's sequential FFMA chain in ascending k from its
 // init value, as in gemm_nt_tiled.
-template <int KR4, int CH>
+constexpr int kSlabCq = 6;  // float4s per reduction chunk (24 k steps)
+
+template <int CH>
 __global__ void __launch_bounds__(256) gemm_nt_slab(const GemmArgs a, const int ng) {
-  extern __shared__ __align__(16) float smem[];  // A rows of the tile: [ng*CH][K]
+  extern __shared__ __align__(16) float smem[];
+  constexpr int CQ = kSlabCq;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = warp % ng, lb = warp / ng;
-  const int MT = ng * CH;
-  const int m0 = blockIdx.y * MT, b = blockIdx.x;
-  const int n = blockIdx.z * (blockDim.x / ng) + lb * 32 + lane;
+  const int MT = ng * CH, NT = blockDim.x / ng;  // tile rows / columns
+  const int m0 = blockIdx.y * MT, n0 = blockIdx.z * NT, b = blockIdx.x;
+  const int n = n0 + lb * 32 + lane;
   const int K4 = a.K >> 2;
+  const int ldA = K4, ldB = K4 | 1;  // row strides in float4s
   const float* A = a.A + (int64_t)b * a.sA;
   const float* B = a.B + (int64_t)b * a.sB;
   float* C = a.C + (int64_t)b * a.sC;
-  const int rowsA = min(MT, a.M - m0);
+  const int rowsA = min(MT, a.M - m0), rowsB = min(NT, a.N - n0);
+  float4* As = reinterpret_cast<float4*>(smem);  // [MT][ldA]
+  float4* Bs = As + MT * ldA;                    // [NT][ldB]
 
-  // A tile -> shared memory (16-byte cp.async by every thread)
-  for (int e = tid; e < rowsA * K4; e += blockDim.x) {
-    const int r = e / K4, c = e - r * K4;
-    cp_async16(smem + r * a.K + 4 * c, A + (int64_t)(m0 + r) * a.lda + 4 * c, 16);
+  // every chunk's copies issued up front, one commit group per chunk
+  const int nch = (K4 + CQ - 1) / CQ;
+  for (int c = 0; c < nch; ++c) {
+    const int q0 = c * CQ, cq = min(CQ, K4 - q0);
+    for (int e = tid; e < (rowsA + rowsB) * cq; e += blockDim.x) {
+      const int r = e / cq, q = q0 + e - r * cq;
+      if (r < rowsA)
+        cp_async16(As + r * ldA + q, A + (int64_t)(m0 + r) * a.lda + 4 * q, 16);
+      else
+        cp_async16(Bs + (r - rowsA) * ldB + q, B + (int64_t)(n0 + r - rowsA) * a.ldb + 4 * q, 16);
+    }
+    cp_async_commit();
   }
-  cp_async_commit();
-  // B row n -> registers (clamped row for lanes past N: computed, not stored)
-  const float4* Brow = reinterpret_cast<const float4*>(B + (int64_t)min(n, a.N - 1) * a.ldb);
-  float4 br[KR4];
-#pragma unroll
-  for (int q = 0; q < KR4; ++q) br[q] = q < K4 ? __ldg(Brow + q) : make_float4(0.f, 0.f, 0.f, 0.f);
   float acc[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     const int m = m0 + g * CH + c;
     acc[c] = (m < a.M && n < a.N) ? initValue(a, C, m, n) : 0.0f;
   }
-  cp_async_wait<0>();
-  __syncthreads();
-
-  const unsigned aS = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const unsigned aS = static_cast<unsigned>(__cvta_generic_to_shared(As));
+  const unsigned bS = static_cast<unsigned>(__cvta_generic_to_shared(Bs + min(lb * 32 + lane, rowsB - 1) * ldB));
   unsigned rowAddr[CH];
 #pragma unroll
-  for (int c = 0; c < CH; ++c) rowAddr[c] = aS + (unsigned)(min(g * CH + c, rowsA - 1) * a.K) * 4u;
+  for (int c = 0; c < CH; ++c) rowAddr[c] = aS + (unsigned)(min(g * CH + c, rowsA - 1) * ldA) * 16u;
+
+  for (int c = 0; c < nch; ++c) {
+    switch (nch - 1 - c) {  // this thread's copies of chunks <= c have landed
+      case 0: cp_async_wait<0>(); break;
+      case 1: cp_async_wait<1>(); break;
+      case 2: cp_async_wait<2>(); break;
+      case 3: cp_async_wait<3>(); break;
+      case 4: cp_async_wait<4>(); break;
+      default: cp_async_wait<5>(); break;
+    }
+    __syncthreads();  // ... and everyone's
+    const int q0 = c * CQ, cq = min(CQ, K4 - q0);
+    float4 br[CQ];
 #pragma unroll
-  for (int q = 0; q < KR4; ++q) {
-    if (q < K4) {  // warp-uniform
-      float4 av[CH];
+    for (int q = 0; q < CQ; ++q)
+      if (q < cq) br[q] = ldsV4(bS + (q0 + q) * 16);
+    float4 av[2][CH];
 #pragma unroll
-      for (int c = 0; c < CH; ++c) av[c] = ldsV4(rowAddr[c] + q * 16);
+    for (int r = 0; r < CH; ++r) av[0][r] = ldsV4(rowAddr[r] + q0 * 16);
 #pragma unroll
-      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].x, br[q].x, acc[c]);
+    for (int q = 0; q < CQ; ++q) {
+      if (q < cq) {  // warp-uniform
+        if (q + 1 < cq) {  // next group's A values before this group's FFMAs
 #pragma unroll
-      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].y, br[q].y, acc[c]);
+          for (int r = 0; r < CH; ++r) av[(q + 1) & 1][r] = ldsV4(rowAddr[r] + (q0 + q + 1) * 16);
+        }
+        const float4* v = av[q & 1];
 #pragma unroll
-      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].z, br[q].z, acc[c]);
+        for (int r = 0; r < CH; ++r) acc[r] = __fmaf_rn(v[r].x, br[q].x, acc[r]);
 #pragma unroll
-      for (int c = 0; c < CH; ++c) acc[c] = __fmaf_rn(av[c].w, br[q].w, acc[c]);
+        for (int r = 0; r < CH; ++r) acc[r] = __fmaf_rn(v[r].y, br[q].y, acc[r]);
+#pragma unroll
+        for (int r = 0; r < CH; ++r) acc[r] = __fmaf_rn(v[r].z, br[q].z, acc[r]);
+#pragma unroll
+        for (int r = 0; r < CH; ++r) acc[r] = __fmaf_rn(v[r].w, br[q].w, acc[r]);
+      }
     }
   }
   if (n < a.N) {
@@ -527,11 +556,9 @@ cudaError_t launchSlabCh(const GemmArgs& a, cudaStream_t s) {
   int nb = std::min(nbMax, (a.N + 31) / 32);
   dim3 grid(a.batch, (a.M + ng * CH - 1) / (ng * CH), (a.N + 32 * nb - 1) / (32 * nb));
   const int threads = ng * nb * 32;
-  const size_t smem = (size_t)ng * CH * a.K * 4;
-  void (*kfn)(GemmArgs, int);
-  if (a.K <= 32) kfn = gemm_nt_slab<8, CH>;
-  else if (a.K <= 72) kfn = gemm_nt_slab<18, CH>;
-  else kfn = gemm_nt_slab<32, CH>;
+  const int K4 = a.K / 4;
+  const size_t smem = ((size_t)ng * CH * K4 + (size_t)32 * nb * (K4 | 1)) * 16;
+  auto kfn = gemm_nt_slab<CH>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -561,7 +588,7 @@ int gemmVariantCount() { return sizeof(kGemmVariants) / sizeof(kGemmVariants[0])
 
 bool slabOk(const GemmArgs& a) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  return a.K > 0 && a.K % 4 == 0 && a.K <= 128 && a.lda % 4 == 0 && a.ldb % 4 == 0 && a.sA % 4 == 0 &&
+  return a.K > 0 && a.K % 4 == 0 && a.K <= 4 * 6 * kSlabCq && a.lda % 4 == 0 && a.ldb % 4 == 0 && a.sA % 4 == 0 &&
          a.sB % 4 == 0 && al16(a.A) && al16(a.B) && a.batch <= 65535 * 1024;
 }
 

@@ -47,7 +47,7 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
 // rows/strides/pointers, one batch's operands fit a shared-memory stage)
 bool batchedOk(const GemmArgs& a);
 // whether the slab variants (tk == -1) can take this problem: K % 4 == 0,
-// K <= 128 (a B row lives in registers), 16-byte rows/strides/pointers
+// K <= 144 (at most six 24-step reduction chunks), 16-byte rows/strides/pointers
 bool slabOk(const GemmArgs& a);
 
 // ------------------------------------------------- GEMM-NT, tensor cores

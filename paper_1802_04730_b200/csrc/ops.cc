@@ -215,7 +215,7 @@ void launchGemmDesc(const GemmDesc& g, const Mapping& m, void* const* in, void* 
   } else if ((k::gemmVariant(m.gemmVariant).tk == 0 && !k::batchedOk(a)) ||
              (k::gemmVariant(m.gemmVariant).tk == -1 && !k::slabOk(a))) {
     // the persistent batched and slab kernels need 16-byte aligned operands
-    // (and the slab K <= 128); the tiled kernel computes the same bit-exact
+    // (and the slab K <= 144); the tiled kernel computes the same bit-exact
     // chains without that need
     e = k::launchGemm(a, 4, 256, s);
   } else {
@@ -569,7 +569,7 @@ MappingOptions defaultOptions(const Problem& p, int math) {
 
       auto ctas = [&](int tm, int tn) { return (double)g.batch * ((g.M + tm - 1) / tm) * ((g.N + tn - 1) / tn); };
       o.unrollCopyShared = g.K > 128;
-      if (g.batch > 1 && g.K % 4 == 0 && g.K <= 128 && g.M <= 64 && g.N <= 256) {
+      if (g.batch > 1 && g.K % 4 == 0 && g.K <= 144 && g.M <= 64 && g.N <= 256) {
         // many small batches (TBMM 500 x 26x26x72): the slab kernel, one
         // CTA per batch, 7 output rows per warp
         o.tileSizes = {g.M <= 16 ? 4 : 7, 1, 2};
