@@ -382,6 +382,21 @@ __global__ void __launch_bounds__(512) gemm_nt_batched(const GemmArgs a, const i
 // init value, as in gemm_nt_tiled.
 constexpr int kSlabCq = 6;  // float4s per reduction chunk (24 k steps)
 
+#ifdef TCB_SLAB_TRACE
+// diagnostic build only (profiles/slab_trace.cu): per-CTA globaltimer stamps
+__device__ unsigned long long g_slab_trace[4096][10];
+#define SLAB_STAMP(ev)                                                      \
+  do {                                                                      \
+    unsigned long long t_;                                                  \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_slab_trace[blockIdx.x][ev] = t_; \
+  } while (0)
+#else
+#define SLAB_STAMP(ev) \
+  do {                 \
+  } while (0)
+#endif
+
 template <int CH>
 __global__ void __launch_bounds__(256) gemm_nt_slab(const GemmArgs a, const int ng) {
   extern __shared__ __align__(16) float smem[];
@@ -399,6 +414,7 @@ __global__ void __launch_bounds__(256) gemm_nt_slab(const GemmArgs a, const int 
   const int rowsA = min(MT, a.M - m0), rowsB = min(NT, a.N - n0);
   float4* As = reinterpret_cast<float4*>(smem);  // [MT][ldA]
   float4* Bs = As + MT * ldA;                    // [NT][ldB]
+  SLAB_STAMP(0);
 
   // every chunk's copies issued up front, one commit group per chunk
   const int nch = (K4 + CQ - 1) / CQ;
@@ -413,6 +429,7 @@ __global__ void __launch_bounds__(256) gemm_nt_slab(const GemmArgs a, const int 
     }
     cp_async_commit();
   }
+  SLAB_STAMP(1);
   float acc[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
@@ -435,6 +452,7 @@ __global__ void __launch_bounds__(256) gemm_nt_slab(const GemmArgs a, const int 
       default: cp_async_wait<5>(); break;
     }
     __syncthreads();  // ... and everyone's
+    SLAB_STAMP(2 + min(c, 5));
     const int q0 = c * CQ, cq = min(CQ, K4 - q0);
     float4 br[CQ];
 #pragma unroll
@@ -462,6 +480,7 @@ __global__ void __launch_bounds__(256) gemm_nt_slab(const GemmArgs a, const int 
       }
     }
   }
+  SLAB_STAMP(8);
   if (n < a.N) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
@@ -473,6 +492,7 @@ __global__ void __launch_bounds__(256) gemm_nt_slab(const GemmArgs a, const int 
       }
     }
   }
+  SLAB_STAMP(9);
 }
 
 int batchedLd(int K) {
