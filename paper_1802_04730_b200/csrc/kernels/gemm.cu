@@ -495,6 +495,131 @@ __global__ void __launch_bounds__(256) gemm_nt_slab(const GemmArgs a, const int 
   SLAB_STAMP(9);
 }
 
+// Register-tiled slab: the same one-CTA-per-batch, chunk-pipelined loads as
+// gemm_nt_slab, but each lane owns an RM x RN block of outputs (rows
+// rg + 4i, columns cg + 8j; lane = rg * 8 + cg), so a warp tile is
+// 4*RM x 8*RN (28 x 32 for 7x4: one warp covers a whole 26x26 TBMM batch).
+// Shared-memory reads are what bound the broadcast slab (ncu: a broadcast
+// LDS.128 costs 2 LSU wavefronts, so 7 A rows per 28 FFMAs saturated the
+// LSU pipe and slowed the cp.async fills sharing it); here each 4-step group
+// reads RM A float4s (4 distinct rows per instruction) and RN B float4s (8
+// distinct rows) for 4*RM*RN FFMAs. Row strides are odd in 16-byte units, so
+// consecutive rows fall in distinct bank groups. Each output is one lane's
+// sequential FFMA chain in ascending k from its init value.
+template <int RM, int RN>
+__global__ void __launch_bounds__(256) gemm_nt_slab_rt(const GemmArgs a, const int wm) {
+  extern __shared__ __align__(16) float smem[];
+  constexpr int CQ = kSlabCq;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rg = lane >> 3, cg = lane & 7;
+  const int wr = warp % wm, wc = warp / wm;
+  const int MT = wm * 4 * RM, NT = (blockDim.x >> 5) / wm * 8 * RN;
+  const int m0 = blockIdx.y * MT, n0 = blockIdx.z * NT, b = blockIdx.x;
+  const int K4 = a.K >> 2;
+  const int ld = K4 | 1;  // row stride in float4s (odd)
+  const float* A = a.A + (int64_t)b * a.sA;
+  const float* B = a.B + (int64_t)b * a.sB;
+  float* C = a.C + (int64_t)b * a.sC;
+  const int rowsA = min(MT, a.M - m0), rowsB = min(NT, a.N - n0);
+  float4* As = reinterpret_cast<float4*>(smem);  // [MT][ld]
+  float4* Bs = As + MT * ld;                     // [NT][ld]
+  SLAB_STAMP(0);
+
+  const int nch = (K4 + CQ - 1) / CQ;
+  for (int c = 0; c < nch; ++c) {
+    const int q0 = c * CQ, cq = min(CQ, K4 - q0);
+    for (int e = tid; e < (rowsA + rowsB) * cq; e += blockDim.x) {
+      const int r = e / cq, q = q0 + e - r * cq;
+      if (r < rowsA)
+        cp_async16(As + r * ld + q, A + (int64_t)(m0 + r) * a.lda + 4 * q, 16);
+      else
+        cp_async16(Bs + (r - rowsA) * ld + q, B + (int64_t)(n0 + r - rowsA) * a.ldb + 4 * q, 16);
+    }
+    cp_async_commit();
+  }
+  SLAB_STAMP(1);
+  // this lane's rows / columns inside the CTA tile (clamped for reads)
+  const int rbase = wr * 4 * RM + rg, cbase = wc * 8 * RN + cg;
+  float acc[RM][RN];
+#pragma unroll
+  for (int i = 0; i < RM; ++i)
+#pragma unroll
+    for (int j = 0; j < RN; ++j) {
+      const int m = m0 + rbase + 4 * i, n = n0 + cbase + 8 * j;
+      acc[i][j] = (m < a.M && n < a.N) ? initValue(a, C, m, n) : 0.0f;
+    }
+  const unsigned aS = static_cast<unsigned>(__cvta_generic_to_shared(As));
+  const unsigned bS = static_cast<unsigned>(__cvta_generic_to_shared(Bs));
+  unsigned ra[RM], rb[RN];
+#pragma unroll
+  for (int i = 0; i < RM; ++i) ra[i] = aS + (unsigned)(min(rbase + 4 * i, rowsA - 1) * ld) * 16u;
+#pragma unroll
+  for (int j = 0; j < RN; ++j) rb[j] = bS + (unsigned)(min(cbase + 8 * j, rowsB - 1) * ld) * 16u;
+
+  for (int c = 0; c < nch; ++c) {
+    switch (nch - 1 - c) {
+      case 0: cp_async_wait<0>(); break;
+      case 1: cp_async_wait<1>(); break;
+      case 2: cp_async_wait<2>(); break;
+      case 3: cp_async_wait<3>(); break;
+      case 4: cp_async_wait<4>(); break;
+      default: cp_async_wait<5>(); break;
+    }
+    __syncthreads();
+    SLAB_STAMP(2 + min(c, 5));
+    const int q0 = c * CQ, cq = min(CQ, K4 - q0);
+    float4 av[2][RM], bv[2][RN];
+#pragma unroll
+    for (int i = 0; i < RM; ++i) av[0][i] = ldsV4(ra[i] + q0 * 16);
+#pragma unroll
+    for (int j = 0; j < RN; ++j) bv[0][j] = ldsV4(rb[j] + q0 * 16);
+#pragma unroll
+    for (int q = 0; q < CQ; ++q) {
+      if (q < cq) {  // block-uniform
+        if (q + 1 < cq) {
+#pragma unroll
+          for (int i = 0; i < RM; ++i) av[(q + 1) & 1][i] = ldsV4(ra[i] + (q0 + q + 1) * 16);
+#pragma unroll
+          for (int j = 0; j < RN; ++j) bv[(q + 1) & 1][j] = ldsV4(rb[j] + (q0 + q + 1) * 16);
+        }
+        const float4* x = av[q & 1];
+        const float4* y = bv[q & 1];
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].x, y[j].x, acc[i][j]);
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].y, y[j].y, acc[i][j]);
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].z, y[j].z, acc[i][j]);
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].w, y[j].w, acc[i][j]);
+      }
+    }
+  }
+  SLAB_STAMP(8);
+#pragma unroll
+  for (int i = 0; i < RM; ++i) {
+    const int m = m0 + rbase + 4 * i;
+#pragma unroll
+    for (int j = 0; j < RN; ++j) {
+      const int n = n0 + cbase + 8 * j;
+      if (m < a.M && n < a.N) {
+        float v = acc[i][j];
+        if (a.relu) v = fmaxf(v, 0.0f);
+        C[(int64_t)m * a.ldc + n] = v;
+      }
+    }
+  }
+  SLAB_STAMP(9);
+}
+
 int batchedLd(int K) {
   int l = (K + 3) & ~3;
   while (l % 32 != 4) l += 4;
@@ -538,6 +663,10 @@ const GemmVariant kGemmVariants[] = {
     {29, 0, 0, 4, 1, -1, "slab_c4", 0},
     {30, 0, 0, 7, 1, -1, "slab_c7", 0},
     {31, 0, 0, 13, 1, -1, "slab_c13", 0},
+    // register-tiled slab (tk = -2): rm x rn outputs per lane
+    {32, 0, 0, 7, 4, -2, "slab_rt7x4", 0},
+    {33, 0, 0, 4, 4, -2, "slab_rt4x4", 0},
+    {34, 0, 0, 4, 2, -2, "slab_rt4x2", 0},
 };
 
 template <int RM, int RN>
@@ -584,6 +713,24 @@ cudaError_t launchSlabCh(const GemmArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   kfn<<<grid, threads, smem, s>>>(a, ng);
+  return cudaGetLastError();
+}
+
+template <int RM, int RN>
+cudaError_t launchSlabRt(const GemmArgs& a, cudaStream_t s) {
+  // warps along M to cover the rows (<= 8), then along N within 8 warps
+  const int wmt = 4 * RM, wnt = 8 * RN;
+  int wm = std::min(8, (a.M + wmt - 1) / wmt);
+  int wn = std::min(std::max(1, 8 / wm), (a.N + wnt - 1) / wnt);
+  dim3 grid(a.batch, (a.M + wm * wmt - 1) / (wm * wmt), (a.N + wn * wnt - 1) / (wn * wnt));
+  const int ld = (a.K / 4) | 1;
+  const size_t smem = (size_t)(wm * wmt + wn * wnt) * ld * 16;
+  auto kfn = gemm_nt_slab_rt<RM, RN>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kfn<<<grid, wm * wn * 32, smem, s>>>(a, wm);
   return cudaGetLastError();
 }
 
@@ -662,6 +809,14 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
       if (variant == 29) return launchSlabCh<4>(a, s);
       if (variant == 30) return launchSlabCh<7>(a, s);
       return launchSlabCh<13>(a, s);
+    }
+    case 32:
+    case 33:
+    case 34: {
+      if (!slabOk(a)) return cudaErrorInvalidValue;
+      if (variant == 32) return launchSlabRt<7, 4>(a, s);
+      if (variant == 33) return launchSlabRt<4, 4>(a, s);
+      return launchSlabRt<4, 2>(a, s);
     }
     case 19:
     case 20:

@@ -159,16 +159,18 @@ void decodeGemm(const MappingOptions& o, Mapping& m) {
     // reduction depth 2 = the slab kernel (one CTA per batch, B rows in
     // registers, A rows broadcast from shared memory); tile_sizes[0] = output
     // rows per warp
-    const int ch = static_cast<int>(o.tileSizes[0]);
+    // (tile_sizes[1] == 1, the broadcast slab) or rows x columns per lane
+    // (tile_sizes[1] > 1, the register-tiled slab)
+    const int ch = static_cast<int>(o.tileSizes[0]), rn = static_cast<int>(o.tileSizes[1]);
     for (int i = 1; i < k::gemmVariantCount(); ++i) {
       const auto& v = k::gemmVariant(i);
-      if (v.tk == -1 && v.rm == ch) {
+      if ((rn == 1 && v.tk == -1 && v.rm == ch) || (rn > 1 && v.tk == -2 && v.rm == ch && v.rn == rn)) {
         m.gemmVariant = i;
         m.gemmThreads = 0;
         return;
       }
     }
-    invalid("slab GEMM rows per warp must be 4, 7 or 13");
+    invalid("slab GEMM micro-tile must be 4x1, 7x1, 13x1 (broadcast) or 7x4, 4x4, 4x2 (register-tiled)");
   }
   if (o.threadShape[2] != 1) invalid("tiled GEMM uses a 2-D thread block");
   int64_t tm = o.tileSizes[0], tn = o.tileSizes[1], tk = o.tileSizes[2];
@@ -213,7 +215,7 @@ void launchGemmDesc(const GemmDesc& g, const Mapping& m, void* const* in, void* 
     k::TcPlan pl = m.tcAuto ? k::tcGemmPlan(g.batch, g.M, g.N, g.K, smCount()) : m.tc;
     e = k::launchTcGemm(a, m.math, pl, s);
   } else if ((k::gemmVariant(m.gemmVariant).tk == 0 && !k::batchedOk(a)) ||
-             (k::gemmVariant(m.gemmVariant).tk == -1 && !k::slabOk(a))) {
+             (k::gemmVariant(m.gemmVariant).tk < 0 && !k::slabOk(a))) {
     // the persistent batched and slab kernels need 16-byte aligned operands
     // (and the slab K <= 144); the tiled kernel computes the same bit-exact
     // chains without that need
@@ -267,7 +269,7 @@ std::string Mapping::describe() const {
   }
   switch (family) {
     case Family::Gemm:
-      if (k::gemmVariant(gemmVariant).tk == -1)
+      if (k::gemmVariant(gemmVariant).tk < 0)
         os << k::gemmVariant(gemmVariant).name;
       else if (k::gemmVariant(gemmVariant).tk == 0)
         os << k::gemmVariant(gemmVariant).name << " grid=" << (gemmThreads ? std::to_string(gemmThreads) : "auto");
@@ -722,7 +724,7 @@ GenePools genePools(const Problem& p, int math) {
       g.tile2 = {16, 32, 64};
       if (p.family == Family::Gemm && p.gemm.batch > 1) {  // + the persistent batched kernel
         g.tile0 = {1, 2, 4, 7, 13, 16, 32, 64};
-        g.tile1 = {1, 2, 16, 32, 64};
+        g.tile1 = {1, 2, 4, 16, 32, 64};
         g.tile2 = {1, 2, 16, 32, 64};  // 1 = persistent batched, 2 = slab
       }
       g.tx = {4, 8, 16, 32};

@@ -18,15 +18,16 @@ NSTEP = int(os.environ.get("NSTEP", "26"))
 
 COMBOS = [  # r02: the slab TBMM plans vs the r01 tiled plans in the step
     {"tbmm": {"tile_sizes": [32, 32, 64], "thread_shape": [16, 16, 1]}},
-    {"tbmm": {"tile_sizes": [4, 1, 2]}},
-    {"tbmm": {"tile_sizes": [13, 1, 2]}},
+    {"tbmm": {"tile_sizes": [7, 1, 2]}},
+    {"tbmm": {"tile_sizes": [7, 4, 2]}},
+    {"tbmm": {"tile_sizes": [4, 4, 2]}},
 ]
 
 VARIANTS = {
     "2FCRelu": [None, {"tile_sizes": [8, 8, 1], "block_shape": [128, 1, 1]}, {"tile_sizes": [8, 16, 1]},
                 {"tile_sizes": [16, 16, 1], "block_shape": [128, 1, 1]}, {"tile_sizes": [8, 4, 1], "block_shape": [256, 1, 1]}],
-    "tbmm": [None, {"tile_sizes": [32, 32, 64], "thread_shape": [16, 16, 1]}, {"tile_sizes": [4, 1, 2]},
-             {"tile_sizes": [13, 1, 2]}],
+    "tbmm": [None, {"tile_sizes": [32, 32, 64], "thread_shape": [16, 16, 1]}, {"tile_sizes": [7, 4, 2]},
+             {"tile_sizes": [4, 4, 2]}],
     "MLP3": [None, {"tile_sizes": [4, 4, 1]}, {"tile_sizes": [2, 2, 1]}],
 }
 
