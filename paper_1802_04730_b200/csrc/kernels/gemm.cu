@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(256) gemm_nt_slab(const GemmArgs a, const int 
 // distinct rows) for 4*RM*RN FFMAs. Row strides are odd in 16-byte units, so
 // consecutive rows fall in distinct bank groups. Each output is one lane's
 // sequential FFMA chain in ascending k from its init value.
-template <int RM, int RN>
+template <int RM, int RN, bool BULK>
 __global__ void __launch_bounds__(256) gemm_nt_slab_rt(const GemmArgs a, const int wm) {
   extern __shared__ __align__(16) float smem[];
   constexpr int CQ = kSlabCq;
@@ -526,16 +526,42 @@ __global__ void __launch_bounds__(256) gemm_nt_slab_rt(const GemmArgs a, const i
   SLAB_STAMP(0);
 
   const int nch = (K4 + CQ - 1) / CQ;
-  for (int c = 0; c < nch; ++c) {
-    const int q0 = c * CQ, cq = min(CQ, K4 - q0);
-    for (int e = tid; e < (rowsA + rowsB) * cq; e += blockDim.x) {
-      const int r = e / cq, q = q0 + e - r * cq;
-      if (r < rowsA)
-        cp_async16(As + r * ld + q, A + (int64_t)(m0 + r) * a.lda + 4 * q, 16);
-      else
-        cp_async16(Bs + (r - rowsA) * ld + q, B + (int64_t)(n0 + r - rowsA) * a.ldb + 4 * q, 16);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Bs + NT * ld);  // BULK: one per chunk
+  if (BULK) {
+    // one bulk copy per (row, chunk) segment, completing on the chunk's
+    // mbarrier: the fills bypass the LSU pipe the chains' shared loads use
+    if (tid == 0) {
+      for (int c = 0; c < nch; ++c) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smemU32(&bars[c])));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      for (int c = 0; c < nch; ++c)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemU32(&bars[c])),
+                     "r"((unsigned)((rowsA + rowsB) * min(CQ, K4 - c * CQ) * 16))
+                     : "memory");
     }
-    cp_async_commit();
+    __syncthreads();
+    if (warp == 0) {
+      for (int e = lane; e < nch * (rowsA + rowsB); e += 32) {
+        const int c = e / (rowsA + rowsB), r = e - c * (rowsA + rowsB);
+        const int q0 = c * CQ;
+        const unsigned bytes = (unsigned)min(CQ, K4 - q0) * 16u;
+        if (r < rowsA)
+          bulkG2S(As + r * ld + q0, A + (int64_t)(m0 + r) * a.lda + 4 * q0, bytes, &bars[c]);
+        else
+          bulkG2S(Bs + (r - rowsA) * ld + q0, B + (int64_t)(n0 + r - rowsA) * a.ldb + 4 * q0, bytes, &bars[c]);
+      }
+    }
+  } else {
+    for (int c = 0; c < nch; ++c) {
+      const int q0 = c * CQ, cq = min(CQ, K4 - q0);
+      for (int e = tid; e < (rowsA + rowsB) * cq; e += blockDim.x) {
+        const int r = e / cq, q = q0 + e - r * cq;
+        if (r < rowsA)
+          cp_async16(As + r * ld + q, A + (int64_t)(m0 + r) * a.lda + 4 * q, 16);
+        else
+          cp_async16(Bs + (r - rowsA) * ld + q, B + (int64_t)(n0 + r - rowsA) * a.ldb + 4 * q, 16);
+      }
+      cp_async_commit();
+    }
   }
   SLAB_STAMP(1);
   // this lane's rows / columns inside the CTA tile (clamped for reads)
@@ -557,15 +583,19 @@ __global__ void __launch_bounds__(256) gemm_nt_slab_rt(const GemmArgs a, const i
   for (int j = 0; j < RN; ++j) rb[j] = bS + (unsigned)(min(cbase + 8 * j, rowsB - 1) * ld) * 16u;
 
   for (int c = 0; c < nch; ++c) {
-    switch (nch - 1 - c) {
-      case 0: cp_async_wait<0>(); break;
-      case 1: cp_async_wait<1>(); break;
-      case 2: cp_async_wait<2>(); break;
-      case 3: cp_async_wait<3>(); break;
-      case 4: cp_async_wait<4>(); break;
-      default: cp_async_wait<5>(); break;
+    if (BULK) {
+      barWait(&bars[c], 0);
+    } else {
+      switch (nch - 1 - c) {
+        case 0: cp_async_wait<0>(); break;
+        case 1: cp_async_wait<1>(); break;
+        case 2: cp_async_wait<2>(); break;
+        case 3: cp_async_wait<3>(); break;
+        case 4: cp_async_wait<4>(); break;
+        default: cp_async_wait<5>(); break;
+      }
+      __syncthreads();
     }
-    __syncthreads();
     SLAB_STAMP(2 + min(c, 5));
     const int q0 = c * CQ, cq = min(CQ, K4 - q0);
     float4 av[2][RM], bv[2][RN];
@@ -667,6 +697,10 @@ const GemmVariant kGemmVariants[] = {
     {32, 0, 0, 7, 4, -2, "slab_rt7x4", 0},
     {33, 0, 0, 4, 4, -2, "slab_rt4x4", 0},
     {34, 0, 0, 4, 2, -2, "slab_rt4x2", 0},
+    // ... filled by bulk copies (tk = -3)
+    {35, 0, 0, 7, 4, -3, "slab_rt7x4_bulk", 0},
+    {36, 0, 0, 4, 4, -3, "slab_rt4x4_bulk", 0},
+    {37, 0, 0, 4, 2, -3, "slab_rt4x2_bulk", 0},
 };
 
 template <int RM, int RN>
@@ -716,7 +750,7 @@ cudaError_t launchSlabCh(const GemmArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int RM, int RN>
+template <int RM, int RN, bool BULK>
 cudaError_t launchSlabRt(const GemmArgs& a, cudaStream_t s) {
   // warps along M to cover the rows (<= 8), then along N within 8 warps
   const int wmt = 4 * RM, wnt = 8 * RN;
@@ -724,8 +758,8 @@ cudaError_t launchSlabRt(const GemmArgs& a, cudaStream_t s) {
   int wn = std::min(std::max(1, 8 / wm), (a.N + wnt - 1) / wnt);
   dim3 grid(a.batch, (a.M + wm * wmt - 1) / (wm * wmt), (a.N + wn * wnt - 1) / (wn * wnt));
   const int ld = (a.K / 4) | 1;
-  const size_t smem = (size_t)(wm * wmt + wn * wnt) * ld * 16;
-  auto kfn = gemm_nt_slab_rt<RM, RN>;
+  const size_t smem = (size_t)(wm * wmt + wn * wnt) * ld * 16 + 8 * 8;
+  auto kfn = gemm_nt_slab_rt<RM, RN, BULK>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -814,9 +848,17 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
     case 33:
     case 34: {
       if (!slabOk(a)) return cudaErrorInvalidValue;
-      if (variant == 32) return launchSlabRt<7, 4>(a, s);
-      if (variant == 33) return launchSlabRt<4, 4>(a, s);
-      return launchSlabRt<4, 2>(a, s);
+      if (variant == 32) return launchSlabRt<7, 4, false>(a, s);
+      if (variant == 33) return launchSlabRt<4, 4, false>(a, s);
+      return launchSlabRt<4, 2, false>(a, s);
+    }
+    case 35:
+    case 36:
+    case 37: {
+      if (!slabOk(a)) return cudaErrorInvalidValue;
+      if (variant == 35) return launchSlabRt<7, 4, true>(a, s);
+      if (variant == 36) return launchSlabRt<4, 4, true>(a, s);
+      return launchSlabRt<4, 2, true>(a, s);
     }
     case 19:
     case 20:

@@ -164,7 +164,9 @@ void decodeGemm(const MappingOptions& o, Mapping& m) {
     const int ch = static_cast<int>(o.tileSizes[0]), rn = static_cast<int>(o.tileSizes[1]);
     for (int i = 1; i < k::gemmVariantCount(); ++i) {
       const auto& v = k::gemmVariant(i);
-      if ((rn == 1 && v.tk == -1 && v.rm == ch) || (rn > 1 && v.tk == -2 && v.rm == ch && v.rn == rn)) {
+      // unroll_copy_shared selects the bulk-copy fill of the register-tiled slab
+      const int tk = rn == 1 ? -1 : o.unrollCopyShared ? -3 : -2;
+      if (v.tk == tk && v.rm == ch && v.rn == rn) {
         m.gemmVariant = i;
         m.gemmThreads = 0;
         return;

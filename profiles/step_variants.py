@@ -20,7 +20,9 @@ COMBOS = [  # r02: the slab TBMM plans vs the r01 tiled plans in the step
     {"tbmm": {"tile_sizes": [32, 32, 64], "thread_shape": [16, 16, 1]}},
     {"tbmm": {"tile_sizes": [7, 1, 2]}},
     {"tbmm": {"tile_sizes": [7, 4, 2]}},
-    {"tbmm": {"tile_sizes": [4, 4, 2]}},
+    {"tbmm": {"tile_sizes": [4, 2, 2]}},
+    {"tbmm": {"tile_sizes": [4, 2, 2], "unroll_copy_shared": True}},
+    {"tbmm": {"tile_sizes": [7, 4, 2], "unroll_copy_shared": True}},
 ]
 
 VARIANTS = {
