@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(256) gemm_nt_slab_rt(const GemmArgs a, const i
   const int MT = wm * 4 * RM, NT = (blockDim.x >> 5) / wm * 8 * RN;
   const int m0 = blockIdx.y * MT, n0 = blockIdx.z * NT, b = blockIdx.x;
   const int K4 = a.K >> 2;
-  const int ld = K4 | 1;  // row stride in float4s (odd)
+  const int ld = BULK ? K4 : (K4 | 1);  // row stride in float4s (odd unless bulk-filled)
   const float* A = a.A + (int64_t)b * a.sA;
   const float* B = a.B + (int64_t)b * a.sB;
   float* C = a.C + (int64_t)b * a.sC;
@@ -526,30 +526,22 @@ __global__ void __launch_bounds__(256) gemm_nt_slab_rt(const GemmArgs a, const i
   SLAB_STAMP(0);
 
   const int nch = (K4 + CQ - 1) / CQ;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(Bs + NT * ld);  // BULK: one per chunk
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Bs + NT * ld);  // BULK: the fill's mbarrier
   if (BULK) {
-    // one bulk copy per (row, chunk) segment, completing on the chunk's
-    // mbarrier: the fills bypass the LSU pipe the chains' shared loads use
+    // dense operand tiles (rows of exactly K floats): one bulk copy per
+    // operand tile, both on one mbarrier. (Per row-chunk bulk copies were
+    // measured at ~6 us to issue 156 of them: a bulk copy costs its issuing
+    // thread ~200 cycles.)
     if (tid == 0) {
-      for (int c = 0; c < nch; ++c) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smemU32(&bars[c])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smemU32(&bars[0])));
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int c = 0; c < nch; ++c)
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemU32(&bars[c])),
-                     "r"((unsigned)((rowsA + rowsB) * min(CQ, K4 - c * CQ) * 16))
-                     : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemU32(&bars[0])),
+                   "r"((unsigned)((rowsA + rowsB) * K4 * 16))
+                   : "memory");
+      bulkG2S(As, A + (int64_t)m0 * a.lda, (unsigned)(rowsA * K4 * 16), &bars[0]);
+      bulkG2S(Bs, B + (int64_t)n0 * a.ldb, (unsigned)(rowsB * K4 * 16), &bars[0]);
     }
-    __syncthreads();
-    if (warp == 0) {
-      for (int e = lane; e < nch * (rowsA + rowsB); e += 32) {
-        const int c = e / (rowsA + rowsB), r = e - c * (rowsA + rowsB);
-        const int q0 = c * CQ;
-        const unsigned bytes = (unsigned)min(CQ, K4 - q0) * 16u;
-        if (r < rowsA)
-          bulkG2S(As + r * ld + q0, A + (int64_t)(m0 + r) * a.lda + 4 * q0, bytes, &bars[c]);
-        else
-          bulkG2S(Bs + (r - rowsA) * ld + q0, B + (int64_t)(n0 + r - rowsA) * a.ldb + 4 * q0, bytes, &bars[c]);
-      }
-    }
+    __syncthreads();  // barrier initialised before anyone waits on it
   } else {
     for (int c = 0; c < nch; ++c) {
       const int q0 = c * CQ, cq = min(CQ, K4 - q0);
@@ -584,7 +576,7 @@ __global__ void __launch_bounds__(256) gemm_nt_slab_rt(const GemmArgs a, const i
 
   for (int c = 0; c < nch; ++c) {
     if (BULK) {
-      barWait(&bars[c], 0);
+      if (c == 0) barWait(&bars[0], 0);
     } else {
       switch (nch - 1 - c) {
         case 0: cp_async_wait<0>(); break;
@@ -757,7 +749,8 @@ cudaError_t launchSlabRt(const GemmArgs& a, cudaStream_t s) {
   int wm = std::min(8, (a.M + wmt - 1) / wmt);
   int wn = std::min(std::max(1, 8 / wm), (a.N + wnt - 1) / wnt);
   dim3 grid(a.batch, (a.M + wm * wmt - 1) / (wm * wmt), (a.N + wn * wnt - 1) / (wn * wnt));
-  const int ld = (a.K / 4) | 1;
+  if (BULK && (a.lda != a.K || a.ldb != a.K)) return launchSlabRt<RM, RN, false>(a, s);
+  const int ld = BULK ? a.K / 4 : (a.K / 4) | 1;
   const size_t smem = (size_t)(wm * wmt + wn * wnt) * ld * 16 + 8 * 8;
   auto kfn = gemm_nt_slab_rt<RM, RN, BULK>;
   if (smem > 48 * 1024) {
