@@ -642,6 +642,149 @@ __global__ void __launch_bounds__(256) gemm_nt_slab_rt(const GemmArgs a, const i
   SLAB_STAMP(9);
 }
 
+// Warp-per-batch GEMM: for batches whose whole output fits one warp tile
+// (M <= 4*RM, N <= 8*RN: TBMM's 26x26 with 7x4). A CTA of W warps owns W
+// consecutive batches, one per warp, so the warps of one SM spread over its
+// four schedulers (a 1-warp CTA per batch left them on few schedulers:
+// profiles/r02_tbmm_trace.txt). Lane 0 of each warp lands its batch's two
+// dense operand blocks with two bulk copies on the warp's own mbarrier (or the
+// warp's lanes use 16-byte cp.async when the rows are not dense) and the
+// warp starts the moment its batch is in. Lane = rg * 8 + cg owns rows
+// rg + 4i and columns cg + 8j; each 4-step group reads RM + RN float4s from
+// shared memory for 4*RM*RN FFMAs (ncu: the LSU pipe, not the FMA pipe,
+// bounded the broadcast slab). Each output is one lane's sequential FFMA
+// chain in ascending k from its init value.
+template <int RM, int RN>
+__global__ void __launch_bounds__(256) gemm_nt_warpbatch(const GemmArgs a, const int dense) {
+  extern __shared__ __align__(16) float smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+  const int b = blockIdx.x * W + warp;
+  const int K4 = a.K >> 2;
+  const int ld = dense ? K4 : (K4 | 1);
+  const int slot = (a.M + a.N) * ld;  // float4s per warp
+  float4* As = reinterpret_cast<float4*>(smem) + warp * slot;
+  float4* Bs = As + a.M * ld;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<float4*>(smem) + W * slot) + warp;
+  SLAB_STAMP(0);
+  if (b >= a.batch) return;  // (no CTA-wide barrier below)
+  const float* A = a.A + (int64_t)b * a.sA;
+  const float* B = a.B + (int64_t)b * a.sB;
+  float* C = a.C + (int64_t)b * a.sC;
+  if (dense) {
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smemU32(bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smemU32(bar)),
+                   "r"((unsigned)((a.M + a.N) * K4 * 16))
+                   : "memory");
+      bulkG2S(As, A, (unsigned)(a.M * K4 * 16), bar);
+      bulkG2S(Bs, B, (unsigned)(a.N * K4 * 16), bar);
+    }
+  } else {
+    for (int e = lane; e < (a.M + a.N) * K4; e += 32) {
+      const int r = e / K4, q = e - r * K4;
+      if (r < a.M)
+        cp_async16(As + r * ld + q, A + (int64_t)r * a.lda + 4 * q, 16);
+      else
+        cp_async16(Bs + (r - a.M) * ld + q, B + (int64_t)(r - a.M) * a.ldb + 4 * q, 16);
+    }
+    cp_async_commit();
+  }
+  SLAB_STAMP(1);
+  const int rg = lane >> 3, cg = lane & 7;
+  float acc[RM][RN];
+#pragma unroll
+  for (int i = 0; i < RM; ++i)
+#pragma unroll
+    for (int j = 0; j < RN; ++j) {
+      const int m = rg + 4 * i, n = cg + 8 * j;
+      acc[i][j] = (m < a.M && n < a.N) ? initValue(a, C, m, n) : 0.0f;
+    }
+  unsigned ra[RM], rb[RN];
+#pragma unroll
+  for (int i = 0; i < RM; ++i) ra[i] = smemU32(As + min(rg + 4 * i, a.M - 1) * ld);
+#pragma unroll
+  for (int j = 0; j < RN; ++j) rb[j] = smemU32(Bs + min(cg + 8 * j, a.N - 1) * ld);
+  if (dense) {
+    __syncwarp();  // lane 0's barrier init before the others poll it
+    barWait(bar, 0);
+  } else {
+    cp_async_wait<0>();
+    __syncwarp();
+  }
+  SLAB_STAMP(2);
+  float4 av[2][RM], bv[2][RN];
+#pragma unroll
+  for (int i = 0; i < RM; ++i) av[0][i] = ldsV4(ra[i]);
+#pragma unroll
+  for (int j = 0; j < RN; ++j) bv[0][j] = ldsV4(rb[j]);
+  int q = 0;
+  for (; q + 2 <= K4; q += 2) {  // two groups per trip: static register buffers
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (q + h + 1 < K4) {
+#pragma unroll
+        for (int i = 0; i < RM; ++i) av[h ^ 1][i] = ldsV4(ra[i] + (q + h + 1) * 16);
+#pragma unroll
+        for (int j = 0; j < RN; ++j) bv[h ^ 1][j] = ldsV4(rb[j] + (q + h + 1) * 16);
+      }
+      const float4* x = av[h];
+      const float4* y = bv[h];
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].x, y[j].x, acc[i][j]);
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].y, y[j].y, acc[i][j]);
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].z, y[j].z, acc[i][j]);
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].w, y[j].w, acc[i][j]);
+    }
+  }
+  if (q < K4) {  // odd group count: the last group sits in buffer 0
+    const float4* x = av[0];
+    const float4* y = bv[0];
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+      for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].x, y[j].x, acc[i][j]);
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+      for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].y, y[j].y, acc[i][j]);
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+      for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].z, y[j].z, acc[i][j]);
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+      for (int j = 0; j < RN; ++j) acc[i][j] = __fmaf_rn(x[i].w, y[j].w, acc[i][j]);
+  }
+  SLAB_STAMP(8);
+#pragma unroll
+  for (int i = 0; i < RM; ++i) {
+    const int m = rg + 4 * i;
+#pragma unroll
+    for (int j = 0; j < RN; ++j) {
+      const int n = cg + 8 * j;
+      if (m < a.M && n < a.N) {
+        float v = acc[i][j];
+        if (a.relu) v = fmaxf(v, 0.0f);
+        C[(int64_t)m * a.ldc + n] = v;
+      }
+    }
+  }
+  SLAB_STAMP(9);
+}
+
 int batchedLd(int K) {
   int l = (K + 3) & ~3;
   while (l % 32 != 4) l += 4;
@@ -693,6 +836,9 @@ const GemmVariant kGemmVariants[] = {
     {35, 0, 0, 7, 4, -3, "slab_rt7x4_bulk", 0},
     {36, 0, 0, 4, 4, -3, "slab_rt4x4_bulk", 0},
     {37, 0, 0, 4, 2, -3, "slab_rt4x2_bulk", 0},
+    // one warp per batch (tk = -4): the whole batch is one rm x rn warp tile
+    {38, 0, 0, 7, 4, -4, "warpbatch_7x4", 0},
+    {39, 0, 0, 4, 4, -4, "warpbatch_4x4", 0},
 };
 
 template <int RM, int RN>
@@ -758,6 +904,24 @@ cudaError_t launchSlabRt(const GemmArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   kfn<<<grid, wm * wn * 32, smem, s>>>(a, wm);
+  return cudaGetLastError();
+}
+
+template <int RM, int RN>
+cudaError_t launchWarpBatch(const GemmArgs& a, int warps, cudaStream_t s) {
+  if (a.M > 4 * RM || a.N > 8 * RN) return cudaErrorInvalidValue;
+  const int dense = a.lda == a.K && a.ldb == a.K;
+  const int K4 = a.K / 4, ld = dense ? K4 : (K4 | 1);
+  if (warps <= 0) warps = 4;
+  warps = std::max(1, std::min(8, warps));
+  const size_t smem = (size_t)warps * (a.M + a.N) * ld * 16 + 8 * warps;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  auto kfn = gemm_nt_warpbatch<RM, RN>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kfn<<<(a.batch + warps - 1) / warps, warps * 32, smem, s>>>(a, dense);
   return cudaGetLastError();
 }
 
@@ -852,6 +1016,13 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
       if (variant == 35) return launchSlabRt<7, 4, true>(a, s);
       if (variant == 36) return launchSlabRt<4, 4, true>(a, s);
       return launchSlabRt<4, 2, true>(a, s);
+    }
+    case 38:
+    case 39: {
+      // warp per batch; `threads` carries the warps per CTA (0 = 4)
+      if (!slabOk(a)) return cudaErrorInvalidValue;
+      if (variant == 38) return launchWarpBatch<7, 4>(a, threads, s);
+      return launchWarpBatch<4, 4>(a, threads, s);
     }
     case 19:
     case 20:

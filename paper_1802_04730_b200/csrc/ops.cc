@@ -165,10 +165,11 @@ void decodeGemm(const MappingOptions& o, Mapping& m) {
     for (int i = 1; i < k::gemmVariantCount(); ++i) {
       const auto& v = k::gemmVariant(i);
       // unroll_copy_shared selects the bulk-copy fill of the register-tiled slab
-      const int tk = rn == 1 ? -1 : o.unrollCopyShared ? -3 : -2;
+      // block_shape[0] > 1 selects one warp per batch with that many warps per CTA
+      const int tk = rn == 1 ? -1 : o.blockShape[0] > 1 ? -4 : o.unrollCopyShared ? -3 : -2;
       if (v.tk == tk && v.rm == ch && v.rn == rn) {
         m.gemmVariant = i;
-        m.gemmThreads = 0;
+        m.gemmThreads = tk == -4 ? static_cast<int>(o.blockShape[0]) : 0;
         return;
       }
     }
@@ -271,7 +272,9 @@ std::string Mapping::describe() const {
   }
   switch (family) {
     case Family::Gemm:
-      if (k::gemmVariant(gemmVariant).tk < 0)
+      if (k::gemmVariant(gemmVariant).tk == -4)
+        os << k::gemmVariant(gemmVariant).name << " warps=" << gemmThreads;
+      else if (k::gemmVariant(gemmVariant).tk < 0)
         os << k::gemmVariant(gemmVariant).name;
       else if (k::gemmVariant(gemmVariant).tk == 0)
         os << k::gemmVariant(gemmVariant).name << " grid=" << (gemmThreads ? std::to_string(gemmThreads) : "auto");

@@ -23,6 +23,8 @@ COMBOS = [  # r02: the slab TBMM plans vs the r01 tiled plans in the step
     {"tbmm": {"tile_sizes": [4, 2, 2]}},
     {"tbmm": {"tile_sizes": [4, 2, 2], "unroll_copy_shared": True}},
     {"tbmm": {"tile_sizes": [7, 4, 2], "unroll_copy_shared": True}},
+    {"tbmm": {"tile_sizes": [7, 4, 2], "block_shape": [4, 1, 1]}},
+    {"tbmm": {"tile_sizes": [7, 4, 2], "block_shape": [2, 1, 1]}},
 ]
 
 VARIANTS = {
