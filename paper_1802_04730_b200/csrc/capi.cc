@@ -84,8 +84,13 @@ struct Compiled {
   std::vector<void*> dIn, dOut;
   std::vector<size_t> inBytes, outBytes;
   std::vector<bool> outInout;
+  // recorded after a host run's last read of the staging buffers (its D2H);
+  // the next host run, on any stream, waits for it before overwriting them
+  cudaEvent_t stagingFree = nullptr;
+  bool stagingPending = false;
   std::mutex runMu;
   ~Compiled() {
+    if (stagingFree) cudaEventDestroy(stagingFree);
     if (dErr) cudaFree(dErr);
     for (void* p : dIn) cudaFree(p);
     for (void* p : dOut) cudaFree(p);
@@ -405,6 +410,10 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
     std::vector<const void*> outMapped(nout, nullptr);
     if (host) {
       ensureStaging(c);
+      if (!c.stagingFree) cudaOk(cudaEventCreateWithFlags(&c.stagingFree, cudaEventDisableTiming), "event");
+      // an earlier async host run (possibly on another stream) may still be
+      // reading these staging buffers
+      if (c.stagingPending) cudaOk(cudaStreamWaitEvent(s, c.stagingFree, 0), "stream wait");
       auto stage = [&](k::SegCopyArgs& a, void* dst, const void* src, const void* mapped, size_t bytes,
                        cudaMemcpyKind kind) {
         if (mapped && a.n < k::kMaxSeg && static_cast<int64_t>(bytes) <= zeroCopyMax() && bytes % 4 == 0) {
@@ -447,6 +456,8 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
           cudaOk(cudaMemcpyAsync(out[i].data, dout[i], c.outBytes[i], cudaMemcpyDeviceToHost, s), "D2H");
       }
       cudaOk(k::launchSegCopy(down, deviceSms(), s), "host copy");
+      cudaOk(cudaEventRecord(c.stagingFree, s), "record");
+      c.stagingPending = (flags & TCB_RUN_ASYNC) != 0;
       if (!(flags & TCB_RUN_ASYNC)) cudaOk(cudaStreamSynchronize(s), "sync");
     }
     if (profile) {

@@ -79,10 +79,12 @@ __global__ void lut_kernel(const LutArgs a0, const LutArgs a1, const int vec) {
 // (batch row, table): stage 1 reads the row's L indices and validates them;
 // stage 2 has every thread of the CTA issue its share of the L x D/4
 // 16-byte gathers at once (all of the row's table rows in flight together)
-// into shared memory; stage 3 sums them in k order, one float4 column per
-// thread (__fadd_rn, the interpreter's order). Chunks of kRows rows keep the
-// staging buffer bounded for any L.
+// into shared memory; stage 3 sums them in k order, each thread owning the
+// float4 columns tid, tid + T, ... (__fadd_rn, the interpreter's order), so
+// any block size covers any D. Chunks of kRows rows keep the staging buffer
+// bounded for any L.
 constexpr int kRows = 64;
+constexpr int kMaxColsPerThread = 8;  // float4 columns per thread: D <= 32 * T
 __global__ void lut_smem_kernel(const LutArgs a0, const LutArgs a1) {
   const LutArgs& a = blockIdx.y == 0 ? a0 : a1;
   const int64_t row = blockIdx.x;
@@ -93,7 +95,9 @@ __global__ void lut_smem_kernel(const LutArgs a0, const LutArgs a1) {
   const int cols = a.D / 4, T = blockDim.x, tid = threadIdx.x;
   const int32_t* idx = a.I + row * a.L;
   if (tid == 0) sBad = 0;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 acc[kMaxColsPerThread];
+#pragma unroll
+  for (int j = 0; j < kMaxColsPerThread; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int k0 = 0; k0 < a.L; k0 += kRows) {
     const int nk = min(kRows, a.L - k0);
     __syncthreads();  // previous chunk consumed
@@ -109,17 +113,25 @@ __global__ void lut_smem_kernel(const LutArgs a0, const LutArgs a1) {
       stage[q] = __ldg(reinterpret_cast<const float4*>(a.LUT + sIdx[k] * a.D) + c);
     }
     __syncthreads();
-    if (tid < cols) {
-      for (int k = 0; k < nk; ++k) {
-        const float4 v = stage[k * cols + tid];
-        acc.x = __fadd_rn(acc.x, v.x);
-        acc.y = __fadd_rn(acc.y, v.y);
-        acc.z = __fadd_rn(acc.z, v.z);
-        acc.w = __fadd_rn(acc.w, v.w);
+#pragma unroll
+    for (int j = 0; j < kMaxColsPerThread; ++j) {
+      const int c = tid + j * T;
+      if (c < cols) {
+        for (int k = 0; k < nk; ++k) {
+          const float4 v = stage[k * cols + c];
+          acc[j].x = __fadd_rn(acc[j].x, v.x);
+          acc[j].y = __fadd_rn(acc[j].y, v.y);
+          acc[j].z = __fadd_rn(acc[j].z, v.z);
+          acc[j].w = __fadd_rn(acc[j].w, v.w);
+        }
       }
     }
   }
-  if (tid < cols) reinterpret_cast<float4*>(a.O + row * a.D)[tid] = acc;
+#pragma unroll
+  for (int j = 0; j < kMaxColsPerThread; ++j) {
+    const int c = tid + j * T;
+    if (c < cols) reinterpret_cast<float4*>(a.O + row * a.D)[c] = acc[j];
+  }
   if (tid == 0 && sBad) atomicOr(a.err, 1);  // IndexOutOfRange; the row's value is unspecified
 }
 
@@ -149,17 +161,18 @@ cudaError_t launchLut(const LutArgs* tables, int ntables, int threads, cudaStrea
     maxB = tables[i].B > maxB ? tables[i].B : maxB;
   }
   const size_t smem = (size_t)kRows * maxD * 4;
-  if (vec && smem <= 160 * 1024) {  // two-stage shared-memory gather: `threads` per (row, table) CTA
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(lut_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      attr = true;
+  int t = threads > 0 ? threads : 256;
+  if (vec && smem <= 160 * 1024 && maxD / 4 <= kMaxColsPerThread * t) {
+    // two-stage shared-memory gather: `threads` per (row, table) CTA. The
+    // attribute is per device context: set on every launch (a per-process
+    // flag would leave a second device at the 48 KB default)
+    if (smem > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(lut_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      if (e != cudaSuccess) return e;
     }
-    int t = threads > 0 ? threads : 256;
     lut_smem_kernel<<<dim3((unsigned)maxB, ntables), t, smem, s>>>(p.t[0], p.t[1]);
     return cudaGetLastError();
   }
-  int t = threads > 0 ? threads : 256;
   dim3 grid((unsigned)((maxLanes + t - 1) / t), ntables);
   lut_kernel<<<grid, t, 0, s>>>(p.t[0], p.t[1], vec);
   return cudaGetLastError();

@@ -23,6 +23,7 @@
 // [r*128/splits, (r+1)*128/splits) of the tile by reading every CTA's
 // partial over DSMEM in fixed rank order (deterministic), adds the init
 // (bias / incoming C), applies ReLU and stores coalesced rows.
+#include <atomic>
 #include <cuda.h>
 
 #include <mutex>
@@ -301,13 +302,18 @@ cudaError_t launchT(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams
                     int batch, cudaStream_t s) {
   using Cfg = TcCfg<BN, X3>;
   auto kern = tc_gemm_kernel<BN, X3>;
-  static std::once_flag once;
-  static cudaError_t attrErr = cudaSuccess;
-  std::call_once(once, [&] {
-    attrErr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-    if (attrErr == cudaSuccess) attrErr = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  });
-  if (attrErr != cudaSuccess) return attrErr;
+  // function attributes belong to a device context: set once per device
+  // (bit d of `done`), never once per process
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    done.fetch_or(bit, std::memory_order_release);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(tilesN, tilesM, batch * p.splits);
   cfg.blockDim = dim3(kThreads);

@@ -118,8 +118,9 @@ struct GenePools {
   std::vector<int> useShared;  // {0,1} or {1}
 };
 GenePools genePools(const Problem& p, int math = k::kMathFfma);
-// the stated tolerance of a tensor-core mode for this problem,
-// max |got - ref| / max(|ref|, 1) against the FFMA/TC reference candidate
+// the tuner's acceptance bound for a tensor-core candidate against the
+// default tensor-core plan of the same problem (accumulation order only),
+// max |got - ref| / max(|ref|, 1); see ops.cc
 double tcTolerance(const Problem& p, int math);
 
 // Launches the whole definition on `stream`. in/out are device pointers in

@@ -330,6 +330,26 @@ def test_lut_paper_shape(engine, oracle):
     np.testing.assert_array_equal(got["O"], oracle.lut(lut, idx))
 
 
+@pytest.mark.parametrize("D,threads", [(256, 32), (640, 128), (512, 64), (64, 32), (1024, 32)])
+def test_lut_wide_rows_small_blocks(engine, oracle, D, threads):
+    """Block sizes smaller than D/4 float4 columns (explicit options): every
+    column is still summed and stored (columns >= 4*blockDim
+    were left unwritten), bit-exact against the oracle."""
+    rng = oracle.rng(D + threads)
+    lut = rng.f32((5000, D))
+    idx = rng.i32((16, 7), 0, 5000)
+    opts = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0, "shared_memory_budget": 49152,
+            "thread_shape": [threads, 1, 1], "tile_sizes": [1, 1, 1], "unroll_copy_shared": False,
+            "unroll_factor": 1, "use_private": True, "use_shared": False}
+    out = np.full((16, D), np.nan, np.float32)
+    p, o = [to_dev(lut), to_dev(idx)], [to_dev(out)]
+    h = engine.compile("1LUT", p, o, opts)
+    assert f"threads={threads}" in engine.describe(h)["kernel"]
+    engine.run(h, p, o)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(o[0].cpu().numpy(), oracle.lut(lut, idx))
+
+
 def test_cuda_graph_capture(engine, oracle, golden):
     case, ins, seeded = case_inputs(oracle, golden, "tbmm_paper")
     p = [to_dev(ins["X"]), to_dev(ins["Y"])]

@@ -1,14 +1,19 @@
-"""GPU parity of the tensor-core (tcgen05 TF32 / 3xTF32) variants against
-the oracle. These variants are not FFMA-exact: a tensor-core reduction
-cannot reproduce the reference interpreter's per-step fp32 chain
-(interpreter.cc:218-233), so the bar is a stated tolerance:
+"""GPU parity of the tensor-core (tcgen05 TF32 / 3xTF32) variants. These
+variants are not FFMA-exact: a tensor-core reduction cannot reproduce the
+reference interpreter's per-step fp32 chain (interpreter.cc:218-233), so the
+bar is a stated tolerance, on maxRelError
+(tensor_data.cc:221-234, denominator max(|ref|, 1)):
 
-  maxRelError (tensor_data.cc:221-234, denominator max(|ref|, 1)) against
-  the oracle, inputs U[-1,1):
-    3xtf32:  <= TOL_3X(K) = 1e-5 + K * 2^-23
-    tf32:    <= TOL_1X(K) = K * 2^-11       (operands rounded to 10-bit mantissas)
+  1. against the tensor-core emulation (tests/tc_emulate.py: the operands
+     rounded exactly as the kernels round them, products summed in fp64):
+       both modes:  <= tol_emu(K) = K * 2^-24 * max(1, max|a| max|b|)
+     — only the fp32 accumulator's rounding separates the two, so a kernel
+     that dropped one 32-deep k-block (~0.1 relative) fails by ~1000x;
+  2. against the oracle (the reference's own fp32 chain), the operand-
+     rounding bound, a sanity check on the emulation itself:
+       3xtf32:  <= 1e-5 + K * 2^-23        tf32:  <= K * 2^-11
 
-Every case also records its measured error next to the bound
+Every case records its measured errors next to the bounds
 (gpurun_out/tc_errors.jsonl when run on the GPU box).
 """
 import json
@@ -17,6 +22,7 @@ import os
 import numpy as np
 import pytest
 
+import tc_emulate as emu
 from conftest import max_rel
 from oracle_lib import Oracle
 
@@ -35,12 +41,21 @@ def opscale(a, b):
     return float(np.max(np.abs(a))) * float(np.max(np.abs(b)))
 
 
-def record(name, math, K, err, exact_err, oracle_exact_err):
+def record(name, math, K, err, exact_err, oracle_exact_err, emu_err=None, emu_bound=None):
     d = os.path.join(ROOT, "gpurun_out")
     os.makedirs(d, exist_ok=True)
     with open(os.path.join(d, "tc_errors.jsonl"), "a") as f:
         f.write(json.dumps({"case": name, "math": math, "K": K, "max_rel_vs_oracle": err, "bound": tol(math, K),
+                            "max_rel_vs_emulation": emu_err, "emulation_bound": emu_bound,
                             "max_rel_vs_fp64": exact_err, "oracle_max_rel_vs_fp64": oracle_exact_err}) + "\n")
+
+
+def check_emu(name, math, K, got, ref_emu, scale=1.0):
+    """The tight bar: got vs the tensor-core emulation."""
+    e = max_rel(ref_emu, got)
+    b = emu.tol_emu(K, scale)
+    assert e <= b, f"{name} {math}: maxRel vs emulation {e:.3g} > {b:.3g}"
+    return e, b
 
 
 @pytest.fixture(scope="module")
@@ -94,8 +109,10 @@ def test_gemm_tc(env, name, shape, math):
         exact = gemm64(A, B)
         (got,), desc = run(ee, "tmm", [A, B], [np.zeros((M, N), np.float32)], math)
     assert desc["math"] == math and "tcgen05" in desc["kernel"]
+    ref_emu = emu.gemm_nt(A, B, math) + (cin.astype(np.float64) if name == "C3" else 0.0)
+    ee_, eb = check_emu(f"{name} {shape}", math, K, got, ref_emu)
     err = max_rel(ref, got)
-    record(f"{name} {M}x{N}x{K}", math, K, err, max_rel(exact, got), max_rel(exact, ref))
+    record(f"{name} {M}x{N}x{K}", math, K, err, max_rel(exact, got), max_rel(exact, ref), ee_, eb)
     assert err <= tol(math, K), f"{name} {shape} {math}: maxRel {err:.3g} > {tol(math, K):.3g}"
 
 
@@ -109,8 +126,9 @@ def test_tbmm_tc(env, shape, math):
     ref = orc.tbmm(X, Y)
     exact = np.einsum("bnm,bkm->bnk", X.astype(np.float64), Y.astype(np.float64))
     (got,), desc = run(ee, "tbmm", [X, Y], [np.zeros((Bt, N, K), np.float32)], math)
+    ee_, eb = check_emu(f"tbmm {shape}", math, M, got, emu.gemm_nt(X, Y, math))
     err = max_rel(ref, got)
-    record(f"tbmm {shape}", math, M, err, max_rel(exact, got), max_rel(exact, ref))
+    record(f"tbmm {shape}", math, M, err, max_rel(exact, got), max_rel(exact, ref), ee_, eb)
     assert err <= tol(math, M)
 
 
@@ -124,17 +142,20 @@ def test_fc_chains_tc(env, math):
     o2 = orc.fc_relu(o1, W2, B2)
     (g1,), desc = run(ee, "MLP1", [I, W1, B1], [np.zeros((128, 128), np.float32)], math)
     assert "tcgen05" in desc["kernel"]
+    ee1, eb1 = check_emu("MLP1", math, 1128, g1, emu.fc_relu(I, W1, B1, math))
     e1 = max_rel(o1, g1)
-    record("MLP1 128x1128->128", math, 1128, e1, None, None)
+    record("MLP1 128x1128->128", math, 1128, e1, None, None, ee1, eb1)
     assert e1 <= tol(math, 1128)
     (h1, h2), _ = run(ee, "2FCRelu", [I, W1, B1, W2, B2], [np.zeros((128, 128), np.float32),
                                                            np.zeros((128, 64), np.float32)], math)
+    check_emu("2FCRelu layer 1", math, 1128, h1, emu.fc_relu(I, W1, B1, math))
     assert max_rel(o1, h1) <= tol(math, 1128)
     # layer 2 consumes the GPU's own layer-1 output: compare against the
-    # oracle applied to that same input, plus the propagated layer-1 error
+    # oracle / emulation applied to that same input
     ref2 = orc.fc_relu(h1, W2, B2)
+    ee2, eb2 = check_emu("2FCRelu layer 2", math, 128, h2, emu.fc_relu(h1, W2, B2, math), opscale(h1, W2))
     e2 = max_rel(ref2, h2)
-    record("2FCRelu layer 2", math, 128, e2, None, None)
+    record("2FCRelu layer 2", math, 128, e2, None, None, ee2, eb2)
     assert e2 <= tol(math, 128, opscale(h1, W2))
     O1 = rng.f32((128, 128))
     M2, C2, M3, C3b, M4, C4 = (rng.f32((64, 128)), rng.f32((64,)), rng.f32((32, 64)), rng.f32((32,)),
@@ -144,8 +165,9 @@ def test_fc_chains_tc(env, math):
                                np.zeros((128, 2), np.float32)], math)
     assert np.array_equal(q1, O1)  # pass-through return untouched
     for got, (inp, W, b, K) in zip((q2, q3, q4), ((O1, M2, C2, 128), (q2, M3, C3b, 64), (q3, M4, C4, 32))):
+        ee_, eb = check_emu(f"MLP3 layer K={K}", math, K, got, emu.fc_relu(inp, W, b, math), opscale(inp, W))
         e = max_rel(orc.fc_relu(inp, W, b), got)
-        record(f"MLP3 layer K={K}", math, K, e, None, None)
+        record(f"MLP3 layer K={K}", math, K, e, None, None, ee_, eb)
         assert e <= tol(math, K, opscale(inp, W))
 
 
@@ -161,6 +183,7 @@ def test_tc_explicit_plan_and_errors(env):
                      "use_shared": True, "fusion_strategy": "min"})
         (got,), desc = run(ee, "tmm", [A, B], [np.zeros((128, 512), np.float32)], "3xtf32", opts)
         assert f"bn={bn} splits={sp}" in desc["kernel"]
+        check_emu(f"tmm bn={bn} splits={sp}", "3xtf32", 256, got, emu.gemm_nt(A, B, "3xtf32"))
         assert max_rel(ref, got) <= tol("3xtf32", 256)
     # rows not a multiple of 16 bytes: no tensor-core kernel
     A2, B2 = rng.f32((16, 30)), rng.f32((16, 30))
@@ -203,8 +226,10 @@ def test_gconv_tc(env, case, math, variant):
     assert "tcgen05" in desc["kernel"]
     assert {"nhwc": "NHWC", "im2col": "im2col", "shift": "shifted halo"}[variant] in desc["kernel"]
     K = C * KH * KW
+    ref_emu = emu.gconv_points(I, W1, Bv, np.arange(got.size), math)
+    ee_, eb = check_emu(f"gconv {case} {variant}", math, K + Mb, got.reshape(-1), ref_emu)
     err = max_rel(ref, got)
-    record(f"gconv {case} {variant}", math, K, err, None, None)
+    record(f"gconv {case} {variant}", math, K, err, None, None, ee_, eb)
     assert err <= tol(math, K), f"gconv {case} {math}: maxRel {err:.3g} > {tol(math, K):.3g}"
 
 
@@ -224,15 +249,19 @@ def test_gconv_tc_shift_odd_planes(env, case, math):
     (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros(ref.shape, np.float32)], math, opts)
     assert "shifted halo" in desc["kernel"]
     K = C * KH * KW
+    ref_emu = emu.gconv_points(I, W1, Bv, np.arange(got.size), math)
+    ee_, eb = check_emu(f"gconv {case} shift-odd", math, K + Mb, got.reshape(-1), ref_emu)
     err = max_rel(ref, got)
-    record(f"gconv {case} shift-odd", math, K, err, None, None)
+    record(f"gconv {case} shift-odd", math, K, err, None, None, ee_, eb)
     assert err <= tol(math, K), f"gconv {case} {math}: maxRel {err:.3g} > {tol(math, K):.3g}"
 
 
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
 @pytest.mark.parametrize("variant", [None, 3])
-def test_gconv_tc_paper_shape_sampled(env, variant):
-    """tcgen05 gconv at the BASELINE shape, 200k sampled points vs the oracle
-    (default plan, and the shifted-halo kernel)."""
+def test_gconv_tc_paper_shape_sampled(env, variant, math):
+    """tcgen05 gconv at the BASELINE shape (32,32,16,16,58x58,3x3), 200k
+    sampled points vs the emulation and the oracle (default plan, and the
+    shifted-halo kernel explicitly), both math modes."""
     from paper_1802_04730_b200 import options_baseline
     ee, orc = env
     rng = orc.rng(11)
@@ -241,12 +270,15 @@ def test_gconv_tc_paper_shape_sampled(env, variant):
     if variant is not None:
         opts = json.loads(options_baseline(0))
         opts.update({"tile_sizes": [128, 16, variant], "thread_shape": [512, 1, 1]})
-    (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros((32, 32, 16, 56, 56), np.float32)], "3xtf32", opts)
+    (got,), desc = run(ee, "gconv", [I, W1, Bv], [np.zeros((32, 32, 16, 56, 56), np.float32)], math, opts)
+    assert "tcgen05" in desc["kernel"]
     idx = np.random.default_rng(0).integers(0, got.size, 200_000)
+    g = got.reshape(-1)[idx]
+    ee_, eb = check_emu("gconv paper shape sampled", math, 144 + 16, g, emu.gconv_points(I, W1, Bv, idx, math))
     ref = orc.gconv_points(I, W1, Bv, idx)
-    err = max_rel(ref, got.reshape(-1)[idx])
-    record("gconv paper shape sampled", "3xtf32", 144, err, None, None)
-    assert err <= tol("3xtf32", 144)
+    err = max_rel(ref, g)
+    record(f"gconv paper shape sampled ({desc['kernel']})", math, 144, err, None, None, ee_, eb)
+    assert err <= tol(math, 144)
 
 
 @pytest.mark.parametrize("math", ["3xtf32", "tf32"])
@@ -264,6 +296,16 @@ def test_kru_tc(env, shape, math):
     outs = [np.zeros(Y.shape, np.float32), np.zeros(XW1.shape, np.float32), np.zeros(XW2.shape, np.float32)]
     (gY, gXW1, gXW2), desc = run(ee, "3KRU", [W0, W1, W2, X], outs, math)
     assert "tcgen05" in desc["kernel"] and "3-step" in desc["kernel"]
+    # emulation stage by stage, each fed the GPU's own previous return (the
+    # kernel's next A operand is exactly that fp32 accumulator value)
+    e2 = emu.gemm_nt(X.reshape(-1, 16), W2, math).reshape(gXW2.shape)
+    t = np.ascontiguousarray(np.transpose(gXW2, (0, 1, 3, 2)))            # [m,n0,d2,r1]
+    e1 = np.transpose(emu.gemm_nt(t.reshape(-1, 16), W1, math).reshape(M, 16, D2, D), (0, 1, 3, 2))
+    t = np.ascontiguousarray(np.transpose(gXW1, (0, 2, 3, 1)))            # [m,d1,d2,r0]
+    e0 = np.transpose(emu.gemm_nt(t.reshape(-1, 16), W0, math).reshape(M, D, D2, D), (0, 3, 1, 2))
+    for name, got, ref_e, K, scale in (("XW2", gXW2, e2, 16, opscale(X, W2)), ("XW1", gXW1, e1, 16, opscale(gXW2, W1)),
+                                       ("Y", gY, e0, 16, opscale(gXW1, W0))):
+        check_emu(f"3KRU {shape} {name}", math, K, got, ref_e, scale)
     for name, got, ref, K, scale in (("XW2", gXW2, XW2, 16, opscale(X, W2)),
                                      ("XW1", gXW1, XW1, 32, opscale(XW2, W1)),
                                      ("Y", gY, Y, 48, opscale(XW1, W0))):
@@ -304,3 +346,36 @@ def test_tc_tuner_and_cache_replay(env, tmp_path, math):
     assert max_rel(ref, dC.cpu().numpy()) <= tol(math, 1024)
     assert ee.describe(ee.compile("C3", [dA, dB], [dC]))["options_source"] == "default"
     tcb.cache_purge()
+
+
+def test_tmm_huge_paper_shape(env):
+    """TMM at the paper's large shape (128, 4096, 16384),
+    every math mode: the FFMA kernel bit-exact against the oracle on sampled
+    rows, the tensor-core kernels within tol_emu of the emulation on sampled
+    rows x columns."""
+    ee, orc = env
+    rng = orc.rng(1632)
+    A, B = rng.f32((128, 16384)), rng.f32((4096, 16384))
+    rows = np.array([0, 1, 37, 64, 101, 127])
+    cols = np.sort(np.random.default_rng(1).choice(4096, 512, replace=False))
+    cols[0], cols[-1] = 0, 4095
+    dA, dB = dev(A), dev(B)
+    ref_rows = orc.tmm(np.ascontiguousarray(A[rows]), B)                    # [6, 4096] fp32 chains
+    for math in ("ffma", "tf32", "3xtf32"):
+        dC = torch.zeros((128, 4096), device="cuda")
+        h = ee.compile("tmm", [dA, dB], [dC], math=math)
+        ee.run(h, [dA, dB], [dC])
+        torch.cuda.synchronize()
+        got = dC.cpu().numpy()[rows]
+        kern = ee.describe(h)["kernel"]
+        if math == "ffma":
+            bad = int(np.sum(got.view(np.uint32) != ref_rows.view(np.uint32)))
+            assert bad == 0, f"tmm 128x4096x16384 ffma ({kern}): {bad} sampled elements not bit-exact"
+            record("tmm 128x4096x16384 sampled rows", math, 16384, max_rel(ref_rows, got), None, None, 0.0, 0.0)
+            continue
+        assert "tcgen05" in kern
+        ref_e = emu.gemm_nt(A[rows], B[cols], math)
+        ee_, eb = check_emu("tmm 128x4096x16384", math, 16384, got[:, cols], ref_e)
+        err = max_rel(ref_rows[:, cols], got[:, cols])
+        record(f"tmm 128x4096x16384 sampled ({kern})", math, 16384, err, None, None, ee_, eb)
+        assert err <= tol(math, 16384)
