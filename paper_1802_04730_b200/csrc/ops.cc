@@ -691,12 +691,12 @@ double tcTolerance(const Problem& p, int math) {
   // partials, MMA grouping). That difference is ~K * 2^-24 * |partial sums|:
   // the bound is 4 * K * 2^-24 per contraction (tests/tc_emulate.py, the
   // same accumulator-only bound the GPU parity tests hold the kernels to
-  // against an fp64 emulation, doubled for two plans). Chained contractions
+  // against an fp64 emulation, doubled for two plans; x3 for 3xtf32, which
+  // issues three MMAs into the accumulator per k). Chained contractions
   // (FC layers, 3-KRU) carry a layer's difference into the next layer's sum
   // over its inputs, so their bound is 64 * sum(K) * 2^-24. A plan that drops
   // or repeats a 32-deep k-block is off by ~1e-1 relative, far outside both.
-  (void)math;
-  const double u = std::ldexp(1.0, -24);
+  const double u = std::ldexp(1.0, -24) * (math == k::kMath3xTf32 ? 3 : 1);
   switch (p.family) {
     case Family::Gemm: return 4.0 * p.gemm.K * u;
     case Family::Gconv: return 4.0 * ((double)p.gconv.C * p.gconv.KH * p.gconv.KW + p.gconv.Mb) * u;

@@ -13,9 +13,9 @@ feed the tensor cores, accumulated in fp64:
           accumulator (tc_gemm.cu); lo*lo is dropped. Product sums in fp64.
 
 What separates a kernel's output from the emulation is then only the fp32
-rounding of the accumulator (<= ~K * 2^-24 of the partial-sum magnitude,
-~sqrt(K) * 2^-24 typically), so the bound `tol_emu` is four orders of
-magnitude tighter than the operand-rounding bound K * 2^-11 it replaces: a
+rounding of the accumulator (~K * 2^-24 of the partial-sum magnitude per MMA
+issued per k: one for tf32, three for 3xtf32), so the bound `tol_emu` is four
+orders of magnitude tighter than the operand-rounding bound K * 2^-11 it replaces: a
 kernel that dropped one 32-deep k-block (~0.1 relative at K = 1024) fails it
 by three orders of magnitude (test_emulation_catches_dropped_kblock).
 """
@@ -59,10 +59,12 @@ def fc_relu(I, W, bias, math):
     return np.maximum(bias.astype(np.float64) + gemm_nt(I, W, math), 0.0)
 
 
-def tol_emu(K, scale=1.0, c=1.0):
+def tol_emu(K, scale=1.0, math="tf32"):
     """Bound on max|got - emu| / max(|emu|, 1) for a K-deep fp32-accumulated
-    tensor-core reduction of operands with max|a| * max|b| = scale."""
-    return c * K * 2.0 ** -24 * max(1.0, scale)
+    tensor-core reduction of operands with max|a| * max|b| = scale: K * 2^-24
+    per MMA issued into the accumulator for each k (3xtf32 issues three:
+    lo*hi, hi*lo, hi*hi)."""
+    return (3 if math == "3xtf32" else 1) * K * 2.0 ** -24 * max(1.0, scale)
 
 
 def gconv_points(I, W1, Bv, idx, math):

@@ -6,7 +6,8 @@ bar is a stated tolerance, on maxRelError
 
   1. against the tensor-core emulation (tests/tc_emulate.py: the operands
      rounded exactly as the kernels round them, products summed in fp64):
-       both modes:  <= tol_emu(K) = K * 2^-24 * max(1, max|a| max|b|)
+       <= tol_emu(K) = r * K * 2^-24 * max(1, max|a| max|b|), r = the MMAs
+          issued into the accumulator per k (tf32: 1, 3xtf32: 3)
      — only the fp32 accumulator's rounding separates the two, so a kernel
      that dropped one 32-deep k-block (~0.1 relative) fails by ~1000x;
   2. against the oracle (the reference's own fp32 chain), the operand-
@@ -53,7 +54,7 @@ def record(name, math, K, err, exact_err, oracle_exact_err, emu_err=None, emu_bo
 def check_emu(name, math, K, got, ref_emu, scale=1.0):
     """The tight bar: got vs the tensor-core emulation."""
     e = max_rel(ref_emu, got)
-    b = emu.tol_emu(K, scale)
+    b = emu.tol_emu(K, scale, math)
     assert e <= b, f"{name} {math}: maxRel vs emulation {e:.3g} > {b:.3g}"
     return e, b
 

@@ -50,14 +50,14 @@ def test_emulation_catches_dropped_kblock():
         ref = emu.gemm_nt(A, B, math)
         # an fp32-accumulated result (what a correct kernel produces)
         good = ref.astype(np.float32)
-        assert max_rel(ref, good) <= emu.tol_emu(K)
+        assert max_rel(ref, good) <= emu.tol_emu(K, math=math)
         # one 32-deep k-block missing
         bad = (ref - emu.gemm_nt(A[:, 256:288], B[:, 256:288], math)).astype(np.float32)
         e = max_rel(ref, bad)
-        assert e > 100 * emu.tol_emu(K), (math, e)
+        assert e > 100 * emu.tol_emu(K, math=math), (math, e)
         # a k-block whose products are scaled by (1 + 2^-8) (e.g. a wrong
         # descriptor offset reading a neighbouring, nearly equal value) slips
         # under the old operand-rounding bound K * 2^-11, not under tol_emu
         bad = (ref + 2.0 ** -8 * emu.gemm_nt(A[:, 256:288], B[:, 256:288], math)).astype(np.float32)
         e = max_rel(ref, bad)
-        assert emu.tol_emu(K) < e < K * 2.0 ** -11, (math, e)
+        assert emu.tol_emu(K, math=math) < e < K * 2.0 ** -11, (math, e)
