@@ -73,6 +73,36 @@ TC_OPS = [("tmm 128x1024x1024", "3xtf32"), ("tmm 128x1024x1024", "tf32"),
 INT_PARAMS = {"2LUT": {1, 3}, "1LUT": {1}}
 
 
+def step_set_bytes():
+    """Bytes of one input+weight+output set of the step (all three ops), from
+    the shapes alone: both arms derive the same `config` from it."""
+    b = 0
+    for name, shapes, seeded in STEP_OPS:
+        b += sum(4 * int(np.prod(s)) for s in shapes)
+    # outputs: TBMM Z, 2FCRelu O1+O2, MLP3 O1..O4
+    b += 4 * (500 * 26 * 26 + 128 * 128 + 128 * 64 + 128 * 128 + 128 * 64 + 128 * 32 + 128 * 2)
+    return b
+
+
+def step_config(world):
+    """The `config` object both arms print (same dict => same_config)."""
+    nsets = max(2, int(np.ceil(2 * L2_BYTES / step_set_bytes())))
+    return {"workload": STEP_WORKLOAD + " (BASELINE.json configs[1])",
+            "global_batch": {"tbmm": 500 * world, "fc": 128 * world}, "parallelism": f"dp{world}",
+            "l2": f"{nsets} rotating input+weight sets ({nsets * step_set_bytes() / 2**20:.0f} MiB > 2x L2)",
+            "flops_per_step_per_rank": 90369280}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -324,8 +354,36 @@ def cpu_baseline(budget_s=15.0):
     while tt < budget_s:
         f, dt = cs.sample(n)
         fl, tt = fl + f, tt + dt
-    return fl / tt / 1e9, {"kind": cs.kind, "cores": cs.threads,
+    return fl / tt / 1e9, {"kind": cs.kind, "cores": cs.threads, "cpu_model": cpu_model(),
                            "sample": cs.describe(n) + f"; {tt:.1f} s timed"}
+
+
+def cpu_baseline_port(budget_s=8.0):
+    """The restated loop nests (oracle/oracle.c, OpenMP over the batch on all
+    host threads: BASELINE.md section 3 path 2) over
+    whole steps of the same workload: the honest compiled-CPU comparison
+    beside the tree-walking interpreter."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import Oracle
+    orc = Oracle()
+    threads = os.cpu_count() or 1
+    orc.lib.orc_set_threads(threads)
+    rng = orc.rng(7)
+    X, Y = rng.f32((500, 26, 72)), rng.f32((500, 26, 72))
+    I, W1, B1, W2, B2 = (rng.f32((128, 1128)), rng.f32((128, 1128)), rng.f32((128,)), rng.f32((64, 128)),
+                         rng.f32((64,)))
+    O1 = rng.f32((128, 128))
+    M = [rng.f32((64, 128)), rng.f32((64,)), rng.f32((32, 64)), rng.f32((32,)), rng.f32((2, 32)), rng.f32((2,))]
+    steps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s or steps < 1:
+        orc.tbmm(X, Y)
+        orc.fc_relu(orc.fc_relu(I, W1, B1), W2, B2)
+        orc.mlp3(O1, *M)
+        steps += 1
+    dt = time.perf_counter() - t0
+    return 90369280 * steps / dt / 1e9, {"kind": "port", "cores": threads, "cpu_model": cpu_model(),
+                                         "sample": f"{steps} whole steps of the restated C loops (OpenMP), "
+                                                   f"{dt:.1f} s timed"}
 
 
 def reference_arm(args, rank, world):
@@ -351,17 +409,42 @@ def reference_arm(args, rank, world):
         "ms_per_step": round(step_flops / (value * 1e9) * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (U[-1,1) fp32, seeded)",
-        "config": {"workload": STEP_WORKLOAD, "parallelism": f"dp{args.gpus}",
-                   "note": "reference CPU interpreter on a bounded sample per step; ms_per_step is "
-                           "the full step's FLOPs at the measured rate"},
+        "config": step_config(args.gpus),
+        "note": "reference CPU interpreter on a bounded sample per step; ms_per_step is the full step's FLOPs "
+                "at the measured rate",
         "cpu_baseline": {"value": round(value, 6), "unit": "GFLOP/s", "kind": cs.kind, "cores": cs.threads,
-                         "sample": cs.describe(n)},
+                         "sample": cs.describe(n), "cpu_model": cpu_model()},
         "e2e": {"value": round(value, 6), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------- main arm
+def _free_port():
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-exec this script under
+    torch.distributed.run with N local ranks (one process per GPU), exactly
+    as the driver launches it. Fails loudly when the box has fewer GPUs."""
+    import subprocess
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus and not args.allow_shared_gpu:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this box has {have}", file=sys.stderr)
+        sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -372,6 +455,9 @@ def main():
     ap.add_argument("--serial-step", action="store_true", help="run the step's operators back to back on one stream")
     ap.add_argument("--no-ops", action="store_true", help="skip the per-op paper table")
     ap.add_argument("--profile-only", action="store_true", help="run a few steps, print nothing (ncu)")
+    ap.add_argument("--allow-shared-gpu", action="store_true",
+                    help="testing only: let N ranks share fewer GPUs (rank r on cuda:r %% count); NCCL is then "
+                         "replaced by gloo for the gather")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -380,16 +466,30 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return reference_arm(args, rank, world)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
 
     import torch
     import torch.distributed as dist
 
     from paper_1802_04730_b200 import ExecutionEngine, device_info, measure_peaks
 
+    ndev = torch.cuda.device_count()
+    if world > ndev and not args.allow_shared_gpu:
+        print(f"bench.py: {world} ranks need {world} GPUs, this box has {ndev}", file=sys.stderr)
+        sys.exit(2)
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    shared = world > ndev
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     peaks, peak_src = load_peaks()
     peaks = dict(peaks)
     mp = measure_peaks(local)  # measured now, this GPU
@@ -398,113 +498,159 @@ def main():
     ee = ExecutionEngine()
 
     # rotating input sets larger than L2 (inputs AND weights rotate)
-    probe = [OpInstance(ee, torch, n, s, sd, 1, dev, 0) for n, s, sd in STEP_OPS]
-    set_bytes = sum(o.set_bytes() for o in probe)
-    nsets = max(2, int(np.ceil(2 * L2_BYTES / set_bytes)))
+    nsets = max(2, int(np.ceil(2 * L2_BYTES / step_set_bytes())))
     ops = [OpInstance(ee, torch, n, s, sd, nsets, dev, 1 + i + 100 * rank) for i, (n, s, sd) in
            enumerate(STEP_OPS)]
-    del probe
+    set_bytes = sum(o.set_bytes() for o in ops)
     flops_step = sum(o.flops for o in ops)
     stream = torch.cuda.Stream(device=dev)
     # the step's three operators are independent: inside the graph they fork
     # onto their own streams and join back (concurrent kernels share the SMs)
     side = [torch.cuda.Stream(device=dev) for _ in ops]
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev if not shared else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     with torch.cuda.stream(stream):
-        def step(i):
+        def fork_join(i, body):
             if args.serial_step:
                 for o in ops:
-                    o.run(i)
+                    body(o, i)
                 return
             # every operator on its own side stream; the main stream only
-            # forks and joins (profiles/r01_concurrency.txt: ~2 us/step better
-            # than running the first operator on the joining stream)
+            # forks and joins (profiles/r01_concurrency.txt)
             for sd in side:
                 sd.wait_stream(stream)
             for o, sd in zip(ops, side):
                 with torch.cuda.stream(sd):
-                    o.run(i)
+                    body(o, i)
             for sd in side:
                 stream.wait_stream(sd)
 
-        # one CUDA graph per input set (3 launches each), plus one graph of
-        # all nsets steps back to back (no graph-launch gap between steps;
-        # every step still joins before the next forks)
+        def step(i):
+            fork_join(i, lambda o, k: o.run(k))
+
+        def graph_of(fn, idx):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for i in idx:
+                    fn(i)
+            return g
+
         for i in range(nsets):
             step(i)
         torch.cuda.synchronize()
-        graphs = []
-        for i in range(nsets):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                step(i)
-            graphs.append(g)
-        g_all = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_all, stream=stream):
-            for i in range(nsets):
-                step(i)
-        for i in range(args.warmup):
-            graphs[i % nsets].replay()
-        g_all.replay()
+        # K steps = (K // nsets) replays of a graph of all nsets steps + one
+        # graph of the K % nsets remaining steps: every step sits inside a
+        # graph beside its neighbours, whatever K is
+        g_all = graph_of(step, range(nsets))
+        full, rest = divmod(args.steps, nsets)
+        g_rest = graph_of(step, range(rest)) if rest else None
+        schedule = [g_all] * full + ([g_rest] if g_rest else [])
+        for i in range(-(-args.warmup // nsets)):  # >= W warm-up steps
+            g_all.replay()
+        if g_rest:
+            g_rest.replay()
         torch.cuda.synchronize()
         if args.profile_only:
-            for i in range(args.steps):
-                graphs[i % nsets].replay()
+            for g in schedule:
+                g.replay()
             torch.cuda.synchronize()
             return
 
-        # K steps = (K // nsets) replays of the all-sets graph + K % nsets single steps
-        full, rest = divmod(args.steps, nsets)
-        schedule = [g_all] * full + graphs[:rest]
-
         # ---- timed region: K steps, barrier + sync both sides, max over ranks
-        if world > 1:
-            dist.barrier()
+        barrier()
         torch.cuda.synchronize()
         with ClockSampler(dev) as clk:
             el = time_device(torch, lambda i: schedule[i].replay(), len(schedule), stream)
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-            t = torch.tensor([el], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        barrier()
+        el = max_over_ranks(el)
         value = world * flops_step * args.steps / el / 1e9
         ms_step = el / args.steps * 1e3
 
-        # ---- N > 1: the same step plus the all-gather of every output over
-        # NCCL (compute-only above, compute + gather here)
-        gather = None
+        # ---- N > 1: strong scaling: ONE global step (TBMM
+        # B=500, FC B=128) split over the ranks through tcb_run_shard
+        # (500 -> 250 / 125 / 63x4+62x4, 128 -> 64 / 32 / 16), compute only and
+        # compute + the all-gather of every output slice (NCCL)
+        strong = None
         if world > 1:
-            outs = [t for o in ops for i, t in enumerate(o.sets[0][1]) if i not in o.inout or o.name == "MLP3"]
-            bufs = [torch.empty((world,) + tuple(t.shape), device=dev, dtype=t.dtype) for t in outs]
+            from paper_1802_04730_b200.shard import BATCH_DIMS
 
-            def step_gather(i):
-                graphs[i % nsets].replay()
-                for t, b in zip(outs, bufs):
-                    dist.all_gather_into_tensor(b, t)
+            def shard_body(o, k):
+                ps, os_ = o.sets[k % nsets]
+                ee.run_shard(o.handle, ps, os_, rank, world, check_errors=False)
+
+            def sstep(i):
+                fork_join(i, shard_body)
+
+            # gather buffers: every batched return, padded to the largest slice
+            gat = []
+            for o in ops:
+                lo, hi, n = ee.shard_range(o.handle, rank, world)
+                mx = ee.shard_range(o.handle, 0, world)[1]
+                for ri in sorted(BATCH_DIMS[o.name][1]):
+                    if o.name == "MLP3" and ri == 0:
+                        continue  # O1 is a read-only pass-through input
+                    t = o.sets[0][1][ri]
+                    pad = torch.zeros((mx,) + tuple(t.shape[1:]), device=dev)
+                    allb = torch.empty((world * mx,) + tuple(t.shape[1:]), device=dev)
+                    gat.append((o, ri, lo, hi, pad, allb))
+
+            def gather(i):
+                for o, ri, lo, hi, pad, allb in gat:
+                    pad[: hi - lo].copy_(o.sets[i % nsets][1][ri][lo:hi])
+                    if shared:
+                        torch.cuda.current_stream().synchronize()
+                        parts = list(allb.cpu().chunk(world))
+                        dist.all_gather(parts, pad.cpu())
+                    else:
+                        dist.all_gather_into_tensor(allb, pad)
 
             for i in range(3):
-                step_gather(i)
-            dist.barrier()
-            kg = max(10, args.steps // 10)
-            eg = time_device(torch, step_gather, kg, stream)
-            t = torch.tensor([eg], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            eg = float(t.item())
-            gather = {"ms_per_step": round(eg / kg * 1e3, 5),
-                      "value": round(world * flops_step * kg / eg / 1e9, 3), "unit": "GFLOP/s",
-                      "gathered_bytes_per_rank": int(sum(t.numel() * 4 for t in outs)),
-                      "collective": "NCCL all_gather_into_tensor per output, after every step"}
+                sstep(i)
+                gather(i)
+            torch.cuda.synchronize()
+            gs_all = graph_of(sstep, range(nsets))
+            for _ in range(3):
+                gs_all.replay()
+            torch.cuda.synchronize()
+            reps = max(2, args.steps // nsets)
+            barrier()
+            ec = max_over_ranks(time_device(torch, lambda i: gs_all.replay(), reps, stream))
+            kg = max(10, min(200, args.steps // 10))
+            barrier()
+
+            def step_gather(i):
+                sstep(i)
+                gather(i)
+
+            eg = max_over_ranks(time_device(torch, step_gather, kg, stream))
+            strong = {"split": {o.name: [list(ee.shard_range(o.handle, r, world)[:2]) for r in range(world)]
+                                for o in ops},
+                      "ms_per_step_compute": round(ec / (reps * nsets) * 1e3, 5),
+                      "value_compute": round(flops_step * reps * nsets / ec / 1e9, 3),
+                      "ms_per_step_with_allgather": round(eg / kg * 1e3, 5),
+                      "value_with_allgather": round(flops_step * kg / eg / 1e9, 3), "unit": "GFLOP/s",
+                      "gathered_bytes_per_rank": int(sum(p.numel() * 4 for *_, p, _ in gat)),
+                      "collective": ("gloo (shared GPU, testing)" if shared else
+                                     "NCCL all_gather_into_tensor per output slice, after every step"),
+                      "timing": "compute: CUDA graph of %d steps (tcb_run_shard per op, forked), max over "
+                                "ranks; with_allgather: %d eager steps incl. the gathers" % (nsets, kg)}
 
         # ---- per-op device time inside the step (same stream, L2-rotated):
         # one graph launches the op on every rotating input set back to back
         per_op = []
         for o in ops:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for i in range(nsets):
-                    o.run(i)
+            g = graph_of(lambda i: o.run(i), range(nsets))
             for i in range(3):
                 g.replay()
             reps = max(4, args.steps // nsets)
@@ -542,16 +688,15 @@ def main():
                 st.synchronize()
 
         # untimed warm-up: the first host calls run slow (pinned-page and IOMMU
-        # mappings warming up; blocks of 50 after 200 warm-up calls still fell
-        # 441, 408, 300, 278, 270 us on one box), ~0.3 s
+        # mappings warming up), ~0.3 s
         for i in range(max(args.warmup, 1000)):
             e2e_step(i)
         # host wall clock (each step ends with its outputs on the host), in 5
-        # blocks of kb steps; the median block is reported (one-off host
-        # hiccups do not decide the number; all blocks are listed)
+        # blocks of kb steps; the median block is reported
         kb = max(4, args.steps // 20)
         ke = 5 * kb
         blocks = []
+        barrier()
         for b in range(5):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -559,11 +704,7 @@ def main():
                 e2e_step(b * kb + i)
             torch.cuda.synchronize()
             blocks.append(time.perf_counter() - t0)
-        e2e_t = sorted(blocks)[2] * 5
-        if world > 1:
-            t = torch.tensor([e2e_t], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_t = float(t.item())
+        e2e_t = max_over_ranks(sorted(blocks)[2] * 5)
         e2e_value = world * flops_step * ke / e2e_t / 1e9
 
     if rank != 0:
@@ -578,9 +719,11 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = dom.bytes / dom_t / 1e9
     traffic = None
-    try:  # committed ncu --set full capture of the same kernel (profiles/gpu_round.sh)
+    try:  # committed ncu --set full capture of the same kernel
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f)["per_launch"].get(dom.name, {}).get("dram_bytes")
+            tj = json.load(f)["per_launch"].get(dom.name, {})
+            if tj.get("kernel") in (None, dom.kernel):
+                traffic = tj.get("dram_bytes")
     except Exception:
         traffic = None
     roofline = {"bound": "hbm", "kernel": f"{dom.name}: {dom.kernel}", "achieved": round(achieved, 1),
@@ -592,25 +735,23 @@ def main():
                 "note": "FFMA-exact fp32 kernels: no tensor-core roofline applies; HBM roofline over the "
                         "kernel's algorithmic bytes (inputs once, outputs once). " + DOM_NOTES.get(dom.name, ""),
                 "chain_floor_us": round(chain_floor_us(dom), 3)}
-    tbmm = [x for x in per_op if x[0].name == "tbmm"][0]
     roofline_ops = {
         o.name: {"us": round(t * 1e6, 3), "gflops": round(o.flops / t / 1e9, 1),
                  "hbm_gbs": round(o.bytes / t / 1e9, 1), "hbm_frac": round(o.bytes / t / 1e9 / hbm_peak, 4),
                  "ffma_frac": round(o.flops / t / 1e12 / peaks["ffma_tflops"], 4),
+                 "chain_floor_us": round(chain_floor_us(o), 3),
                  "share": round(t / step_dev, 3), "kernel": o.kernel} for o, t in per_op}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (U[-1,1) fp32, seeded)",
-        "config": {"workload": STEP_WORKLOAD + " (BASELINE.json configs[1])",
-                   "global_batch": {"tbmm": 500 * world, "fc": 128 * world}, "parallelism": f"dp{world}",
-                   "l2": f"{nsets} rotating input+weight sets ({nsets * set_bytes / 2**20:.0f} MiB > 2x L2)",
-                   "graphs": "one CUDA graph of all %d input sets' steps (3 kernel launches each, "
-                             "replayed K // %d times, + K %% %d single-step graphs)" % (nsets, nsets, nsets) + (
+        "config": step_config(world),
+        "timing": {"graphs": "K // %d replays of one CUDA graph of all %d input sets' steps + one graph of the "
+                             "K %% %d remaining steps (3 kernel launches per step)" % (nsets, nsets, nsets) + (
                        ", operators serialised on one stream" if args.serial_step else
                        ", the 3 independent operators forked onto 3 streams and joined"),
-                   "flops_per_step": int(flops_step)},
+                   "set_bytes": int(set_bytes), "nsets": nsets},
         "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "us_per_step": round(e2e_t / ke * 1e6, 2),
                 "timing": "host wall clock, median of 5 blocks of %d steps; each step = the 3 tcb_run calls with "
@@ -618,7 +759,7 @@ def main():
                           "synchronised" % kb,
                 "blocks_us_per_step": [round(x / kb * 1e6, 2) for x in blocks]},
         "gpu_launches": 3 * args.steps,
-        "with_allgather": gather,
+        "strong": strong,
         "roofline": roofline,
         "step_ops": roofline_ops,
         "clocks": clk.summary(),
@@ -634,6 +775,8 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         v, info = cpu_baseline()
         line["cpu_baseline"] = {"value": round(v, 6), "unit": "GFLOP/s", **info}
+        v, info = cpu_baseline_port()
+        line["cpu_baseline_port"] = {"value": round(v, 6), "unit": "GFLOP/s", **info}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

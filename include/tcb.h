@@ -151,6 +151,22 @@ int tcb_compile_ex(tcb_engine* e, const char* name, const tcb_tensor* inputs, in
 int tcb_run(tcb_engine* e, uint64_t handle, const tcb_tensor* inputs, int n_inputs,
             const tcb_tensor* outputs, int n_outputs, void* stream, int flags, int64_t* duration_ns);
 
+/* Batch sharding, one process per GPU (the reference has
+ * no distributed code — the paper used several GPUs only to tune,
+ * PAPER.md:1512-1521). Every registered form has one independent outer
+ * dimension (TMM/C3 rows, TBMM batches, FC-chain rows, 3-KRU M, gconv N,
+ * LUT rows) and no reduction across it. tcb_shard_range gives rank `rank`'s
+ * balanced contiguous slice [lo, hi) of that dimension (the first
+ * extent % world ranks get one extra: TBMM 500 over 8 = 63 x 4, 62 x 4).
+ * tcb_run_shard runs only that slice of a handle compiled for the FULL
+ * shapes, reading and writing the full device tensors in place (weights
+ * replicated on every rank). The caller then all-gathers the output slices
+ * (ncclAllGather / torch.distributed; shard.py does it). No host tensors. */
+int tcb_shard_range(tcb_engine* e, uint64_t handle, int rank, int world, int64_t* lo, int64_t* hi,
+                    int64_t* extent);
+int tcb_run_shard(tcb_engine* e, uint64_t handle, const tcb_tensor* inputs, int n_inputs,
+                  const tcb_tensor* outputs, int n_outputs, int rank, int world, void* stream, int flags);
+
 /* synchronises the handle's last stream and reports a device-side error
  * (IndexOutOfRange from a data-dependent subscript) raised since the last check */
 int tcb_check(tcb_engine* e, uint64_t handle);

@@ -480,6 +480,75 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
   });
 }
 
+int tcb_shard_range(tcb_engine* e, uint64_t h, int rank, int world, int64_t* lo, int64_t* hi, int64_t* extent) {
+  return guarded([&] {
+    Compiled* cp;
+    {
+      std::lock_guard<std::mutex> g(e->mu);
+      cp = &e->handle(h);
+    }
+    const int64_t n = ops::shardExtent(cp->prob);
+    int64_t a = 0, b = 0;
+    ops::shardRange(n, rank, world, &a, &b);
+    if (lo) *lo = a;
+    if (hi) *hi = b;
+    if (extent) *extent = n;
+  });
+}
+
+int tcb_run_shard(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_tensor* out, int nout,
+                  int rank, int world, void* stream, int flags) {
+  return guarded([&] {
+    Compiled* cp;
+    {
+      std::lock_guard<std::mutex> g(e->mu);
+      cp = &e->handle(h);
+    }
+    Compiled& c = *cp;
+    const auto& params = c.spec.v.def.params;
+    const auto& rets = c.spec.v.def.rets;
+    if (nin != static_cast<int>(params.size()) || nout != static_cast<int>(rets.size()))
+      fail(ErrorKind::ShapeMismatch, "run_shard: wrong number of inputs or outputs for '" + c.name + "'");
+    auto checkT = [&](const tcb_tensor& t, const std::string& nm, bool isInt) {
+      if (shapeOf(t) != c.spec.shapes.at(nm))
+        fail(ErrorKind::ShapeMismatch, "run_shard: tensor '" + nm + "' does not have the compiled (full) shape");
+      if (t.dtype != (isInt ? TCB_I32 : TCB_F32)) fail(ErrorKind::ShapeMismatch, "run_shard: tensor '" + nm + "' has the wrong dtype");
+      if (!t.data) fail(ErrorKind::Io, "run_shard: tensor '" + nm + "' has no data");
+      if (t.location == TCB_HOST) fail(ErrorKind::Io, "run_shard: shards run on device tensors (one process per GPU)");
+    };
+    std::vector<void*> din(nin), dout(nout);
+    for (int i = 0; i < nin; ++i) {
+      if (!params[i].scalar()) checkT(in[i], params[i].name, params[i].elem == lang::Elem::Int);
+      din[i] = in[i].data;
+    }
+    for (int i = 0; i < nout; ++i) {
+      checkT(out[i], rets[i], false);
+      dout[i] = out[i].data;
+    }
+    int64_t lo = 0, hi = 0;
+    ops::shardRange(ops::shardExtent(c.prob), rank, world, &lo, &hi);
+    if (hi == lo) return;
+    ops::Problem q = ops::shardOf(c.prob, lo, hi, din, dout);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::lock_guard<std::mutex> rg(c.runMu);
+    if (!c.dErr) {
+      cudaOk(cudaMalloc(&c.dErr, sizeof(int)), "cudaMalloc");
+      cudaOk(cudaMemset(c.dErr, 0, sizeof(int)), "cudaMemset");
+    }
+    c.lastStream = s;
+    ops::launch(q, c.map, din.data(), dout.data(), c.dErr, s);
+    if (c.prob.family == ops::Family::Lut && !(flags & (TCB_RUN_NOCHECK | TCB_RUN_ASYNC))) {
+      int flag = 0;
+      cudaOk(cudaMemcpyAsync(&flag, c.dErr, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+      cudaOk(cudaStreamSynchronize(s), "sync");
+      if (flag) {
+        cudaOk(cudaMemset(c.dErr, 0, sizeof(int)), "cudaMemset");
+        fail(ErrorKind::IndexOutOfRange, "a data-dependent subscript escaped its tensor's extent");
+      }
+    }
+  });
+}
+
 int tcb_check(tcb_engine* e, uint64_t h) {
   return guarded([&] {
     Compiled* cp;

@@ -788,6 +788,93 @@ GenePools genePools(const Problem& p, int math) {
   return g;
 }
 
+int64_t shardExtent(const Problem& p) {
+  switch (p.family) {
+    case Family::Gemm: return p.gemm.batch > 1 ? p.gemm.batch : p.gemm.M;
+    case Family::FcChain: return p.fc.batch;
+    case Family::Kru3: return p.kru.M;
+    case Family::Gconv: return p.gconv.N;
+    case Family::Lut: return p.lut.empty() ? 0 : p.lut[0].B;
+  }
+  return 0;
+}
+
+void shardRange(int64_t n, int rank, int world, int64_t* lo, int64_t* hi) {
+  if (world < 1 || rank < 0 || rank >= world) fail(ErrorKind::MappingInvalid, "shard: rank outside [0, world)");
+  const int64_t base = n / world, extra = n % world;
+  *lo = rank * base + std::min<int64_t>(rank, extra);
+  *hi = *lo + base + (rank < extra ? 1 : 0);
+}
+
+Problem shardOf(const Problem& p, int64_t lo, int64_t hi, std::vector<void*>& in, std::vector<void*>& out) {
+  if (lo < 0 || hi < lo || hi > shardExtent(p)) fail(ErrorKind::MappingInvalid, "shard: range outside the batch");
+  Problem q = p;
+  const int n = static_cast<int>(hi - lo);
+  // elements per batch row of every batched tensor (each Ref offset once:
+  // MLP3's batch input O1 is also its first return)
+  std::vector<std::pair<Ref, int64_t>> rows;
+  auto add = [&](const Ref& r, int64_t per) {
+    if (!r.valid()) return;
+    for (const auto& x : rows)
+      if (x.first.out == r.out && x.first.idx == r.idx) return;
+    rows.push_back({r, per});
+  };
+  switch (p.family) {
+    case Family::Gemm: {
+      const GemmDesc& g = p.gemm;
+      if (g.batch > 1) {
+        add(g.A, g.sA);
+        add(g.B, g.sB);
+        add(g.C, g.sC);
+        q.gemm.batch = n;
+      } else {
+        add(g.A, g.lda);
+        add(g.C, g.ldc);
+        q.gemm.M = n;
+      }
+      q.flops = p.flops * n / std::max<int64_t>(1, shardExtent(p));
+      break;
+    }
+    case Family::FcChain:
+      add(p.fc.I, p.fc.ldi);
+      for (const auto& L : p.fc.layers) add(L.O, L.out);
+      q.fc.batch = n;
+      break;
+    case Family::Kru3: {
+      const KruDesc& k = p.kru;
+      add(k.X, (int64_t)k.N0 * k.N1 * k.N2);
+      add(k.Y, (int64_t)k.D0 * k.D1 * k.D2);
+      add(k.XW1, (int64_t)k.N0 * k.D1 * k.D2);
+      add(k.XW2, (int64_t)k.N0 * k.N1 * k.D2);
+      q.kru.M = n;
+      break;
+    }
+    case Family::Gconv: {
+      const GconvDesc& g = p.gconv;
+      add(g.I, (int64_t)g.G * g.C * g.H * g.W);
+      add(g.O, (int64_t)g.G * g.F * (g.H - g.KH + 1) * (g.W - g.KW + 1));
+      q.gconv.N = n;
+      break;
+    }
+    case Family::Lut:
+      for (size_t t = 0; t < p.lut.size(); ++t) {
+        add(p.lut[t].I, p.lut[t].L);
+        add(p.lut[t].O, p.lut[t].D);
+        q.lut[t].B = n;
+      }
+      break;
+  }
+  for (const auto& x : rows) {
+    std::vector<void*>& v = x.first.out ? out : in;
+    v[x.first.idx] = static_cast<char*>(v[x.first.idx]) + lo * x.second * 4;  // fp32 / int32 elements
+  }
+  if (p.family != Family::Gemm) {
+    const double f = (double)n / std::max<int64_t>(1, shardExtent(p));
+    q.flops = p.flops * f;
+  }
+  return q;
+}
+
 void launch(const Problem& p, const Mapping& m, void* const* in, void* const* out, int* errFlag, cudaStream_t s) {
   auto ptr = [&](const Ref& r) -> void* { return r.out ? out[r.idx] : in[r.idx]; };
   auto check = [](cudaError_t e, const char* what) {

@@ -123,6 +123,15 @@ GenePools genePools(const Problem& p, int math = k::kMathFfma);
 // max |got - ref| / max(|ref|, 1); see ops.cc
 double tcTolerance(const Problem& p, int math);
 
+// Batch sharding: every registered form has one
+// independent outer dimension (TBMM/C3/TMM/FC rows, 3-KRU M, gconv N, LUT B)
+// with no reduction across it. shardExtent() is its length; shardOf()
+// rewrites a problem and its tensor pointers so the launch covers only
+// [lo, hi) of that dimension, reading and writing the full tensors in place.
+int64_t shardExtent(const Problem& p);
+void shardRange(int64_t n, int rank, int world, int64_t* lo, int64_t* hi);  // balanced contiguous split
+Problem shardOf(const Problem& p, int64_t lo, int64_t hi, std::vector<void*>& in, std::vector<void*>& out);
+
 // Launches the whole definition on `stream`. in/out are device pointers in
 // declaration order. errFlag: device int for data-dependent index checks.
 void launch(const Problem& p, const Mapping& m, void* const* in, void* const* out, int* errFlag,

@@ -157,6 +157,24 @@ class ExecutionEngine:
                           C.byref(dur)))
         return dur.value if profile else None
 
+    def shard_range(self, handle, rank, world):
+        """(lo, hi, extent): rank's balanced slice of the handle's batch
+        dimension (tcb_shard_range)."""
+        lo, hi, n = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.tcb_shard_range(self._h, handle, rank, world, C.byref(lo), C.byref(hi), C.byref(n)))
+        return lo.value, hi.value, n.value
+
+    def run_shard(self, handle, inputs, outputs, rank, world, stream=None, check_errors=True):
+        """Runs only this rank's batch slice of a handle compiled for the
+        full shapes, in place on the full device tensors (tcb_run_shard)."""
+        ins, nin = _arr(inputs)
+        outs, nout = _arr(outputs)
+        if stream is None and torch is not None:
+            stream = torch.cuda.current_stream().cuda_stream
+        flags = 0 if check_errors else _lib.TCB_RUN_NOCHECK
+        check(lib.tcb_run_shard(self._h, handle, ins, nin, outs, nout, rank, world, C.c_void_p(stream or 0),
+                                flags))
+
     def check(self, handle):
         check(lib.tcb_check(self._h, handle))
 

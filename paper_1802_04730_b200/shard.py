@@ -51,6 +51,43 @@ def shard_views(form, inputs, outputs, lo, hi):
     return ins, outs
 
 
+def gather_shards(form, outputs, n, group=None):
+    """All-gathers every batched return's rank slices (padded to the
+    largest shard) so each rank holds the full outputs."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, hi = shard_range(n, world, rank)
+    _, pout = BATCH_DIMS[form]
+    mx = shard_range(n, world, 0)[1]  # the largest shard (rank 0's)
+    for i in sorted(pout):
+        full = outputs[i]
+        pad = torch.zeros((mx,) + tuple(full.shape[1:]), dtype=full.dtype, device=full.device)
+        pad[: hi - lo].copy_(full[lo:hi])
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad, group=group)
+        for r, part in enumerate(parts):
+            a, b = shard_range(n, world, r)
+            if b > a and r != rank:
+                full[a:b].copy_(part[: b - a])
+
+
+def engine_sharded_run(ee, handle, form, inputs, outputs, group=None, gather=True, stream=None):
+    """This rank's slice through the C ABI (tcb_run_shard on the full device
+    tensors, a handle compiled for the full shapes), then the all-gather."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lo, hi, n = ee.shard_range(handle, rank, world)
+    ee.run_shard(handle, inputs, outputs, rank, world, stream=stream)
+    if gather and world > 1:
+        gather_shards(form, outputs, n, group)
+    return lo, hi
+
+
 def sharded_run(form, run_shard, inputs, outputs, group=None, gather=True):
     """Runs `run_shard(ins, outs)` on this rank's batch slice, then
     all-gathers every batched return so each rank holds the full outputs.

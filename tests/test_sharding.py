@@ -90,3 +90,22 @@ def test_every_form_has_a_batch_dimension():
     forms = [line.split("(")[0].split()[-1] for line in L.lib.tcb_builtin_ops().decode().splitlines()
              if line.startswith("def ")]
     assert sorted(forms) == sorted(BATCH_DIMS)
+
+
+def test_c_abi_shard_range_matches_python_split():
+    """tcb_shard_range (the C ABI a C++ host shards with) gives the same
+    balanced split as shard.py, on the operator's own batch dimension."""
+    from paper_1802_04730_b200 import ExecutionEngine
+    ee = ExecutionEngine()
+    X = np.zeros((500, 26, 72), np.float32)
+    h = ee.compile("tbmm", [X, X], [np.zeros((500, 26, 26), np.float32)])
+    for w in (1, 2, 3, 4, 8):
+        assert [ee.shard_range(h, r, w) for r in range(w)] == [shard_range(500, w, r) + (500,) for r in range(w)]
+    g = ee.compile("gconv", [np.zeros((32, 32, 16, 58, 58), np.float32), np.zeros((32, 16, 16, 3, 3), np.float32),
+                             np.zeros((16,), np.float32)], [np.zeros((32, 32, 16, 56, 56), np.float32)])
+    assert ee.shard_range(g, 3, 4) == (24, 32, 32)
+    m = ee.compile("MLP3", [np.zeros(s, np.float32) for s in [(128, 128), (64, 128), (64,), (32, 64), (32,),
+                                                              (2, 32), (2,)]],
+                   [np.zeros((128, 128), np.float32), np.zeros((128, 64), np.float32),
+                    np.zeros((128, 32), np.float32), np.zeros((128, 2), np.float32)])
+    assert ee.shard_range(m, 7, 8) == (112, 128, 128)
