@@ -1,0 +1,237 @@
+// fc_regs.cu — FC chains whose layers are all short reductions (MLP3:
+// 128 -> 64 -> 32 -> 2, proj/kernels/mlp3.tc:4-16; kred <= 128 per layer),
+// one CTA per R batch rows, no cluster, no shared-memory weight staging.
+//
+// The cluster kernel (fc_chain.cu) spends most of an MLP3 call before its
+// first FFMA: bulk-copy issue (~0.1-0.2 us per copy on the SM's TMA unit),
+// DSMEM pushes and cluster barriers between layers (fc_trace: the first
+// layer's data lands ~5400 cycles after entry; the whole chain is ~1100
+// cycles of FFMA latency). Here every warp is assigned to one layer and one
+// lane to one output column of it; at entry each lane issues plain 16-byte
+// global loads of its whole weight row (<= 32 float4 registers) and its
+// bias, and the CTA stages its R input rows in shared memory, so every
+// global load of the kernel is in flight within the first few hundred
+// cycles. Then layer by layer (one CTA barrier between layers) the layer's
+// lanes run their R chains from registers (weights) and shared-memory
+// broadcasts (activations), write the layer's return and leave the result
+// in shared memory for the next layer.
+//
+// Exactness: each (row, column) output is one lane's sequential FFMA chain
+// in ascending k from bias[o], then fmaxf(., 0) — the interpreter's order
+// (interpreter.cc:218-233; builtin fmaxf -> std::fmax, :22-24).
+#include "kernels.cuh"
+
+namespace tcb {
+namespace k {
+
+namespace {
+
+constexpr int kRegsKq = 32;  // float4s of one weight row held in registers (kred <= 128)
+
+struct FcRegsPlan {
+  int vecW[kMaxLayers];         // weight rows load as float4 (ldw % 4 == 0, 16-byte aligned)
+  int vecI;                     // input rows load as float4
+  int warpOff[kMaxLayers + 1];  // first warp of each layer
+  int ald[kMaxLayers + 1];      // activation row strides (floats, multiple of 4)
+  int actOff[kMaxLayers + 1];   // activation buffers in shared memory (floats)
+};
+
+__device__ __forceinline__ float4 ldsV4(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
+template <int NL, int R>
+__global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ FcChainArgs a,
+                                                       const __grid_constant__ FcRegsPlan p) {
+  extern __shared__ __align__(16) float act[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row0 = blockIdx.x * R;
+  const int rows = min(R, a.batch - row0);
+  int layer = -1;
+#pragma unroll
+  for (int l = 0; l < NL; ++l)
+    if (warp >= p.warpOff[l] && warp < p.warpOff[l + 1]) layer = l;
+
+  // ---- every global load up front: this lane's weight row and bias ...
+  float4 w[kRegsKq];
+  float bias = 0.0f;
+  int col = 0, K4 = 0, KT = 0;  // full float4 groups, tail steps (kred % 4)
+  bool live = false;
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    if (layer == l) {
+      col = (warp - p.warpOff[l]) * 32 + lane;
+      live = col < a.L[l].out;
+      K4 = a.L[l].kred >> 2;
+      KT = a.L[l].kred & 3;
+      const float* wr = a.L[l].W + (int64_t)min(col, a.L[l].out - 1) * a.L[l].ldw;
+      if (p.vecW[l]) {
+#pragma unroll
+        for (int q = 0; q < kRegsKq; ++q)
+          if (q < K4) w[q] = __ldg(reinterpret_cast<const float4*>(wr) + q);
+      } else {
+#pragma unroll
+        for (int q = 0; q < kRegsKq; ++q)
+          if (q < K4) w[q] = make_float4(__ldg(wr + 4 * q), __ldg(wr + 4 * q + 1), __ldg(wr + 4 * q + 2),
+                                         __ldg(wr + 4 * q + 3));
+      }
+#pragma unroll
+      for (int q = 0; q < kRegsKq; ++q)
+        if (q == K4 && KT) {
+          w[q].x = __ldg(wr + 4 * q);
+          w[q].y = KT > 1 ? __ldg(wr + 4 * q + 1) : 0.0f;
+          w[q].z = KT > 2 ? __ldg(wr + 4 * q + 2) : 0.0f;
+          w[q].w = 0.0f;
+        }
+      bias = live ? __ldg(a.L[l].bias + col) : 0.0f;
+    }
+  }
+  // ... and the CTA's input rows into shared memory (zero rows past the
+  // batch, zero columns past the reduction)
+  {
+    const int kr = a.L[0].kred, k0 = (kr + 3) >> 2;
+    float* a0 = act + p.actOff[0];
+    for (int e = tid; e < R * k0; e += blockDim.x) {
+      const int r = e / k0, q = e - r * k0;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      const float* src = a.I + (int64_t)(row0 + r) * a.ldi + 4 * q;
+      if (r < rows) {
+        if (p.vecI && 4 * q + 4 <= kr) {
+          v = __ldg(reinterpret_cast<const float4*>(src));
+        } else {
+          v.x = 4 * q < kr ? __ldg(src) : 0.0f;
+          v.y = 4 * q + 1 < kr ? __ldg(src + 1) : 0.0f;
+          v.z = 4 * q + 2 < kr ? __ldg(src + 2) : 0.0f;
+          v.w = 4 * q + 3 < kr ? __ldg(src + 3) : 0.0f;
+        }
+      }
+      reinterpret_cast<float4*>(a0 + r * p.ald[0])[q] = v;
+    }
+  }
+  __syncthreads();
+
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    if (layer == l) {
+      const float* in = act + p.actOff[l];
+      float acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = bias;
+#pragma unroll
+      for (int q = 0; q < kRegsKq; ++q) {
+        if (q < K4) {  // warp-uniform
+          float4 x[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) x[r] = ldsV4(in + r * p.ald[l] + 4 * q);  // broadcast
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].x, w[q].x, acc[r]);
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].y, w[q].y, acc[r]);
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].z, w[q].z, acc[r]);
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].w, w[q].w, acc[r]);
+        } else if (q == K4 && KT) {  // the kred % 4 tail steps, still in order
+          float4 x[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) x[r] = ldsV4(in + r * p.ald[l] + 4 * q);
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].x, w[q].x, acc[r]);
+          if (KT > 1) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].y, w[q].y, acc[r]);
+          }
+          if (KT > 2) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].z, w[q].z, acc[r]);
+          }
+        }
+      }
+      if (live) {
+        float* nxt = act + p.actOff[l + 1];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float v = fmaxf(acc[r], 0.0f);
+          nxt[r * p.ald[l + 1] + col] = v;
+          if (r < rows) a.L[l].O[(int64_t)(row0 + r) * a.L[l].out + col] = v;
+        }
+      }
+    }
+    if (l + 1 < NL) __syncthreads();  // layer l's activations complete
+  }
+}
+
+template <int NL>
+void* pickRegs(int R) {
+  switch (R) {
+    case 1: return reinterpret_cast<void*>(fc_regs_kernel<NL, 1>);
+    case 2: return reinterpret_cast<void*>(fc_regs_kernel<NL, 2>);
+    case 4: return reinterpret_cast<void*>(fc_regs_kernel<NL, 4>);
+    default: return nullptr;
+  }
+}
+
+}  // namespace
+
+bool fcRegsSupported(const FcChainArgs& a, int rows, const char** why) {
+  auto no = [&](const char* m) {
+    if (why) *why = m;
+    return false;
+  };
+  if (rows != 1 && rows != 2 && rows != 4) return no("register FC chain rows per CTA must be 1, 2 or 4");
+  if (a.layers < 1 || a.layers > 3) return no("register FC chain takes 1 to 3 layers");
+  int warps = 0;
+  for (int l = 0; l < a.layers; ++l) {
+    // kred_l of the kRegsKq register float4s, the last one possibly partial
+    if (a.L[l].kred > 4 * kRegsKq) return no("register FC chain needs every reduction <= 128 steps");
+    warps += (a.L[l].out + 31) / 32;
+  }
+  if (warps > 8) return no("register FC chain: more than 256 output columns in all layers");
+  return true;
+}
+
+size_t fcRegsSmem(const FcChainArgs& a, int rows) {
+  size_t f = 0;
+  for (int l = 0; l <= a.layers; ++l) {
+    const int w = l == 0 ? a.L[0].kred : a.L[l - 1].out;
+    f += (size_t)rows * ((w + 3) & ~3);
+  }
+  return f * 4;
+}
+
+cudaError_t launchFcRegs(const FcChainArgs& a, int rows, cudaStream_t s) {
+  if (a.batch <= 0) return cudaSuccess;
+  if (!fcRegsSupported(a, rows, nullptr)) return cudaErrorInvalidValue;
+  FcRegsPlan p{};
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  for (int l = 0; l < a.layers; ++l) p.vecW[l] = a.L[l].ldw % 4 == 0 && al16(a.L[l].W);
+  p.vecI = a.ldi % 4 == 0 && al16(a.I);
+  int warps = 0, off = 0;
+  for (int l = 0; l < a.layers; ++l) {
+    p.warpOff[l] = warps;
+    warps += (a.L[l].out + 31) / 32;
+  }
+  p.warpOff[a.layers] = warps;
+  for (int l = 0; l <= a.layers; ++l) {
+    const int w = l == 0 ? a.L[0].kred : a.L[l - 1].out;
+    p.ald[l] = (w + 3) & ~3;  // zero-padded to whole float4s (the tail group reads them, never uses them)
+    p.actOff[l] = off;
+    off += rows * p.ald[l];
+  }
+  const size_t smem = (size_t)off * 4;
+  void* kern = a.layers == 1 ? pickRegs<1>(rows) : a.layers == 2 ? pickRegs<2>(rows) : pickRegs<3>(rows);
+  if (!kern) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  void* args[] = {const_cast<FcChainArgs*>(&a), &p};
+  return cudaLaunchKernel(kern, dim3((a.batch + rows - 1) / rows), dim3(warps * 32), args, smem, s);
+}
+
+}  // namespace k
+}  // namespace tcb

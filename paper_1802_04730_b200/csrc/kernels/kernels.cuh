@@ -86,6 +86,10 @@ struct FcChainArgs {
 cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s);
 size_t fcChainSmem(const FcChainArgs& a, int rows, int cn);
 int fcChainThreads(const FcChainArgs& a, int rows, int cn);  // single-pass block size
+// register-resident chains (fc_regs.cu): every layer kred <= 128, one CTA per
+// `rows` (1, 2, 4) batch rows, one warp group per layer, weights in registers
+bool fcRegsSupported(const FcChainArgs& a, int rows, const char** why);
+cudaError_t launchFcRegs(const FcChainArgs& a, int rows, cudaStream_t s);
 
 // ------------------------------------------------------------------ KRU
 struct KruArgs {

@@ -282,7 +282,8 @@ std::string Mapping::describe() const {
         os << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
       break;
     case Family::FcChain:
-      if (fused) os << "cluster rows=" << rows << " cn=" << cn << " threads=" << threads;
+      if (fused && fcKind == 1) os << "registers rows=" << rows;
+      else if (fused) os << "cluster rows=" << rows << " cn=" << cn << " threads=" << threads;
       else os << "per-layer " << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
       break;
     case Family::Kru3: os << "fused dchunk=" << dchunk << " threads=" << threads; break;
@@ -470,6 +471,23 @@ Mapping decode(const Problem& p, const MappingOptions& o, int math) {
       m.fused = true;
       m.rows = o.tileSizes.empty() ? 1 : static_cast<int>(o.tileSizes[0]);
       m.cn = o.tileSizes.size() < 2 ? 1 : static_cast<int>(o.tileSizes[1]);
+      if (o.tileSizes.size() > 2 && o.tileSizes[2] == 2) {
+        // tile_sizes[2] == 2: register chains, tile_sizes[0] rows per CTA
+        m.fcKind = 1;
+        m.cn = 1;
+        k::FcChainArgs a{};
+        a.layers = static_cast<int>(p.fc.layers.size());
+        a.ldi = p.fc.ldi;
+        for (int l = 0; l < a.layers; ++l) {
+          a.L[l].out = p.fc.layers[l].out;
+          a.L[l].kred = p.fc.layers[l].kred;
+          a.L[l].ldw = p.fc.layers[l].ldw;
+        }
+        const char* why = nullptr;  // (null pointers pass the alignment checks)
+        if (!k::fcRegsSupported(a, m.rows, &why)) invalid(why);
+        m.threads = 0;
+        break;
+      }
       if (m.rows < 1 || m.rows > 32) invalid("fused FC chain rows per cluster must be in [1, 32]");
       if (m.cn < 1 || m.cn > 16) invalid("fused FC chain cluster size must be in [1, 16]");
       m.threads = static_cast<int>(o.threads());
@@ -629,6 +647,16 @@ MappingOptions defaultOptions(const Problem& p, int math) {
       }
       while (rows > 1 && k::fcChainSmem(a, rows, cn) > 110 * 1024) rows /= 2;
       int t = std::max(64, k::fcChainThreads(a, rows, cn));  // one pass per layer
+      a.ldi = p.fc.ldi;
+      for (int l = 0; l < a.layers; ++l) a.L[l].ldw = p.fc.layers[l].ldw;
+      if (k::fcRegsSupported(a, 2, nullptr)) {
+        // every layer a short reduction (MLP3): register chains, 2 rows per CTA
+        o.tileSizes = {2, 1, 2};
+        o.threadShape = {{64, 1, 1}};
+        o.fusion = Fusion::Max;
+        o.useShared = true;
+        break;
+      }
       o.tileSizes = {rows, cn, 1};
       o.threadShape = {{t, 1, 1}};
       o.fusion = Fusion::Max;
@@ -750,6 +778,7 @@ GenePools genePools(const Problem& p, int math) {
       if (p.family == Family::FcChain) {
         g.tile0 = {1, 2, 4, 8, 16, 32, 64};
         g.tile1 = {1, 2, 4, 8, 16, 32, 64};
+        g.tile2 = {1, 2, 16, 32, 64};  // fused: 1 = cluster kernel, 2 = register chains
         g.tx = {4, 8, 16, 32, 64, 128, 256, 512};
         g.fusion = {Fusion::Max, Fusion::Min};
       }
@@ -922,6 +951,10 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
         a.L[l].out = L.out;
         a.L[l].kred = L.kred;
         a.L[l].ldw = L.ldw;
+      }
+      if (m.fcKind == 1) {
+        check(k::launchFcRegs(a, m.rows, s), "FC chain (registers)");
+        return;
       }
       check(k::launchFcChain(a, m.rows, m.cn, m.threads, s), "FC chain");
       return;

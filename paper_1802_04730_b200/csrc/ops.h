@@ -87,6 +87,7 @@ struct Mapping {
   int gemmVariant = 4, gemmThreads = 0;
   // FcChain
   bool fused = true;
+  int fcKind = 0;  // fused: 0 = cluster kernel (fc_chain.cu), 1 = register chains (fc_regs.cu)
   int rows = 1, cn = 1, threads = 128;
   // Kru3
   int dchunk = 16;

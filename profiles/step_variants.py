@@ -16,15 +16,10 @@ from paper_1802_04730_b200 import ExecutionEngine  # noqa: E402
 
 NSTEP = int(os.environ.get("NSTEP", "26"))
 
-COMBOS = [  # r02: the slab TBMM plans vs the r01 tiled plans in the step
-    {"tbmm": {"tile_sizes": [32, 32, 64], "thread_shape": [16, 16, 1]}},
-    {"tbmm": {"tile_sizes": [7, 1, 2]}},
-    {"tbmm": {"tile_sizes": [7, 4, 2]}},
-    {"tbmm": {"tile_sizes": [4, 2, 2]}},
-    {"tbmm": {"tile_sizes": [4, 2, 2], "unroll_copy_shared": True}},
-    {"tbmm": {"tile_sizes": [7, 4, 2], "unroll_copy_shared": True}},
-    {"tbmm": {"tile_sizes": [7, 4, 2], "block_shape": [4, 1, 1]}},
-    {"tbmm": {"tile_sizes": [7, 4, 2], "block_shape": [2, 1, 1]}},
+COMBOS = [  # r02: the cluster FC kernel vs the register chains for MLP3 in the step
+    {"MLP3": {"tile_sizes": [4, 4, 1], "thread_shape": [64, 1, 1]}},
+    {"MLP3": {"tile_sizes": [1, 1, 2]}},
+    {"MLP3": {"tile_sizes": [4, 1, 2]}},
 ]
 
 VARIANTS = {

@@ -150,6 +150,32 @@ def test_fc_chain_cluster_variants(engine, oracle, golden, rows, cn, threads):
     assert ran >= 3
 
 
+@pytest.mark.parametrize("rows", [1, 2, 4])
+def test_fc_regs_variants(engine, oracle, golden, rows):
+    """Register-resident FC chains (fc_regs.cu, tile_sizes[2] == 2) at 1, 2 and
+    4 rows per CTA (ragged last CTA), bit-exact on every golden FC case they
+    take; defs with a reduction > 128 (layer 1 of MLP1/2FCRelu) are rejected
+    with MappingInvalid."""
+    from paper_1802_04730_b200 import TcError
+    ran = 0
+    for name in ["2fcrelu_small", "mlp3_small", "mlp3_paper", "mlp1_ragged", "2fcrelu_paper", "mlp1_paper"]:
+        case, ins, seeded = case_inputs(oracle, golden, name)
+        o = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0,
+             "shared_memory_budget": 49152, "thread_shape": [64, 1, 1], "tile_sizes": [rows, 1, 2],
+             "unroll_copy_shared": False, "unroll_factor": 1, "use_private": False, "use_shared": True}
+        try:
+            got, h = run_on_gpu(engine, case["def"], ins, seeded, options=o)
+        except TcError as e:
+            assert e.kind == "MappingInvalid", str(e)
+            assert case["def"] != "MLP3"
+            continue
+        assert "registers" in engine.describe(h)["kernel"]
+        ran += 1
+        for k, rec in case["outputs"].items():
+            assert_exact(oracle, name, k, got[k], rec["fnv"])
+    assert ran >= 4
+
+
 @pytest.mark.parametrize("dchunk,threads", [(1, 64), (3, 128), (8, 256), (16, 512)])
 def test_kru_chunks(engine, oracle, golden, dchunk, threads):
     case, ins, seeded = case_inputs(oracle, golden, "kru_paper_m8")
