@@ -7,14 +7,13 @@
 // DSMEM pushes and cluster barriers between layers (fc_trace: the first
 // layer's data lands ~5400 cycles after entry; the whole chain is ~1100
 // cycles of FFMA latency). Here every warp is assigned to one layer and one
-// lane to one output column of it; at entry each lane issues plain 16-byte
-// global loads of its whole weight row (<= 32 float4 registers) and its
-// bias, and the CTA stages its R input rows in shared memory, so every
-// global load of the kernel is in flight within the first few hundred
-// cycles. Then layer by layer (one CTA barrier between layers) the layer's
-// lanes run their R chains from registers (weights) and shared-memory
-// broadcasts (activations), write the layer's return and leave the result
-// in shared memory for the next layer.
+// lane to one output column of it. At entry the CTA issues plain coalesced
+// 16-byte loads of every layer's weights and its R input rows into shared
+// memory (all in flight within the first few hundred cycles); each lane
+// then moves its weight row into registers (<= 32 float4s). Layer by layer
+// (one CTA barrier between layers) the layer's lanes run their R chains
+// from registers (weights) and shared-memory broadcasts (activations),
+// write the layer's return and leave it in shared memory for the next.
 //
 // Exactness: each (row, column) output is one lane's sequential FFMA chain
 // in ascending k from bias[o], then fmaxf(., 0) — the interpreter's order
@@ -30,6 +29,8 @@ constexpr int kRegsKq = 32;  // float4s of one weight row held in registers (kre
 
 struct FcRegsPlan {
   int vecW[kMaxLayers];         // weight rows load as float4 (ldw % 4 == 0, 16-byte aligned)
+  int wOff[kMaxLayers];         // weights in shared memory (floats)
+  int wld4[kMaxLayers];         // their row stride (float4s, odd)
   int vecI;                     // input rows load as float4
   int warpOff[kMaxLayers + 1];  // first warp of each layer
   int ald[kMaxLayers + 1];      // activation row strides (floats, multiple of 4)
@@ -56,42 +57,31 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
   for (int l = 0; l < NL; ++l)
     if (warp >= p.warpOff[l] && warp < p.warpOff[l + 1]) layer = l;
 
-  // ---- every global load up front: this lane's weight row and bias ...
-  float4 w[kRegsKq];
-  float bias = 0.0f;
-  int col = 0, K4 = 0, KT = 0;  // full float4 groups, tail steps (kred % 4)
-  bool live = false;
+  // ---- every global load up front, coalesced: all layers' weights into
+  // shared memory (rows padded to an odd number of float4s, so the lanes'
+  // row reads below hit distinct bank groups), the CTA's input rows, and
+  // this lane's bias. (Each lane loading its own weight row straight from
+  // global memory put 32 scattered sectors in every warp load; the SM's
+  // outstanding-miss limit made MLP3 a 10-20 us kernel.)
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
-    if (layer == l) {
-      col = (warp - p.warpOff[l]) * 32 + lane;
-      live = col < a.L[l].out;
-      K4 = a.L[l].kred >> 2;
-      KT = a.L[l].kred & 3;
-      const float* wr = a.L[l].W + (int64_t)min(col, a.L[l].out - 1) * a.L[l].ldw;
-      if (p.vecW[l]) {
-#pragma unroll
-        for (int q = 0; q < kRegsKq; ++q)
-          if (q < K4) w[q] = __ldg(reinterpret_cast<const float4*>(wr) + q);
+    const int kr = a.L[l].kred, k4 = (kr + 3) >> 2, n = a.L[l].out;
+    float4* dst = reinterpret_cast<float4*>(act + p.wOff[l]);
+    for (int e = tid; e < n * k4; e += blockDim.x) {
+      const int r = e / k4, q = e - r * k4;
+      const float* src = a.L[l].W + (int64_t)r * a.L[l].ldw + 4 * q;
+      float4 v;
+      if (p.vecW[l] && 4 * q + 4 <= kr) {
+        v = __ldg(reinterpret_cast<const float4*>(src));
       } else {
-#pragma unroll
-        for (int q = 0; q < kRegsKq; ++q)
-          if (q < K4) w[q] = make_float4(__ldg(wr + 4 * q), __ldg(wr + 4 * q + 1), __ldg(wr + 4 * q + 2),
-                                         __ldg(wr + 4 * q + 3));
+        v.x = 4 * q < kr ? __ldg(src) : 0.0f;
+        v.y = 4 * q + 1 < kr ? __ldg(src + 1) : 0.0f;
+        v.z = 4 * q + 2 < kr ? __ldg(src + 2) : 0.0f;
+        v.w = 4 * q + 3 < kr ? __ldg(src + 3) : 0.0f;
       }
-#pragma unroll
-      for (int q = 0; q < kRegsKq; ++q)
-        if (q == K4 && KT) {
-          w[q].x = __ldg(wr + 4 * q);
-          w[q].y = KT > 1 ? __ldg(wr + 4 * q + 1) : 0.0f;
-          w[q].z = KT > 2 ? __ldg(wr + 4 * q + 2) : 0.0f;
-          w[q].w = 0.0f;
-        }
-      bias = live ? __ldg(a.L[l].bias + col) : 0.0f;
+      dst[r * p.wld4[l] + q] = v;
     }
   }
-  // ... and the CTA's input rows into shared memory (zero rows past the
-  // batch, zero columns past the reduction)
   {
     const int kr = a.L[0].kred, k0 = (kr + 3) >> 2;
     float* a0 = act + p.actOff[0];
@@ -112,7 +102,31 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
       reinterpret_cast<float4*>(a0 + r * p.ald[0])[q] = v;
     }
   }
+  float bias = 0.0f;
+  int col = 0, K4 = 0, KT = 0;  // full float4 groups, tail steps (kred % 4)
+  bool live = false;
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    if (layer == l) {
+      col = (warp - p.warpOff[l]) * 32 + lane;
+      live = col < a.L[l].out;
+      K4 = a.L[l].kred >> 2;
+      KT = a.L[l].kred & 3;
+      bias = live ? __ldg(a.L[l].bias + col) : 0.0f;
+    }
+  }
   __syncthreads();
+  // this lane's weight row: shared memory -> registers
+  float4 w[kRegsKq];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    if (layer == l) {
+      const float4* wr = reinterpret_cast<const float4*>(act + p.wOff[l]) + min(col, a.L[l].out - 1) * p.wld4[l];
+#pragma unroll
+      for (int q = 0; q < kRegsKq; ++q)
+        if (q < K4 || (q == K4 && KT)) w[q] = wr[q];
+    }
+  }
 
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
@@ -177,6 +191,16 @@ void* pickRegs(int R) {
 
 }  // namespace
 
+size_t fcRegsSmem(const FcChainArgs& a, int rows) {
+  size_t f = 0;
+  for (int l = 0; l <= a.layers; ++l) {
+    const int w = l == 0 ? a.L[0].kred : a.L[l - 1].out;
+    f += (size_t)rows * ((w + 3) & ~3);
+  }
+  for (int l = 0; l < a.layers; ++l) f += (size_t)a.L[l].out * ((((a.L[l].kred + 3) / 4) | 1) * 4);
+  return f * 4;
+}
+
 bool fcRegsSupported(const FcChainArgs& a, int rows, const char** why) {
   auto no = [&](const char* m) {
     if (why) *why = m;
@@ -191,17 +215,10 @@ bool fcRegsSupported(const FcChainArgs& a, int rows, const char** why) {
     warps += (a.L[l].out + 31) / 32;
   }
   if (warps > 8) return no("register FC chain: more than 256 output columns in all layers");
+  if (fcRegsSmem(a, rows) > 200 * 1024) return no("register FC chain: weights exceed shared memory");
   return true;
 }
 
-size_t fcRegsSmem(const FcChainArgs& a, int rows) {
-  size_t f = 0;
-  for (int l = 0; l <= a.layers; ++l) {
-    const int w = l == 0 ? a.L[0].kred : a.L[l - 1].out;
-    f += (size_t)rows * ((w + 3) & ~3);
-  }
-  return f * 4;
-}
 
 cudaError_t launchFcRegs(const FcChainArgs& a, int rows, cudaStream_t s) {
   if (a.batch <= 0) return cudaSuccess;
@@ -221,6 +238,11 @@ cudaError_t launchFcRegs(const FcChainArgs& a, int rows, cudaStream_t s) {
     p.ald[l] = (w + 3) & ~3;  // zero-padded to whole float4s (the tail group reads them, never uses them)
     p.actOff[l] = off;
     off += rows * p.ald[l];
+  }
+  for (int l = 0; l < a.layers; ++l) {
+    p.wOff[l] = off;
+    p.wld4[l] = ((a.L[l].kred + 3) / 4) | 1;
+    off += a.L[l].out * p.wld4[l] * 4;
   }
   const size_t smem = (size_t)off * 4;
   void* kern = a.layers == 1 ? pickRegs<1>(rows) : a.layers == 2 ? pickRegs<2>(rows) : pickRegs<3>(rows);
