@@ -45,6 +45,21 @@ __device__ __forceinline__ float4 ldsV4(const float* p) {
   return v;
 }
 
+#ifdef TCB_FCR_TRACE
+// diagnostic build only (profiles/fc_regs_trace.cu): per-CTA globaltimer stamps
+__device__ unsigned long long g_fcr_trace[1024][8];
+#define FCR_STAMP(ev)                                                          \
+  do {                                                                         \
+    unsigned long long t_;                                                     \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_fcr_trace[blockIdx.x][ev] = t_; \
+  } while (0)
+#else
+#define FCR_STAMP(ev) \
+  do {                \
+  } while (0)
+#endif
+
 template <int NL, int R>
 __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ FcChainArgs a,
                                                        const __grid_constant__ FcRegsPlan p) {
@@ -52,6 +67,7 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int row0 = blockIdx.x * R;
   const int rows = min(R, a.batch - row0);
+  FCR_STAMP(0);
   int layer = -1;
 #pragma unroll
   for (int l = 0; l < NL; ++l)
@@ -116,6 +132,7 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
     }
   }
   __syncthreads();
+  FCR_STAMP(1);
   // this lane's weight row: shared memory -> registers
   float4 w[kRegsKq];
 #pragma unroll
@@ -176,6 +193,7 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
       }
     }
     if (l + 1 < NL) __syncthreads();  // layer l's activations complete
+    FCR_STAMP(2 + l);
   }
 }
 
