@@ -25,7 +25,7 @@ namespace k {
 
 namespace {
 
-constexpr int kRegsKq = 32;  // float4s of one weight row held in registers (kred <= 128)
+constexpr int kRegsKq = 32;  // float4s per weight row (kred <= 128)
 
 struct FcRegsPlan {
   int vecW[kMaxLayers];         // weight rows load as float4 (ldw % 4 == 0, 16-byte aligned)
@@ -37,11 +37,9 @@ struct FcRegsPlan {
   int actOff[kMaxLayers + 1];   // activation buffers in shared memory (floats)
 };
 
-__device__ __forceinline__ float4 ldsV4(const float* p) {
+__device__ __forceinline__ float4 ldsA(unsigned addr) {
   float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
 
@@ -83,7 +81,12 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
   for (int l = 0; l < NL; ++l) {
     const int kr = a.L[l].kred, k4 = (kr + 3) >> 2, n = a.L[l].out;
     float4* dst = reinterpret_cast<float4*>(act + p.wOff[l]);
-    for (int e = tid; e < n * k4; e += blockDim.x) {
+    // every CTA reads the same weights: start each CTA at a different row so
+    // concurrent requests spread over L2 slices instead of queueing on one
+    const int tot = n * k4, rot = (blockIdx.x * 7 % max(1, n)) * k4;
+    for (int e0 = tid; e0 < tot; e0 += blockDim.x) {
+      int e = e0 + rot;
+      if (e >= tot) e -= tot;
       const int r = e / k4, q = e - r * k4;
       const float* src = a.L[l].W + (int64_t)r * a.L[l].ldw + 4 * q;
       float4 v;
@@ -133,17 +136,6 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
   }
   __syncthreads();
   FCR_STAMP(1);
-  // this lane's weight row: shared memory -> registers
-  float4 w[kRegsKq];
-#pragma unroll
-  for (int l = 0; l < NL; ++l) {
-    if (layer == l) {
-      const float4* wr = reinterpret_cast<const float4*>(act + p.wOff[l]) + min(col, a.L[l].out - 1) * p.wld4[l];
-#pragma unroll
-      for (int q = 0; q < kRegsKq; ++q)
-        if (q < K4 || (q == K4 && KT)) w[q] = wr[q];
-    }
-  }
 
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
@@ -152,34 +144,37 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
       float acc[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) acc[r] = bias;
+      // weights: this lane's row in shared memory (odd float4 stride: the
+      // lanes' reads hit distinct bank groups); activations: broadcasts.
+      // A compact loop: fully unrolled per-layer chains overflowed the
+      // instruction cache (~38 cycles per step)
+      const unsigned wr = static_cast<unsigned>(__cvta_generic_to_shared(act + p.wOff[l])) +
+                          (unsigned)(min(col, a.L[l].out - 1) * p.wld4[l]) * 16u;
+      const unsigned xr = static_cast<unsigned>(__cvta_generic_to_shared(in));
+      const unsigned xs = (unsigned)p.ald[l] * 4u;
+#pragma unroll 2
+      for (int q = 0; q < K4; ++q) {
+        const float4 wv = ldsA(wr + q * 16);
+        float4 x[R];
 #pragma unroll
-      for (int q = 0; q < kRegsKq; ++q) {
-        if (q < K4) {  // warp-uniform
-          float4 x[R];
+        for (int r = 0; r < R; ++r) x[r] = ldsA(xr + r * xs + q * 16);
 #pragma unroll
-          for (int r = 0; r < R; ++r) x[r] = ldsV4(in + r * p.ald[l] + 4 * q);  // broadcast
+        for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].x, wv.x, acc[r]);
 #pragma unroll
-          for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].x, w[q].x, acc[r]);
+        for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].y, wv.y, acc[r]);
 #pragma unroll
-          for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].y, w[q].y, acc[r]);
+        for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].z, wv.z, acc[r]);
 #pragma unroll
-          for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].z, w[q].z, acc[r]);
+        for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].w, wv.w, acc[r]);
+      }
+      if (KT) {  // the kred % 4 tail steps, still in order
+        const float4 wv = ldsA(wr + K4 * 16);
 #pragma unroll
-          for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].w, w[q].w, acc[r]);
-        } else if (q == K4 && KT) {  // the kred % 4 tail steps, still in order
-          float4 x[R];
-#pragma unroll
-          for (int r = 0; r < R; ++r) x[r] = ldsV4(in + r * p.ald[l] + 4 * q);
-#pragma unroll
-          for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].x, w[q].x, acc[r]);
-          if (KT > 1) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].y, w[q].y, acc[r]);
-          }
-          if (KT > 2) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[r] = __fmaf_rn(x[r].z, w[q].z, acc[r]);
-          }
+        for (int r = 0; r < R; ++r) {
+          const float4 x = ldsA(xr + r * xs + K4 * 16);
+          acc[r] = __fmaf_rn(x.x, wv.x, acc[r]);
+          if (KT > 1) acc[r] = __fmaf_rn(x.y, wv.y, acc[r]);
+          if (KT > 2) acc[r] = __fmaf_rn(x.z, wv.z, acc[r]);
         }
       }
       if (live) {
@@ -193,6 +188,9 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
       }
     }
     if (l + 1 < NL) __syncthreads();  // layer l's activations complete
+#ifdef TCB_FCR_TRACE
+    if (l + 1 == NL) __syncthreads();
+#endif
     FCR_STAMP(2 + l);
   }
 }
