@@ -73,54 +73,49 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
 
   // ---- every global load up front, coalesced: all layers' weights into
   // shared memory (rows padded to an odd number of float4s, so the lanes'
-  // row reads below hit distinct bank groups), the CTA's input rows, and
-  // this lane's bias. (Each lane loading its own weight row straight from
-  // global memory put 32 scattered sectors in every warp load; the SM's
-  // outstanding-miss limit made MLP3 a 10-20 us kernel.)
+  // row reads below hit distinct bank groups) and the CTA's input rows, by
+  // 16-byte cp.async where the rows allow it (asynchronous: a load-then-store
+  // loop serialised every thread on one L2 round trip per 16 bytes, ~6 us
+  // for MLP3's 40 KB, profiles/fc_regs_trace.cu). Each lane owns one output
+  // column of one layer. (Each lane loading its own weight row straight from
+  // global memory put 32 scattered sectors in every warp load instead.)
+  auto stage = [&](float4* dst, const float* src, int kr, bool vec) {
+    // one zero-padded float4 of a row: 4 k values starting at src
+    if (vec) {
+      const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+    } else {
+      float4 v;
+      v.x = 0 < kr ? __ldg(src) : 0.0f;
+      v.y = 1 < kr ? __ldg(src + 1) : 0.0f;
+      v.z = 2 < kr ? __ldg(src + 2) : 0.0f;
+      v.w = 3 < kr ? __ldg(src + 3) : 0.0f;
+      *dst = v;
+    }
+  };
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
     const int kr = a.L[l].kred, k4 = (kr + 3) >> 2, n = a.L[l].out;
     float4* dst = reinterpret_cast<float4*>(act + p.wOff[l]);
-    // every CTA reads the same weights: start each CTA at a different row so
-    // concurrent requests spread over L2 slices instead of queueing on one
-    const int tot = n * k4, rot = (blockIdx.x * 7 % max(1, n)) * k4;
-    for (int e0 = tid; e0 < tot; e0 += blockDim.x) {
-      int e = e0 + rot;
-      if (e >= tot) e -= tot;
+    for (int e = tid; e < n * k4; e += blockDim.x) {
       const int r = e / k4, q = e - r * k4;
-      const float* src = a.L[l].W + (int64_t)r * a.L[l].ldw + 4 * q;
-      float4 v;
-      if (p.vecW[l] && 4 * q + 4 <= kr) {
-        v = __ldg(reinterpret_cast<const float4*>(src));
-      } else {
-        v.x = 4 * q < kr ? __ldg(src) : 0.0f;
-        v.y = 4 * q + 1 < kr ? __ldg(src + 1) : 0.0f;
-        v.z = 4 * q + 2 < kr ? __ldg(src + 2) : 0.0f;
-        v.w = 4 * q + 3 < kr ? __ldg(src + 3) : 0.0f;
-      }
-      dst[r * p.wld4[l] + q] = v;
+      stage(dst + r * p.wld4[l] + q, a.L[l].W + (int64_t)r * a.L[l].ldw + 4 * q, kr - 4 * q,
+            p.vecW[l] && 4 * q + 4 <= kr);
     }
   }
   {
     const int kr = a.L[0].kred, k0 = (kr + 3) >> 2;
-    float* a0 = act + p.actOff[0];
+    float4* a0 = reinterpret_cast<float4*>(act + p.actOff[0]);
     for (int e = tid; e < R * k0; e += blockDim.x) {
       const int r = e / k0, q = e - r * k0;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      const float* src = a.I + (int64_t)(row0 + r) * a.ldi + 4 * q;
-      if (r < rows) {
-        if (p.vecI && 4 * q + 4 <= kr) {
-          v = __ldg(reinterpret_cast<const float4*>(src));
-        } else {
-          v.x = 4 * q < kr ? __ldg(src) : 0.0f;
-          v.y = 4 * q + 1 < kr ? __ldg(src + 1) : 0.0f;
-          v.z = 4 * q + 2 < kr ? __ldg(src + 2) : 0.0f;
-          v.w = 4 * q + 3 < kr ? __ldg(src + 3) : 0.0f;
-        }
-      }
-      reinterpret_cast<float4*>(a0 + r * p.ald[0])[q] = v;
+      if (r < rows)
+        stage(a0 + r * (p.ald[0] >> 2) + q, a.I + (int64_t)(row0 + r) * a.ldi + 4 * q, kr - 4 * q,
+              p.vecI && 4 * q + 4 <= kr);
+      else
+        a0[r * (p.ald[0] >> 2) + q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   float bias = 0.0f;
   int col = 0, K4 = 0, KT = 0;  // full float4 groups, tail steps (kred % 4)
   bool live = false;
@@ -134,6 +129,7 @@ __global__ void __launch_bounds__(256) fc_regs_kernel(const __grid_constant__ Fc
       bias = live ? __ldg(a.L[l].bias + col) : 0.0f;
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   FCR_STAMP(1);
 
