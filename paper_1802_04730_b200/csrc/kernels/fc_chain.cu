@@ -31,6 +31,8 @@ namespace k {
 namespace {
 
 
+constexpr size_t kFcAsyncMaxBytes = 32 * 1024;  // automatic load mode: cp.async up to this per CTA
+
 struct FcPlan {
   int cn, R;
   int cols[kMaxLayers];     // output columns per CTA
@@ -40,7 +42,7 @@ struct FcPlan {
   int offAct[kMaxLayers];   // [0]: input rows; [l>0]: layer l-1's output = layer l's input
   int offBar;
   int denseIn;              // input rows land unpadded with one copy (ald[0] == kred, conflict-free)
-  int bulk;                 // 1: cp.async.bulk path, 0: cooperative loads
+  int bulk;                 // 1: cp.async.bulk path, 2: 16-byte cp.async path, 0: cooperative loads
 };
 
 __host__ __device__ inline int up4(int x) { return (x + 3) & ~3; }
@@ -87,6 +89,13 @@ __device__ __forceinline__ void bulkCopy(void* dst, const void* src, unsigned by
           smemAddr(dst)),
       "l"(src), "r"(bytes), "r"(smemAddr(bar))
       : "memory");
+}
+__device__ __forceinline__ void cpAsync16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smemAddr(dst)), "l"(src) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cpAsyncWait() {
+  if constexpr (N >= 0) asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ unsigned clusterRank() {
   unsigned r;
@@ -282,6 +291,27 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     // input rows past the batch end are zero
     for (int e = tid; e < (R - rows) * p.ald[0]; e += T) sm[p.offAct[0] + rows * p.ald[0] + e] = 0.0f;
     if (rows < R) __syncthreads();
+  } else if (p.bulk == 2) {
+    // 16-byte cp.async from every thread, one commit group per layer (the
+    // input rows ride with layer 0): for small per-CTA loads (MLP3: ~12 KB)
+    // the SM's bulk-copy engine costs more in per-copy issue than it saves
+    // (profiles/r02_fc_notes.txt)
+    const int k4in = a.L[0].kred >> 2;
+    for (int e = tid; e < rows * k4in; e += T) {
+      const int r = e / k4in, q = e - r * k4in;
+      cpAsync16(sm + p.offAct[0] + r * p.ald[0] + 4 * q, a.I + (int64_t)(row0 + r) * a.ldi + 4 * q);
+    }
+    for (int e = tid; e < (R - rows) * p.ald[0]; e += T) sm[p.offAct[0] + rows * p.ald[0] + e] = 0.0f;
+#pragma unroll
+    for (int l = 0; l < layers; ++l) {
+      const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0)), k4 = a.L[l].kred >> 2;
+      const float* src = a.L[l].W + (int64_t)c0 * a.L[l].ldw;
+      for (int e = tid; e < nc * k4; e += T) {
+        const int j = e / k4, q = e - j * k4;
+        cpAsync16(sm + p.offW[l] + j * p.wld[l] + 4 * q, src + (int64_t)j * a.L[l].ldw + 4 * q);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
   } else {
     for (int e = tid; e < R * p.ald[0]; e += T) {
       int r = e / p.ald[0], kk = e % p.ald[0];
@@ -306,8 +336,17 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     const bool last = l + 1 == layers;
     const int ald = p.ald[l];
     const unsigned actBase = smemAddr(sm + p.offAct[l]), wBase = smemAddr(sm + p.offW[l]);
-    if ((l > 0 && cn > 1) || (l == 0 && p.bulk)) mbarWait(&bars[l], 0, l);
-    if (p.bulk) mbarWait(&bars[layers + l], 0, layers + l);
+    if ((l > 0 && cn > 1) || (l == 0 && p.bulk == 1)) mbarWait(&bars[l], 0, l);
+    if (p.bulk == 1) mbarWait(&bars[layers + l], 0, layers + l);
+    if (p.bulk == 2) {  // this thread's copies of layers <= l landed, then everyone's
+      switch (NL - 1 - l) {
+        case 0: cpAsyncWait<0>(); break;
+        case 1: cpAsyncWait<1>(); break;
+        case 2: cpAsyncWait<2>(); break;
+        default: cpAsyncWait<3>(); break;
+      }
+      __syncthreads();
+    }
     FC_STAMP(3 + 3 * l);
     if (!last && l == 0 && cn > 1) asm volatile("barrier.cluster.wait;" ::: "memory");
     const int nchains = R * cols;
@@ -349,7 +388,7 @@ __global__ void __launch_bounds__(kFcMaxThreads)
 
 // Builds the plan; returns the dynamic shared-memory size. Every operand
 // buffer is followed by >= 32 floats of slack (the chain prefetches ahead).
-static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p) {
+static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads = 0) {
   p = FcPlan{};
   p.cn = cn;
   p.R = R;
@@ -391,7 +430,13 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p) {
   for (int l = 0; l < a.layers; ++l)
     bulk = bulk && (a.L[l].kred % 4 == 0) && (a.L[l].ldw % 4 == 0) &&
            ((reinterpret_cast<uintptr_t>(a.L[l].W) & 15) == 0);
-  p.bulk = bulk ? 1 : 0;
+  p.bulk = !bulk ? 0 : loads == 1 ? 1 : loads == 2 ? 2 : 0;
+  if (bulk && loads == 0) {
+    // automatic: cp.async for small per-CTA loads, the bulk engine for big ones
+    size_t bytes = (size_t)R * a.L[0].kred * 4;
+    for (int l = 0; l < a.layers; ++l) bytes += (size_t)p.cols[l] * a.L[l].kred * 4;
+    p.bulk = bytes <= kFcAsyncMaxBytes ? 2 : 1;
+  }
   return (size_t)off * sizeof(float);
 }
 
@@ -422,10 +467,10 @@ static void (*fcKernel(int layers))(FcChainArgs, FcPlan) {
   }
 }
 
-cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s) {
+cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s, int loads) {
   if (a.batch <= 0) return cudaSuccess;
   FcPlan p;
-  size_t smem = planFc(a, rows, cn, p);
+  size_t smem = planFc(a, rows, cn, p, loads);
   if (smem > 227 * 1024 || cn < 1 || cn > 16 || rows < 1) return cudaErrorInvalidConfiguration;
   if (threads < 32 || threads > kFcMaxThreads || threads % 32) return cudaErrorInvalidConfiguration;
   void (*kern)(FcChainArgs, FcPlan) = fcKernel(a.layers);

@@ -83,7 +83,9 @@ struct FcChainArgs {
   int layers;
   FcLayer L[kMaxLayers];
 };
-cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s);
+// loads: 0 = automatic (16-byte cp.async for <= 32 KB per CTA, else the bulk
+// copy engine), 1 = bulk copies, 2 = cp.async
+cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s, int loads = 0);
 size_t fcChainSmem(const FcChainArgs& a, int rows, int cn);
 int fcChainThreads(const FcChainArgs& a, int rows, int cn);  // single-pass block size
 // register-resident chains (fc_regs.cu): every layer kred <= 128, one CTA per

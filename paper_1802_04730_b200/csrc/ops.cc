@@ -283,7 +283,9 @@ std::string Mapping::describe() const {
       break;
     case Family::FcChain:
       if (fused && fcKind == 1) os << "registers rows=" << rows;
-      else if (fused) os << "cluster rows=" << rows << " cn=" << cn << " threads=" << threads;
+      else if (fused)
+        os << "cluster rows=" << rows << " cn=" << cn << " threads=" << threads
+           << (fcLoads == 1 ? " loads=bulk" : fcLoads == 2 ? " loads=cp.async" : "");
       else os << "per-layer " << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
       break;
     case Family::Kru3: os << "fused dchunk=" << dchunk << " threads=" << threads; break;
@@ -471,6 +473,10 @@ Mapping decode(const Problem& p, const MappingOptions& o, int math) {
       m.fused = true;
       m.rows = o.tileSizes.empty() ? 1 : static_cast<int>(o.tileSizes[0]);
       m.cn = o.tileSizes.size() < 2 ? 1 : static_cast<int>(o.tileSizes[1]);
+      // tile_sizes[2]: 1 = cluster kernel, automatic loads; 3 / 4 = cluster
+      // kernel with bulk-copy / cp.async loads
+      if (o.tileSizes.size() > 2 && (o.tileSizes[2] == 3 || o.tileSizes[2] == 4))
+        m.fcLoads = o.tileSizes[2] == 3 ? 1 : 2;
       if (o.tileSizes.size() > 2 && o.tileSizes[2] == 2) {
         // tile_sizes[2] == 2: register chains, tile_sizes[0] rows per CTA
         m.fcKind = 1;
@@ -778,7 +784,7 @@ GenePools genePools(const Problem& p, int math) {
       if (p.family == Family::FcChain) {
         g.tile0 = {1, 2, 4, 8, 16, 32, 64};
         g.tile1 = {1, 2, 4, 8, 16, 32, 64};
-        g.tile2 = {1, 2, 16, 32, 64};  // fused: 1 = cluster kernel, 2 = register chains
+        g.tile2 = {1, 2, 3, 4, 16, 32, 64};  // fused: 1 = cluster kernel, 2 = register chains, 3/4 = cluster loads
         g.tx = {4, 8, 16, 32, 64, 128, 256, 512};
         g.fusion = {Fusion::Max, Fusion::Min};
       }
@@ -956,7 +962,7 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
         check(k::launchFcRegs(a, m.rows, s), "FC chain (registers)");
         return;
       }
-      check(k::launchFcChain(a, m.rows, m.cn, m.threads, s), "FC chain");
+      check(k::launchFcChain(a, m.rows, m.cn, m.threads, s, m.fcLoads), "FC chain");
       return;
     }
     case Family::Kru3: {

@@ -16,10 +16,11 @@ from paper_1802_04730_b200 import ExecutionEngine  # noqa: E402
 
 NSTEP = int(os.environ.get("NSTEP", "26"))
 
-COMBOS = [  # r02: the cluster FC kernel vs the register chains for MLP3 in the step
-    {"MLP3": {"tile_sizes": [4, 4, 1], "thread_shape": [64, 1, 1]}},
-    {"MLP3": {"tile_sizes": [1, 1, 2]}},
-    {"MLP3": {"tile_sizes": [4, 1, 2]}},
+COMBOS = [  # r02: FC load modes in the step
+    {"MLP3": {"tile_sizes": [4, 4, 3]}},
+    {"MLP3": {"tile_sizes": [4, 4, 4]}},
+    {"2FCRelu": {"tile_sizes": [4, 8, 3]}},
+    {"2FCRelu": {"tile_sizes": [4, 8, 4]}},
 ]
 
 VARIANTS = {
