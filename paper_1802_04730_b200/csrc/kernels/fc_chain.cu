@@ -21,6 +21,7 @@
 // Exactness: each (row, column) output is one thread's sequential FFMA
 // chain in ascending k from bias[o], then fmaxf(·, 0) — the interpreter's
 // order (interpreter.cc:218-233; builtin fmaxf → std::fmax, :22-24).
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -30,8 +31,6 @@ namespace k {
 
 namespace {
 
-
-constexpr size_t kFcAsyncMaxBytes = 32 * 1024;  // automatic load mode: cp.async up to this per CTA
 
 struct FcPlan {
   int cn, R;
@@ -43,6 +42,7 @@ struct FcPlan {
   int offBar;
   int denseIn;              // input rows land unpadded with one copy (ald[0] == kred, conflict-free)
   int bulk;                 // 1: cp.async.bulk path, 2: 16-byte cp.async path, 0: cooperative loads
+  int nch, kc4;             // cp.async path: layer 0 in nch chunks of kc4 float4s of the reduction
 };
 
 __host__ __device__ inline int up4(int x) { return (x + 3) & ~3; }
@@ -296,14 +296,27 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     // input rows ride with layer 0): for small per-CTA loads (MLP3: ~12 KB)
     // the SM's bulk-copy engine costs more in per-copy issue than it saves
     // (profiles/r02_fc_notes.txt)
-    const int k4in = a.L[0].kred >> 2;
-    for (int e = tid; e < rows * k4in; e += T) {
-      const int r = e / k4in, q = e - r * k4in;
-      cpAsync16(sm + p.offAct[0] + r * p.ald[0] + 4 * q, a.I + (int64_t)(row0 + r) * a.ldi + 4 * q);
-    }
+    // Layer 0 lands in p.nch reduction chunks (its input rows and weight
+    // slice, one commit group per chunk), so its chains start on chunk 0
+    // while the rest is in flight; every later layer is one more group.
     for (int e = tid; e < (R - rows) * p.ald[0]; e += T) sm[p.offAct[0] + rows * p.ald[0] + e] = 0.0f;
+    {
+      const int c0 = rank * p.cols[0], nc = max(0, min(p.cols[0], a.L[0].out - c0));
+      const float* src = a.L[0].W + (int64_t)c0 * a.L[0].ldw;
+      for (int ch = 0; ch < p.nch; ++ch) {
+        const int q0 = ch * p.kc4, q1 = min(q0 + p.kc4, a.L[0].kred >> 2), w4 = q1 - q0;
+        for (int e = tid; e < (rows + nc) * w4; e += T) {
+          const int j = e / w4, q = q0 + e - j * w4;
+          if (j < rows)
+            cpAsync16(sm + p.offAct[0] + j * p.ald[0] + 4 * q, a.I + (int64_t)(row0 + j) * a.ldi + 4 * q);
+          else
+            cpAsync16(sm + p.offW[0] + (j - rows) * p.wld[0] + 4 * q, src + (int64_t)(j - rows) * a.L[0].ldw + 4 * q);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+    }
 #pragma unroll
-    for (int l = 0; l < layers; ++l) {
+    for (int l = 1; l < layers; ++l) {
       const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0)), k4 = a.L[l].kred >> 2;
       const float* src = a.L[l].W + (int64_t)c0 * a.L[l].ldw;
       for (int e = tid; e < nc * k4; e += T) {
@@ -338,15 +351,21 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     const unsigned actBase = smemAddr(sm + p.offAct[l]), wBase = smemAddr(sm + p.offW[l]);
     if ((l > 0 && cn > 1) || (l == 0 && p.bulk == 1)) mbarWait(&bars[l], 0, l);
     if (p.bulk == 1) mbarWait(&bars[layers + l], 0, layers + l);
-    if (p.bulk == 2) {  // this thread's copies of layers <= l landed, then everyone's
-      switch (NL - 1 - l) {
+    // cp.async mode: commit groups in flight after layer l's (or layer-0
+    // chunk ch's) group; waiting for that leaves only later groups pending
+    auto asyncWait = [&](int pending) {
+      switch (pending) {
         case 0: cpAsyncWait<0>(); break;
         case 1: cpAsyncWait<1>(); break;
         case 2: cpAsyncWait<2>(); break;
-        default: cpAsyncWait<3>(); break;
+        case 3: cpAsyncWait<3>(); break;
+        case 4: cpAsyncWait<4>(); break;
+        case 5: cpAsyncWait<5>(); break;
+        default: cpAsyncWait<6>(); break;
       }
-      __syncthreads();
-    }
+      __syncthreads();  // this thread's copies landed, then everyone's
+    };
+    if (p.bulk == 2 && l > 0) asyncWait(NL - 1 - l);
     FC_STAMP(3 + 3 * l);
     if (!last && l == 0 && cn > 1) asm volatile("barrier.cluster.wait;" ::: "memory");
     const int nchains = R * cols;
@@ -361,7 +380,16 @@ __global__ void __launch_bounds__(kFcMaxThreads)
       for (int q = 0; q < kMaxLayers; ++q)
         if (q == l) bpre = biasPre[q];  // static register indexing
       float acc = !live ? 0.0f : base == 0 ? bpre : __ldg(L.bias + c0 + c);
-      acc = chainSegment(actBase + (unsigned)(r * ald) * 4u, wBase + (unsigned)(c * p.wld[l]) * 4u, L.kred, acc);
+      const unsigned xa = actBase + (unsigned)(r * ald) * 4u, wa = wBase + (unsigned)(c * p.wld[l]) * 4u;
+      if (l == 0 && p.bulk == 2) {
+        for (int ch = 0; ch < p.nch; ++ch) {  // the chain follows the chunks in
+          if (base == 0) asyncWait(p.nch - 1 - ch + NL - 1);
+          const int k0 = ch * 4 * p.kc4, n = min(4 * p.kc4, L.kred - k0);
+          acc = chainSegment(xa + 4u * k0, wa + 4u * k0, n, acc);
+        }
+      } else {
+        acc = chainSegment(xa, wa, L.kred, acc);
+      }
       FC_STAMP(16 + l);  // chain done (thread 0's first pass), before its stores
       if (live) {
         const float v = fmaxf(acc, 0.0f);
@@ -430,12 +458,18 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads =
   for (int l = 0; l < a.layers; ++l)
     bulk = bulk && (a.L[l].kred % 4 == 0) && (a.L[l].ldw % 4 == 0) &&
            ((reinterpret_cast<uintptr_t>(a.L[l].W) & 15) == 0);
-  p.bulk = !bulk ? 0 : loads == 1 ? 1 : loads == 2 ? 2 : 0;
-  if (bulk && loads == 0) {
-    // automatic: cp.async for small per-CTA loads, the bulk engine for big ones
-    size_t bytes = (size_t)R * a.L[0].kred * 4;
-    for (int l = 0; l < a.layers; ++l) bytes += (size_t)p.cols[l] * a.L[l].kred * 4;
-    p.bulk = bytes <= kFcAsyncMaxBytes ? 2 : 1;
+  // automatic loads: 16-byte cp.async from every thread (measured faster
+  // than the bulk-copy engine for every FC chain at the paper shapes,
+  // profiles/r02_fc_notes.txt)
+  p.bulk = !bulk ? 0 : loads == 1 ? 1 : 2;
+  {
+    // layer-0 chunks: ~256-step pieces, at most 4, multiples of 16 steps
+    // (chainSegment's granularity; the chunk boundaries keep the k order)
+    const int k4 = a.L[0].kred >> 2;
+    p.nch = std::max(1, std::min(4, a.L[0].kred / 256));
+    p.kc4 = ((k4 + p.nch - 1) / p.nch + 3) & ~3;
+    p.nch = (k4 + p.kc4 - 1) / p.kc4;
+    if (a.layers + p.nch - 1 > 7) p.nch = 1, p.kc4 = k4;  // (wait_group immediates up to 6)
   }
   return (size_t)off * sizeof(float);
 }

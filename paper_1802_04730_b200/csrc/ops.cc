@@ -655,14 +655,6 @@ MappingOptions defaultOptions(const Problem& p, int math) {
       int t = std::max(64, k::fcChainThreads(a, rows, cn));  // one pass per layer
       a.ldi = p.fc.ldi;
       for (int l = 0; l < a.layers; ++l) a.L[l].ldw = p.fc.layers[l].ldw;
-      if (k::fcRegsSupported(a, 2, nullptr)) {
-        // every layer a short reduction (MLP3): register chains, 2 rows per CTA
-        o.tileSizes = {2, 1, 2};
-        o.threadShape = {{64, 1, 1}};
-        o.fusion = Fusion::Max;
-        o.useShared = true;
-        break;
-      }
       o.tileSizes = {rows, cn, 1};
       o.threadShape = {{t, 1, 1}};
       o.fusion = Fusion::Max;

@@ -17,10 +17,8 @@ from paper_1802_04730_b200 import ExecutionEngine  # noqa: E402
 NSTEP = int(os.environ.get("NSTEP", "26"))
 
 COMBOS = [  # r02: FC load modes in the step
-    {"MLP3": {"tile_sizes": [4, 4, 3]}},
-    {"MLP3": {"tile_sizes": [4, 4, 4]}},
     {"2FCRelu": {"tile_sizes": [4, 8, 3]}},
-    {"2FCRelu": {"tile_sizes": [4, 8, 4]}},
+    {"MLP3": {"tile_sizes": [2, 1, 2]}},
 ]
 
 VARIANTS = {
