@@ -462,6 +462,7 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads =
   // than the bulk-copy engine for every FC chain at the paper shapes,
   // profiles/r02_fc_notes.txt)
   p.bulk = !bulk ? 0 : loads == 1 ? 1 : 2;
+  const bool oneChunk = loads == 3;
   {
     // layer-0 chunks: ~256-step pieces, at most 4, multiples of 16 steps
     // (chainSegment's granularity; the chunk boundaries keep the k order)
@@ -469,7 +470,7 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads =
     p.nch = std::max(1, std::min(4, a.L[0].kred / 256));
     p.kc4 = ((k4 + p.nch - 1) / p.nch + 3) & ~3;
     p.nch = (k4 + p.kc4 - 1) / p.kc4;
-    if (a.layers + p.nch - 1 > 7) p.nch = 1, p.kc4 = k4;  // (wait_group immediates up to 6)
+    if (a.layers + p.nch - 1 > 7 || oneChunk) p.nch = 1, p.kc4 = k4;  // (wait_group immediates up to 6)
   }
   return (size_t)off * sizeof(float);
 }

@@ -285,7 +285,7 @@ std::string Mapping::describe() const {
       if (fused && fcKind == 1) os << "registers rows=" << rows;
       else if (fused)
         os << "cluster rows=" << rows << " cn=" << cn << " threads=" << threads
-           << (fcLoads == 1 ? " loads=bulk" : fcLoads == 2 ? " loads=cp.async" : "");
+           << (fcLoads == 1 ? " loads=bulk" : fcLoads == 2 ? " loads=cp.async" : fcLoads == 3 ? " loads=cp.async/1" : "");
       else os << "per-layer " << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
       break;
     case Family::Kru3: os << "fused dchunk=" << dchunk << " threads=" << threads; break;
@@ -475,8 +475,8 @@ Mapping decode(const Problem& p, const MappingOptions& o, int math) {
       m.cn = o.tileSizes.size() < 2 ? 1 : static_cast<int>(o.tileSizes[1]);
       // tile_sizes[2]: 1 = cluster kernel, automatic loads; 3 / 4 = cluster
       // kernel with bulk-copy / cp.async loads
-      if (o.tileSizes.size() > 2 && (o.tileSizes[2] == 3 || o.tileSizes[2] == 4))
-        m.fcLoads = o.tileSizes[2] == 3 ? 1 : 2;
+      if (o.tileSizes.size() > 2 && (o.tileSizes[2] == 3 || o.tileSizes[2] == 4 || o.tileSizes[2] == 5))
+        m.fcLoads = o.tileSizes[2] == 3 ? 1 : o.tileSizes[2] == 4 ? 2 : 3;
       if (o.tileSizes.size() > 2 && o.tileSizes[2] == 2) {
         // tile_sizes[2] == 2: register chains, tile_sizes[0] rows per CTA
         m.fcKind = 1;
