@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kFcMaxThreads)
   // ---- every global load of the kernel is issued up front. A bulk copy
   // costs the issuing thread ~200 cycles, so the copies are dealt round-robin
   // to lane 0 of every warp (copy j -> warp j % warps) and issue in parallel.
-  if (p.bulk) {
+  if (p.bulk == 1) {
     const int warp = tid >> 5, nw = (T + 31) >> 5, lane = tid & 31;
     const unsigned rowBytes = (unsigned)a.L[0].kred * 4u;
     if (tid == 0) {
