@@ -292,10 +292,7 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     for (int e = tid; e < (R - rows) * p.ald[0]; e += T) sm[p.offAct[0] + rows * p.ald[0] + e] = 0.0f;
     if (rows < R) __syncthreads();
   } else if (p.bulk == 2) {
-    // 16-byte cp.async from every thread, one commit group per layer (the
-    // input rows ride with layer 0): for small per-CTA loads (MLP3: ~12 KB)
-    // the SM's bulk-copy engine costs more in per-copy issue than it saves
-    // (profiles/r02_fc_notes.txt)
+    // 16-byte cp.async from every thread (a tunable; see planFc)
     // Layer 0 lands in p.nch reduction chunks (its input rows and weight
     // slice, one commit group per chunk), so its chains start on chunk 0
     // while the rest is in flight; every later layer is one more group.
@@ -458,10 +455,11 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads =
   for (int l = 0; l < a.layers; ++l)
     bulk = bulk && (a.L[l].kred % 4 == 0) && (a.L[l].ldw % 4 == 0) &&
            ((reinterpret_cast<uintptr_t>(a.L[l].W) & 15) == 0);
-  // automatic loads: 16-byte cp.async from every thread (measured faster
-  // than the bulk-copy engine for every FC chain at the paper shapes,
-  // profiles/r02_fc_notes.txt)
-  p.bulk = !bulk ? 0 : loads == 1 ? 1 : 2;
+  // automatic loads: the bulk-copy engine. 16-byte cp.async from every
+  // thread (loads 2/3) measured slower at every paper shape — MLP3 5.95 vs
+  // 5.49 us, 2FCRelu 16.9 vs 7.9, MLP1 15.5 vs 6.5: an SM keeps too few
+  // cp.async sectors in flight for ~90 KB per CTA (profiles/r02_fc_notes.txt)
+  p.bulk = !bulk ? 0 : (loads == 2 || loads == 3) ? 2 : 1;
   const bool oneChunk = loads == 3;
   {
     // layer-0 chunks: ~256-step pieces, at most 4, multiples of 16 steps

@@ -83,8 +83,8 @@ struct FcChainArgs {
   int layers;
   FcLayer L[kMaxLayers];
 };
-// loads: 0 = automatic (16-byte cp.async for <= 32 KB per CTA, else the bulk
-// copy engine), 1 = bulk copies, 2 = cp.async
+// loads: 0 = automatic (bulk copies), 1 = bulk copies, 2 = 16-byte cp.async
+// with layer 0 in reduction chunks, 3 = cp.async in one chunk
 cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s, int loads = 0);
 size_t fcChainSmem(const FcChainArgs& a, int rows, int cn);
 int fcChainThreads(const FcChainArgs& a, int rows, int cn);  // single-pass block size
