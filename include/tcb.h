@@ -249,6 +249,13 @@ int tcb_concat_cols(const float* const* srcs, const int64_t* widths, int n, int6
 /* pinned host memory for TCB_HOST tensors (cudaMallocHost) */
 int tcb_host_alloc(void** p, int64_t bytes);
 int tcb_host_free(void* p);
+/* device memory and synchronisation for hosts that do not link the CUDA
+ * runtime themselves (the `tcb` CLI's latency verb): cudaMalloc / cudaFree,
+ * cudaMemcpy (kind inferred from the pointers), cudaStreamSynchronize */
+int tcb_device_alloc(void** p, int64_t bytes);
+int tcb_device_free(void* p);
+int tcb_copy(void* dst, const void* src, int64_t bytes);
+int tcb_stream_sync(void* stream);
 
 #ifdef __cplusplus
 }

@@ -110,6 +110,10 @@ def _load():
                                       C.c_void_p, C.c_void_p]),
         "tcb_host_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_int64]),
         "tcb_host_free": (C.c_int, [C.c_void_p]),
+        "tcb_device_alloc": (C.c_int, [C.POINTER(C.c_void_p), C.c_int64]),
+        "tcb_device_free": (C.c_int, [C.c_void_p]),
+        "tcb_copy": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+        "tcb_stream_sync": (C.c_int, [C.c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -130,7 +134,7 @@ EXPORTED = [
     "tcb_cache_deserialize", "tcb_cache_lookup", "tcb_cache_inject", "tcb_canonical",
     "tcb_session_inputs", "tcb_fill_uniform", "tcb_options_validate", "tcb_options_normalize",
     "tcb_options_digest", "tcb_options_baseline", "tcb_options_default", "tcb_host_alloc",
-    "tcb_host_free", "tcb_tensor_file_write", "tcb_tensor_file_read", "tcb_tensor_file_free", "tcb_def_params",
+    "tcb_host_free", "tcb_device_alloc", "tcb_device_free", "tcb_copy", "tcb_stream_sync", "tcb_tensor_file_write", "tcb_tensor_file_read", "tcb_tensor_file_free", "tcb_def_params",
     "tcb_cache_entries", "tcb_concat_cols",
 ]
 

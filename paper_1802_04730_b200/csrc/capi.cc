@@ -824,6 +824,18 @@ int tcb_host_alloc(void** p, int64_t bytes) {
 int tcb_host_free(void* p) {
   return guarded([&] { cudaOk(cudaFreeHost(p), "cudaFreeHost"); });
 }
+int tcb_device_alloc(void** p, int64_t bytes) {
+  return guarded([&] { cudaOk(cudaMalloc(p, static_cast<size_t>(bytes)), "cudaMalloc"); });
+}
+int tcb_device_free(void* p) {
+  return guarded([&] { cudaOk(cudaFree(p), "cudaFree"); });
+}
+int tcb_copy(void* dst, const void* src, int64_t bytes) {
+  return guarded([&] { cudaOk(cudaMemcpy(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault), "cudaMemcpy"); });
+}
+int tcb_stream_sync(void* stream) {
+  return guarded([&] { cudaOk(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "sync"); });
+}
 
 }  // extern "C"
 

@@ -8,6 +8,11 @@
 //               [options] [--cache PATH] [--profile]
 //   tcb tune    FILE --def NAME --sizes ... [--pop P] [--gens G] [--seed S]
 //               [--log PATH] --cache PATH
+//   tcb latency FILE --def NAME --sizes ... [--iters N] [--warmup W] [options]
+//               the paper's protocol: N synchronised
+//               calls of tcb_run on device tensors (session inputs), host
+//               wall time per call (launch + kernel + sync); prints one JSON
+//               line with p0/p50/p90/p99 in us and the device time
 //   tcb cache   list|inspect|inject|purge --cache PATH
 //               [inspect: --index I] [inject: FILE --def NAME --sizes ... --options JSON --cost NS]
 //
@@ -20,6 +25,8 @@
 // spec's contract: 0 success, 1 user/input error, 2 internal.
 // `run` has no CPU path: the reference interpreter is not part of tc-b200
 // (use --compare against tensors the reference wrote).
+#include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -426,6 +433,68 @@ int cmdCache(const Args& a) {
 
 }  // namespace
 
+int cmdLatency(const Args& a) {
+  Engine E;
+  loadCache(a);
+  std::string src = readFile(a.file), def = a.need("def");
+  ck(tcb_define(E.e, src.c_str()), "define");
+  Shapes s = bindSizes(E.e, def, a.need("sizes"));
+  std::vector<std::vector<uint32_t>> hin(s.in.size()), hout(s.out.size());
+  for (size_t i = 0; i < s.in.size(); ++i) {
+    hin[i].assign(static_cast<size_t>(volume(s.in[i])), 0u);
+    s.in[i].data = hin[i].data();
+  }
+  for (size_t i = 0; i < s.out.size(); ++i) {
+    hout[i].assign(static_cast<size_t>(volume(s.out[i])), 0u);
+    s.out[i].data = hout[i].data();
+  }
+  ck(tcb_session_inputs(E.e, def.c_str(), s.in.data(), static_cast<int>(s.in.size()), s.out.data(),
+                        static_cast<int>(s.out.size()), 0),
+     "session inputs");
+  // device copies of every tensor: the call under test reads device tensors,
+  // as the reference's caller passes DLTensors resident on the GPU
+  std::vector<tcb_tensor> din = s.in, dout = s.out;
+  std::vector<void*> bufs;
+  auto toDev = [&](tcb_tensor& t) {
+    void* p = nullptr;
+    const int64_t bytes = volume(t) * 4;
+    ck(tcb_device_alloc(&p, bytes), "device alloc");
+    ck(tcb_copy(p, t.data, bytes), "copy");
+    t.data = p;
+    t.location = TCB_DEVICE;
+    bufs.push_back(p);
+  };
+  for (auto& t : din) toDev(t);
+  for (auto& t : dout) toDev(t);
+  Json d;
+  uint64_t h = compile(a, E.e, def, s, &d);
+  const int iters = std::atoi(a.get("iters", "1000").c_str()), warm = std::atoi(a.get("warmup", "100").c_str());
+  auto call = [&] {
+    ck(tcb_run(E.e, h, din.data(), static_cast<int>(din.size()), dout.data(), static_cast<int>(dout.size()), nullptr,
+               TCB_RUN_NOCHECK, nullptr),
+       "run");
+    ck(tcb_stream_sync(nullptr), "sync");
+  };
+  for (int i = 0; i < warm; ++i) call();
+  std::vector<double> us(iters);
+  for (int i = 0; i < iters; ++i) {
+    auto t0 = std::chrono::steady_clock::now();
+    call();
+    us[i] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  }
+  std::sort(us.begin(), us.end());
+  int64_t ns = 0;
+  ck(tcb_run(E.e, h, din.data(), static_cast<int>(din.size()), dout.data(), static_cast<int>(dout.size()), nullptr,
+             TCB_RUN_PROFILE, &ns),
+     "run");
+  auto pct = [&](double q) { return us[std::min<size_t>(us.size() - 1, static_cast<size_t>(q * us.size()))]; };
+  std::printf("{\"def\": \"%s\", \"kernel\": \"%s\", \"iters\": %d, \"us_p0\": %.2f, \"us_p50\": %.2f, "
+              "\"us_p90\": %.2f, \"us_p99\": %.2f, \"device_us\": %.3f}\n",
+              def.c_str(), d.at("kernel").asStr().c_str(), iters, us[0], pct(0.5), pct(0.9), pct(0.99), ns * 1e-3);
+  for (void* p : bufs) tcb_device_free(p);
+  return 0;
+}
+
 int main(int argc, char** argv) {
   try {
     Args a = parse(argc, argv);
@@ -435,7 +504,8 @@ int main(int argc, char** argv) {
     if (a.verb == "run") return cmdRun(a);
     if (a.verb == "tune") return cmdTune(a);
     if (a.verb == "cache") return cmdCache(a);
-    die(1, "unknown verb '" + a.verb + "' (check | compile | run | tune | cache)");
+    if (a.verb == "latency") return cmdLatency(a);
+    die(1, "unknown verb '" + a.verb + "' (check | compile | run | tune | cache | latency)");
   } catch (const Exit& e) {
     std::fprintf(stderr, "tcb: %s\n", e.msg.c_str());
     return e.code;
