@@ -483,14 +483,25 @@ int cmdLatency(const Args& a) {
     us[i] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
   }
   std::sort(us.begin(), us.end());
+  // host cost of one tcb_run alone: enqueue-only calls back to back
+  ck(tcb_stream_sync(nullptr), "sync");
+  const int nh = std::min(iters, 200);
+  auto h0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < nh; ++i)
+    ck(tcb_run(E.e, h, din.data(), static_cast<int>(din.size()), dout.data(), static_cast<int>(dout.size()), nullptr,
+               TCB_RUN_NOCHECK, nullptr),
+       "run");
+  const double hostUs = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h0).count() / nh;
+  ck(tcb_stream_sync(nullptr), "sync");
   int64_t ns = 0;
   ck(tcb_run(E.e, h, din.data(), static_cast<int>(din.size()), dout.data(), static_cast<int>(dout.size()), nullptr,
              TCB_RUN_PROFILE, &ns),
      "run");
   auto pct = [&](double q) { return us[std::min<size_t>(us.size() - 1, static_cast<size_t>(q * us.size()))]; };
   std::printf("{\"def\": \"%s\", \"kernel\": \"%s\", \"iters\": %d, \"us_p0\": %.2f, \"us_p50\": %.2f, "
-              "\"us_p90\": %.2f, \"us_p99\": %.2f, \"device_us\": %.3f}\n",
-              def.c_str(), d.at("kernel").asStr().c_str(), iters, us[0], pct(0.5), pct(0.9), pct(0.99), ns * 1e-3);
+              "\"us_p90\": %.2f, \"us_p99\": %.2f, \"device_us\": %.3f, \"host_enqueue_us\": %.2f}\n",
+              def.c_str(), d.at("kernel").asStr().c_str(), iters, us[0], pct(0.5), pct(0.9), pct(0.99), ns * 1e-3,
+              hostUs);
   for (void* p : bufs) tcb_device_free(p);
   return 0;
 }
