@@ -84,6 +84,16 @@ struct Compiled {
   std::vector<void*> dIn, dOut;
   std::vector<size_t> inBytes, outBytes;
   std::vector<bool> outInout;
+  // the compiled tensor signature, flattened once (tcb_run's per-call check
+  // compares against it without map lookups or allocations)
+  struct Sig {
+    int rank = 0, dtype = TCB_F32;
+    bool scalar = false;
+    int64_t dims[TCB_MAX_RANK] = {};
+    const std::string* name = nullptr;
+  };
+  std::vector<Sig> inSig, outSig;
+  std::once_flag sigOnce;
   // recorded after a host run's last read of the staging buffers (its D2H);
   // the next host run, on any stream, waits for it before overwriting them
   cudaEvent_t stagingFree = nullptr;
@@ -369,6 +379,34 @@ void ensureStaging(Compiled& c) {
 
 }  // namespace
 
+// flattens the compiled tensor signature of a handle (once)
+static void buildSigOnce(Compiled& c) {
+  std::vector<Compiled::Sig> in, out;
+  for (const auto& p : c.spec.v.def.params) {
+    Compiled::Sig s;
+    s.name = &p.name;
+    s.scalar = p.scalar();
+    if (!s.scalar) {
+      const auto& sh = c.spec.shapes.at(p.name);
+      s.rank = static_cast<int>(sh.size());
+      std::copy(sh.begin(), sh.end(), s.dims);
+      s.dtype = p.elem == lang::Elem::Int ? TCB_I32 : TCB_F32;
+    }
+    in.push_back(s);
+  }
+  for (const auto& r : c.spec.v.def.rets) {
+    Compiled::Sig s;
+    s.name = &r;
+    const auto& sh = c.spec.shapes.at(r);
+    s.rank = static_cast<int>(sh.size());
+    std::copy(sh.begin(), sh.end(), s.dims);
+    out.push_back(s);
+  }
+  c.outSig = std::move(out);
+  c.inSig = std::move(in);
+}
+static void buildSig(Compiled& c) { std::call_once(c.sigOnce, [&] { buildSigOnce(c); }); }
+
 int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_tensor* out, int nout, void* stream,
             int flags, int64_t* duration_ns) {
   return guarded([&] {
@@ -383,16 +421,18 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
     if (nin != static_cast<int>(params.size()) || nout != static_cast<int>(rets.size()))
       fail(ErrorKind::ShapeMismatch, "run: wrong number of inputs or outputs for '" + c.name + "'");
     bool host = false, dev = false;
-    auto checkT = [&](const tcb_tensor& t, const std::string& nm, bool isInt) {
-      if (shapeOf(t) != c.spec.shapes.at(nm))
-        fail(ErrorKind::ShapeMismatch, "run: tensor '" + nm + "' does not have the compiled shape");
-      if (t.dtype != (isInt ? TCB_I32 : TCB_F32)) fail(ErrorKind::ShapeMismatch, "run: tensor '" + nm + "' has the wrong dtype");
-      if (!t.data) fail(ErrorKind::Io, "run: tensor '" + nm + "' has no data");
+    buildSig(c);
+    auto checkT = [&](const tcb_tensor& t, const Compiled::Sig& g) {
+      bool ok = t.rank == g.rank;
+      for (int d = 0; ok && d < g.rank; ++d) ok = t.shape[d] == g.dims[d];
+      if (!ok) fail(ErrorKind::ShapeMismatch, "run: tensor '" + *g.name + "' does not have the compiled shape");
+      if (t.dtype != g.dtype) fail(ErrorKind::ShapeMismatch, "run: tensor '" + *g.name + "' has the wrong dtype");
+      if (!t.data) fail(ErrorKind::Io, "run: tensor '" + *g.name + "' has no data");
       (t.location == TCB_HOST ? host : dev) = true;
     };
     for (int i = 0; i < nin; ++i)
-      if (!params[i].scalar()) checkT(in[i], params[i].name, params[i].elem == lang::Elem::Int);
-    for (int i = 0; i < nout; ++i) checkT(out[i], rets[i], false);
+      if (!c.inSig[i].scalar) checkT(in[i], c.inSig[i]);
+    for (int i = 0; i < nout; ++i) checkT(out[i], c.outSig[i]);
     if (host && dev) fail(ErrorKind::Io, "run: mixing host and device tensors in one call is not supported");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
 
@@ -402,12 +442,22 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
       cudaOk(cudaMemset(c.dErr, 0, sizeof(int)), "cudaMemset");
     }
     c.lastStream = s;
-    std::vector<void*> din(nin), dout(nout);
+    // per-call pointer lists without heap allocations for the usual arity
+    void* dinBuf[16];
+    void* doutBuf[16];
+    const void* mapBuf[16];
+    std::vector<void*> dinV, doutV;
+    std::vector<const void*> mapV;
+    void** din = dinBuf;
+    void** dout = doutBuf;
+    const void** outMapped = mapBuf;
+    if (nin > 16) dinV.resize(nin), din = dinV.data();
+    if (nout > 16) doutV.resize(nout), mapV.resize(nout), dout = doutV.data(), outMapped = mapV.data();
+    for (int i = 0; i < nout; ++i) outMapped[i] = nullptr;
     bool profile = (flags & TCB_RUN_PROFILE) != 0;
     // host tensors: mapped pinned buffers up to zeroCopyMax() move in one
     // segment-copy launch per direction; the rest (pageable or large) by DMA
     k::SegCopyArgs up{}, down{};
-    std::vector<const void*> outMapped(nout, nullptr);
     if (host) {
       ensureStaging(c);
       if (!c.stagingFree) cudaOk(cudaEventCreateWithFlags(&c.stagingFree, cudaEventDisableTiming), "event");
@@ -446,7 +496,7 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
       cudaOk(cudaEventCreate(&ev1), "event");
       cudaOk(cudaEventRecord(ev0, s), "record");
     }
-    ops::launch(c.prob, c.map, din.data(), dout.data(), c.dErr, s);
+    ops::launch(c.prob, c.map, din, dout, c.dErr, s);
     if (profile) cudaOk(cudaEventRecord(ev1, s), "record");
     if (host) {
       for (int i = 0; i < nout; ++i) {

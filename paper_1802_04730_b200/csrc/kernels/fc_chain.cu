@@ -508,8 +508,10 @@ cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, c
   if (threads < 32 || threads > kFcMaxThreads || threads % 32) return cudaErrorInvalidConfiguration;
   void (*kern)(FcChainArgs, FcPlan) = fcKernel(a.layers);
   if (!kern) return cudaErrorInvalidValue;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (cn > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  {
+    cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kern), (int)smem, cn > 8);
+    if (e != cudaSuccess) return e;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cn, (a.batch + rows - 1) / rows, 1);
   cfg.blockDim = dim3(threads, 1, 1);

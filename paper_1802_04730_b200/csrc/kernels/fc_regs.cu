@@ -259,8 +259,8 @@ cudaError_t launchFcRegs(const FcChainArgs& a, int rows, cudaStream_t s) {
   const size_t smem = (size_t)off * 4;
   void* kern = a.layers == 1 ? pickRegs<1>(rows) : a.layers == 2 ? pickRegs<2>(rows) : pickRegs<3>(rows);
   if (!kern) return cudaErrorInvalidValue;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kern), (int)smem);
     if (e != cudaSuccess) return e;
   }
   void* args[] = {const_cast<FcChainArgs*>(&a), &p};

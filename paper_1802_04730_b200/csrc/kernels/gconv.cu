@@ -200,7 +200,10 @@ cudaError_t launchV(const GconvArgs& a, int th, cudaStream_t s) {
   const int want = static_cast<int>(std::max<int64_t>(1, (4 * sms + pairs - 1) / pairs));
   const int rpb = std::max(1, (nblk + want - 1) / want);
   auto kfn = gconv_kernel<RF, RW, KW>;
-  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kfn), (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   dim3 grid((nblk + rpb - 1) / rpb, a.G, a.N);
   kfn<<<grid, threads, smem, s>>>(a, th, TW, TF, rpb);
   return cudaGetLastError();

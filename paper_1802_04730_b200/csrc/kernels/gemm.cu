@@ -861,7 +861,10 @@ cudaError_t launchBatched(const GemmArgs& a, int grid, cudaStream_t s) {
   const int ntask = ((a.M + RM - 1) / RM) * ((a.N + RN - 1) / RN);
   const int threads = std::max(32, std::min(512, (ntask + 31) / 32 * 32));
   auto kfn = gemm_nt_batched<RM, RN>;
-  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kfn), (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   kfn<<<grid, threads, smem, s>>>(a, ldS, S);
   return cudaGetLastError();
 }
@@ -880,8 +883,8 @@ cudaError_t launchSlabCh(const GemmArgs& a, cudaStream_t s) {
   const int K4 = a.K / 4;
   const size_t smem = ((size_t)ng * CH * K4 + (size_t)32 * nb * (K4 | 1)) * 16;
   auto kfn = gemm_nt_slab<CH>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kfn), (int)smem);
     if (e != cudaSuccess) return e;
   }
   kfn<<<grid, threads, smem, s>>>(a, ng);
@@ -899,8 +902,8 @@ cudaError_t launchSlabRt(const GemmArgs& a, cudaStream_t s) {
   const int ld = BULK ? a.K / 4 : (a.K / 4) | 1;
   const size_t smem = (size_t)(wm * wmt + wn * wnt) * ld * 16 + 8 * 8;
   auto kfn = gemm_nt_slab_rt<RM, RN, BULK>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kfn), (int)smem);
     if (e != cudaSuccess) return e;
   }
   kfn<<<grid, wm * wn * 32, smem, s>>>(a, wm);
@@ -917,8 +920,8 @@ cudaError_t launchWarpBatch(const GemmArgs& a, int warps, cudaStream_t s) {
   const size_t smem = (size_t)warps * (a.M + a.N) * ld * 16 + 8 * warps;
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
   auto kfn = gemm_nt_warpbatch<RM, RN>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kfn), (int)smem);
     if (e != cudaSuccess) return e;
   }
   kfn<<<(a.batch + warps - 1) / warps, warps * 32, smem, s>>>(a, dense);
@@ -932,8 +935,8 @@ cudaError_t launchTiled(const GemmArgs& a, int vec, cudaStream_t s) {
   auto kfn = gemm_nt_tiled<TM, TN, RM, RN, TK, S>;
   // set on every launch: the attribute is per device context, and a cached
   // per-process flag would leave other devices at the 48 KB default
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kfn), (int)smem);
     if (e != cudaSuccess) return e;
   }
   kfn<<<grid, (TM / RM) * (TN / RN), smem, s>>>(a, vec);

@@ -15,6 +15,13 @@
 namespace tcb {
 namespace k {
 
+// Sets a kernel's dynamic shared-memory limit (and, when asked, the
+// non-portable cluster size permission) on the current device, once per
+// (kernel, device, size): function attributes belong to a device context, and
+// a cudaFuncSetAttribute on every launch costs host time on the paper's
+// synchronised-call protocol. Thread-safe (attr.cu).
+cudaError_t ensureFuncAttrs(const void* fn, int smemBytes, bool nonPortableCluster = false);
+
 // ------------------------------------------------------------- GEMM-NT
 // C[b][m][n] = epi(init + sum_k A[b][m][k] * B[b][n][k]),  k ascending.
 enum InitMode : int { kInitZero = 0, kInitInout = 1, kInitBias = 2 };

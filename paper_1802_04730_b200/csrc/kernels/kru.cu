@@ -216,7 +216,10 @@ cudaError_t launchKru3(const KruArgs& a, int DC, int threads, cudaStream_t s) {
   if (smem > 227 * 1024 || DC < 1 || threads > 512) return cudaErrorInvalidConfiguration;
   const int tiled = tiledShape(a, DC) ? 1 : 0;
   auto kfn = kru3_kernel<16>;
-  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  {
+    cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kfn), (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   dim3 grid((a.D2 + DC - 1) / DC, a.M);
   kfn<<<grid, threads, smem, s>>>(a, DC, tiled);
   return cudaGetLastError();

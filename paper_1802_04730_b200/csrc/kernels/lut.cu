@@ -167,7 +167,7 @@ cudaError_t launchLut(const LutArgs* tables, int ntables, int threads, cudaStrea
     // attribute is per device context: set on every launch (a per-process
     // flag would leave a second device at the 48 KB default)
     if (smem > 48 * 1024) {
-      cudaError_t e = cudaFuncSetAttribute(lut_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+      cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(lut_smem_kernel), 160 * 1024);
       if (e != cudaSuccess) return e;
     }
     lut_smem_kernel<<<dim3((unsigned)maxB, ntables), t, smem, s>>>(p.t[0], p.t[1]);

@@ -324,7 +324,7 @@ cudaError_t launchT(const TcConvParams& p, cudaStream_t s) {
   q.kc = (p.kSteps + chunks - 1) / chunks;  // balanced chunks
   const int smemBytes = fixed + kStagesConv * Cfg::stageBytes(q.kc);
   if (smemBytes > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smemBytes);
+  cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kern), smemBytes);
   if (e != cudaSuccess) return e;
   kern<<<p.G * p.ctasPerGroup, kThreadsTc, smemBytes, s>>>(q);
   return cudaGetLastError();

@@ -288,7 +288,7 @@ cudaError_t launchShift(const ShiftParams& p, cudaStream_t s) {
   auto kern = tc_gconv_shift_kernel<F, X3>;
   const int smemBytes = Cfg::smem(p);
   if (smemBytes > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smemBytes);
+  cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kern), smemBytes);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

@@ -301,7 +301,7 @@ cudaError_t launchT(const Params& p, cudaStream_t s) {
   auto kern = tc_gconv_nhwc_kernel<F, X3>;
   const int smemBytes = C_::smem(p.kAtoms, p.Mb);
   if (smemBytes > 227 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smemBytes);
+  cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kern), smemBytes);
   if (e != cudaSuccess) return e;
   kern<<<p.G * p.ctasPerGroup, kThreads, smemBytes, s>>>(p);
   return cudaGetLastError();

@@ -222,7 +222,7 @@ cudaError_t launchT(const KruArgs& a, cudaStream_t s) {
   const size_t smemBytes = (size_t)KruCfg<X3>::smemFloats(DN, DN, DC) * 4 + 1024 + 64;
   if (smemBytes > 227 * 1024) return cudaErrorInvalidValue;
   auto kern = tc_kru3_kernel<X3, DN, DC>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemBytes);
+  cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kern), (int)smemBytes);
   if (e != cudaSuccess) return e;
   kern<<<dim3(a.D2 / DC, a.M), kThreadsKru, smemBytes, s>>>(a);
   return cudaGetLastError();
