@@ -837,6 +837,39 @@ def prod_model_line(ee, torch, dev):
         return {"error": f"{type(e).__name__}: {e}"}
 
 
+# the paper's latency protocol from C++ through the C ABI (`tcb latency`,
+# csrc/cli/tcb_main.cc): 1000 synchronised tcb_run calls on device tensors
+CLI_SIZES = {
+    "tmm 128x256x32": ("tmm", "M=128,N=256,K=32"),
+    "tmm 128x1024x1024": ("tmm", "M=128,N=1024,K=1024"),
+    "tbmm 500,26,72,26": ("tbmm", "B=500,N=26,M=72,K=26"),
+    "MLP1 128x1128->128": ("MLP1", "B=128,M=1128,O=128,N=1128"),
+    "2FCRelu 128x1128->128->64": ("2FCRelu", "B=128,M=1128,O=128,N=1128,P=64"),
+    "MLP3 128->64->32->2": ("MLP3", "B=128,M=128,O=64,N=128,P=32,Q=2,O1__0=128,O1__1=128"),
+    "C3 128x1024->1000": ("C3", "B=128,WX=1024,WY=1000"),
+    "3KRU M=256 16^3->32^3": ("3KRU", "D0=32,N0=16,D1=32,N1=16,D2=32,N2=16,M=256"),
+}
+
+
+def capi_latency(label, math="ffma", iters=1000, dev=0):
+    if label not in CLI_SIZES:
+        return None
+    import subprocess
+    d, sizes = CLI_SIZES[label]
+    cmd = [os.path.join(ROOT, "paper_1802_04730_b200", "bin", "tcb"), "latency",
+           os.path.join(ROOT, "paper_1802_04730_b200", "tc", "ops.tc"), "--def", d, "--sizes", sizes,
+           "--iters", str(iters), "--math", math]
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(dev)))
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=120, env=env)
+        j = json.loads(r.stdout.strip().splitlines()[-1])
+        return {"us_p0_p50_p90_p99": [j["us_p0"], j["us_p50"], j["us_p90"], j["us_p99"]],
+                "host_enqueue_us": j["host_enqueue_us"], "iters": j["iters"],
+                "protocol": "C++ (bin/tcb latency): tcb_run on device tensors + stream sync, host wall clock"}
+    except Exception as e:  # report, don't hide
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
 def paper_op_table(ee, torch, dev, stream, peaks):
     """µs/call (device, L2-cold where the working set allows rotation) and the
     paper's protocol (p50 of synchronised calls incl. host overhead,
@@ -883,6 +916,8 @@ def paper_op_table(ee, torch, dev, stream, peaks):
                                                  round(lat[int(len(lat) * 0.9)] * 1e6, 1)],
                           "l2": "cold (rotated)" if nsets > 1 else "warm (working set > L2)" if big else "warm",
                           "kernel": o.kernel, "math": math}
+            if math == "ffma" or label == "tmm 128x256x32":
+                out[label]["capi_sync_latency"] = capi_latency(label, math)
             if math != "ffma":
                 # tensor-pipe roofline: TF32 dense = half the measured bf16 dense peak; 3xTF32
                 # issues three TF32 MMAs per useful multiply-add
