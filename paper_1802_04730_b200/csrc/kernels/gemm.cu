@@ -839,6 +839,14 @@ const GemmVariant kGemmVariants[] = {
     // one warp per batch (tk = -4): the whole batch is one rm x rn warp tile
     {38, 0, 0, 7, 4, -4, "warpbatch_7x4", 0},
     {39, 0, 0, 4, 4, -4, "warpbatch_4x4", 0},
+    // TMA-fed tiles (tk = -5, gemm_tma.cu): two tensor copies per 32-deep stage
+    {40, 32, 32, 4, 4, -5, "tma_t32x32_r4x4", 8},
+    {41, 32, 32, 4, 2, -5, "tma_t32x32_r4x2", 8},
+    {42, 32, 64, 4, 4, -5, "tma_t32x64_r4x4", 6},
+    {43, 16, 32, 2, 4, -5, "tma_t16x32_r2x4", 8},
+    {44, 32, 16, 4, 2, -5, "tma_t32x16_r4x2", 8},
+    {45, 64, 32, 4, 4, -5, "tma_t64x32_r4x4", 6},
+    {46, 32, 32, 2, 2, -5, "tma_t32x32_r2x2", 8},
 };
 
 template <int RM, int RN>
@@ -1027,6 +1035,13 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
       if (variant == 38) return launchWarpBatch<7, 4>(a, threads, s);
       return launchWarpBatch<4, 4>(a, threads, s);
     }
+    case 40:
+    case 41:
+    case 42:
+    case 43:
+    case 44:
+    case 45:
+    case 46: return launchGemmTma(a, variant - 40, s);
     case 19:
     case 20:
     case 21:

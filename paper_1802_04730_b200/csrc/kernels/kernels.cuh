@@ -56,6 +56,9 @@ bool batchedOk(const GemmArgs& a);
 // whether the slab variants (tk == -1) can take this problem: K % 4 == 0,
 // K <= 144 (at most six 24-step reduction chunks), 16-byte rows/strides/pointers
 bool slabOk(const GemmArgs& a);
+// TMA-fed tiles (gemm_tma.cu): 16-byte aligned operands and strides
+bool gemmTmaOk(const GemmArgs& a);
+cudaError_t launchGemmTma(const GemmArgs& a, int which, cudaStream_t s);
 
 // ------------------------------------------------- GEMM-NT, tensor cores
 // tcgen05 .kind::tf32 variant of the same contraction (tc_gemm.cu). Not

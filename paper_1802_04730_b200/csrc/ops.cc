@@ -175,6 +175,21 @@ void decodeGemm(const MappingOptions& o, Mapping& m) {
     }
     invalid("slab GEMM micro-tile must be 4x1, 7x1, 13x1 (broadcast) or 7x4, 4x4, 4x2 (register-tiled)");
   }
+  if (o.tileSizes[2] == 3) {
+    // reduction depth 3 = TMA-fed tiles (32-deep stages): tile tm x tn,
+    // micro-tile (tm / thread_shape[1]) x (tn / thread_shape[0])
+    const int64_t tm = o.tileSizes[0], tn = o.tileSizes[1], tx = o.threadShape[0], ty = o.threadShape[1];
+    for (int i = 1; i < k::gemmVariantCount(); ++i) {
+      const auto& v = k::gemmVariant(i);
+      if (v.tk == -5 && v.tm == tm && v.tn == tn && tx * v.rn == tn && ty * v.rm == tm) {
+        m.gemmVariant = i;
+        m.gemmThreads = static_cast<int>(tx * ty);
+        return;
+      }
+    }
+    invalid("no TMA-fed GEMM kernel for tile " + std::to_string(tm) + "x" + std::to_string(tn) + " with a " +
+            std::to_string(tx) + "x" + std::to_string(ty) + " block");
+  }
   if (o.threadShape[2] != 1) invalid("tiled GEMM uses a 2-D thread block");
   int64_t tm = o.tileSizes[0], tn = o.tileSizes[1], tk = o.tileSizes[2];
   int64_t tx = o.threadShape[0], ty = o.threadShape[1];
@@ -218,7 +233,8 @@ void launchGemmDesc(const GemmDesc& g, const Mapping& m, void* const* in, void* 
     k::TcPlan pl = m.tcAuto ? k::tcGemmPlan(g.batch, g.M, g.N, g.K, smCount()) : m.tc;
     e = k::launchTcGemm(a, m.math, pl, s);
   } else if ((k::gemmVariant(m.gemmVariant).tk == 0 && !k::batchedOk(a)) ||
-             (k::gemmVariant(m.gemmVariant).tk < 0 && !k::slabOk(a))) {
+             (k::gemmVariant(m.gemmVariant).tk < 0 && k::gemmVariant(m.gemmVariant).tk > -5 && !k::slabOk(a)) ||
+             (k::gemmVariant(m.gemmVariant).tk == -5 && !k::gemmTmaOk(a))) {
     // the persistent batched and slab kernels need 16-byte aligned operands
     // (and the slab K <= 144); the tiled kernel computes the same bit-exact
     // chains without that need
@@ -274,7 +290,7 @@ std::string Mapping::describe() const {
     case Family::Gemm:
       if (k::gemmVariant(gemmVariant).tk == -4)
         os << k::gemmVariant(gemmVariant).name << " warps=" << gemmThreads;
-      else if (k::gemmVariant(gemmVariant).tk < 0)
+      else if (k::gemmVariant(gemmVariant).tk < 0 && k::gemmVariant(gemmVariant).tk > -5)
         os << k::gemmVariant(gemmVariant).name;
       else if (k::gemmVariant(gemmVariant).tk == 0)
         os << k::gemmVariant(gemmVariant).name << " grid=" << (gemmThreads ? std::to_string(gemmThreads) : "auto");
@@ -766,7 +782,7 @@ GenePools genePools(const Problem& p, int math) {
       if (p.family == Family::Gemm && p.gemm.batch > 1) {  // + the persistent batched kernel
         g.tile0 = {1, 2, 4, 7, 13, 16, 32, 64};
         g.tile1 = {1, 2, 4, 16, 32, 64};
-        g.tile2 = {1, 2, 16, 32, 64};  // 1 = persistent batched, 2 = slab
+        g.tile2 = {1, 2, 3, 16, 32, 64};  // 1 = persistent batched, 2 = slab, 3 = TMA-fed
       }
       g.tx = {4, 8, 16, 32};
       g.ty = {4, 8, 16, 32};
