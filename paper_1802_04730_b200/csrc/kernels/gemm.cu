@@ -847,6 +847,11 @@ const GemmVariant kGemmVariants[] = {
     {44, 32, 16, 4, 2, -5, "tma_t32x16_r4x2", 8},
     {45, 64, 32, 4, 4, -5, "tma_t64x32_r4x4", 6},
     {46, 32, 32, 2, 2, -5, "tma_t32x32_r2x2", 8},
+    // ... with the A tile multicast over a cluster of `stages` CTAs along N (tk = -6)
+    {47, 32, 32, 2, 2, -6, "tma_t32x32_r2x2_mc4", 4},
+    {48, 32, 32, 4, 2, -6, "tma_t32x32_r4x2_mc4", 4},
+    {49, 32, 16, 2, 2, -6, "tma_t32x16_r2x2_mc4", 4},
+    {50, 32, 32, 2, 2, -6, "tma_t32x32_r2x2_mc2", 2},
 };
 
 template <int RM, int RN>
@@ -1041,7 +1046,11 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
     case 43:
     case 44:
     case 45:
-    case 46: return launchGemmTma(a, variant - 40, s);
+    case 46:
+    case 47:
+    case 48:
+    case 49:
+    case 50: return launchGemmTma(a, variant - 40, s);
     case 19:
     case 20:
     case 21:

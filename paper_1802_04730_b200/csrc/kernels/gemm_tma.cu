@@ -46,18 +46,44 @@ __device__ __forceinline__ float ldsSw1(uint32_t rowBase, int r, int k) {
   return v;
 }
 
+// multicast tensor copy: the box lands at the same offset in every CTA of
+// ctaMask and completes `bytes` on each one's barrier at the same offset
+__device__ __forceinline__ void tmaLoad3dMc(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar,
+                                            uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
+      "[%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem(bar)), "h"(mask)
+      : "memory");
+}
+// arrive on the mbarrier at the same offset in cluster CTA `rank`
+__device__ __forceinline__ void mbarArriveRemote(uint64_t* bar, uint32_t rank) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(smem(bar)),
+      "r"(rank)
+      : "memory");
+}
+
 __device__ __forceinline__ float initOf(const GemmArgs& a, const float* C, int m, int n) {
   if (a.init == kInitInout) return C[(int64_t)m * a.ldc + n];
   if (a.init == kInitBias) return a.bias[n];
   return 0.0f;
 }
 
-template <int TM, int TN, int RM, int RN, int S>
+// CN > 1: the CN CTAs of a cluster along N share their A tile (same rows
+// m0.., different column tiles): each loads TM / CN of its rows and
+// multicasts them to all CN, so every A line leaves L2 once per cluster
+// instead of once per CTA (C3's I3 rows were read by 32 CTAs at once). A
+// stage is refilled only when every consumer warp of every cluster CTA has
+// released it (remote arrivals on each CTA's empty barrier).
+template <int TM, int TN, int RM, int RN, int S, int CN>
 __global__ void __launch_bounds__((TM / RM) * (TN / RN) + 32)
     gemm_nt_tma(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, const GemmArgs a) {
   constexpr int TX = TN / RN, TY = TM / RM, CT = TX * TY, CW = CT / 32;
   constexpr int ABYTES = TM * 128, SBYTES = (TM + TN) * 128;
   static_assert(CT % 32 == 0 && TM % 8 == 0 && TN % 8 == 0, "tile");
+  static_assert(CN == 1 || (TM / CN) % 8 == 0, "multicast slices are whole 8-row swizzle atoms");
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * SBYTES);
@@ -65,14 +91,16 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN) + 32)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n0 = blockIdx.x * TN, m0 = blockIdx.y * TM, b = blockIdx.z;
   const int nk = (a.K + kTK - 1) / kTK;
+  const uint32_t rank = CN > 1 ? clusterRank() : 0;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbarInit(&full[s], 1);
-      mbarInit(&empty[s], CW);
+      mbarInit(&empty[s], CW * CN);
     }
     fenceBarrierInit();
   }
-  __syncthreads();
+  if (CN > 1) clusterSync();  // every CTA's barriers exist before any multicast lands
+  else __syncthreads();
 
   if (warp == CW) {  // ---- producer: one elected lane issues every TMA copy
     if (lane == 0) {
@@ -83,11 +111,18 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN) + 32)
         const int s = kt % S;
         if (kt >= S) mbarWait(&empty[s], ((kt / S) - 1) & 1, 1);
         mbarExpectTx(&full[s], SBYTES);
-        tmaLoad3d(sm + s * SBYTES, &ta, kt * kTK, m0, bA, &full[s]);
+        if (CN > 1) {
+          constexpr int SL = TM / CN;
+          tmaLoad3dMc(sm + s * SBYTES + rank * SL * 128, &ta, kt * kTK, m0 + rank * SL, bA, &full[s],
+                      (uint16_t)((1u << CN) - 1));
+        } else {
+          tmaLoad3d(sm + s * SBYTES, &ta, kt * kTK, m0, bA, &full[s]);
+        }
         tmaLoad3d(sm + s * SBYTES + ABYTES, &tb, kt * kTK, n0, bB, &full[s]);
       }
     }
-    return;  // (no CTA-wide barrier follows)
+    if (CN > 1) clusterSync();  // stay until no peer can still multicast into this CTA
+    return;
   }
 
   // ---- consumers: RM x RN chains per thread
@@ -153,7 +188,12 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN) + 32)
             acc[i][j] = __fmaf_rn(ldsSw1(ra[i], ty + i * TY, kk), ldsSw1(rb[j], tx + j * TX, kk), acc[i][j]);
     }
     __syncwarp();
-    if (lane == 0) mbarArrive(&empty[s]);  // this warp is done with stage s
+    if (lane == 0) {  // this warp is done with stage s (in every cluster CTA: they share its A slice)
+      if (CN > 1)
+        for (uint32_t r = 0; r < CN; ++r) mbarArriveRemote(&empty[s], r);
+      else
+        mbarArrive(&empty[s]);
+    }
   }
 #pragma unroll
   for (int i = 0; i < RM; ++i)
@@ -166,6 +206,7 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN) + 32)
         C[(int64_t)m * a.ldc + n] = v;
       }
     }
+  if (CN > 1) clusterSync();
 }
 
 // ------------------------------------------------------------------ host
@@ -214,19 +255,38 @@ bool mapOf(CUtensorMap* m, const float* base, int K, int rows, int batch, int64_
   return true;
 }
 
-template <int TM, int TN, int RM, int RN, int S>
+template <int TM, int TN, int RM, int RN, int S, int CN = 1>
 cudaError_t launchT(const GemmArgs& a, cudaStream_t s) {
   CUtensorMap ta, tb;
   const int batched = a.batch > 1;
-  if (!mapOf(&ta, a.A, a.K, a.M, batched && a.sA ? a.batch : 1, a.lda, a.sA, TM)) return cudaErrorInvalidValue;
+  if (!mapOf(&ta, a.A, a.K, a.M, batched && a.sA ? a.batch : 1, a.lda, a.sA, CN > 1 ? TM / CN : TM))
+    return cudaErrorInvalidValue;
   if (!mapOf(&tb, a.B, a.K, a.N, batched && a.sB ? a.batch : 1, a.ldb, a.sB, TN)) return cudaErrorInvalidValue;
-  auto kfn = gemm_nt_tma<TM, TN, RM, RN, S>;
+  auto kfn = gemm_nt_tma<TM, TN, RM, RN, S, CN>;
   const int smem = S * (TM + TN) * 128 + 2 * S * 8 + 1024;
   cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kfn), smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((a.N + TN - 1) / TN, (a.M + TM - 1) / TM, a.batch);
-  kfn<<<grid, (TM / RM) * (TN / RN) + 32, smem, s>>>(ta, tb, a);
-  return cudaGetLastError();
+  const int tilesN = (a.N + TN - 1) / TN;
+  // the grid's N extent rounded up to whole clusters (CTAs past N load and
+  // share their A slice, store nothing)
+  dim3 grid((tilesN + CN - 1) / CN * CN, (a.M + TM - 1) / TM, a.batch);
+  if (CN == 1) {
+    kfn<<<grid, (TM / RM) * (TN / RN) + 32, smem, s>>>(ta, tb, a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3((TM / RM) * (TN / RN) + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CN;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kfn, ta, tb, a);
 }
 
 }  // namespace
@@ -238,8 +298,9 @@ bool gemmTmaOk(const GemmArgs& a) {
          a.batch <= 65535 && sm100::encodeFn() != nullptr;
 }
 
-// (TM, TN, RM, RN): 0 (32,32,4,4)  1 (32,32,4,2)  2 (32,64,4,4)  3 (16,32,2,4)
-//                   4 (32,16,4,2)  5 (64,32,4,4)  6 (32,32,2,2)
+// (TM, TN, RM, RN[, A multicast over CN]): 0 (32,32,4,4)  1 (32,32,4,2)
+// 2 (32,64,4,4)  3 (16,32,2,4)  4 (32,16,4,2)  5 (64,32,4,4)  6 (32,32,2,2)
+// 7 (32,32,2,2 CN 4)  8 (32,32,4,2 CN 4)  9 (32,16,2,2 CN 4)  10 (32,32,2,2 CN 2)
 cudaError_t launchGemmTma(const GemmArgs& a, int which, cudaStream_t s) {
   if (!gemmTmaOk(a)) return cudaErrorInvalidValue;
   switch (which) {
@@ -250,6 +311,10 @@ cudaError_t launchGemmTma(const GemmArgs& a, int which, cudaStream_t s) {
     case 4: return launchT<32, 16, 4, 2, 8>(a, s);
     case 5: return launchT<64, 32, 4, 4, 6>(a, s);
     case 6: return launchT<32, 32, 2, 2, 8>(a, s);
+    case 7: return launchT<32, 32, 2, 2, 8, 4>(a, s);
+    case 8: return launchT<32, 32, 4, 2, 8, 4>(a, s);
+    case 9: return launchT<32, 16, 2, 2, 8, 4>(a, s);
+    case 10: return launchT<32, 32, 2, 2, 8, 2>(a, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -177,11 +177,14 @@ void decodeGemm(const MappingOptions& o, Mapping& m) {
   }
   if (o.tileSizes[2] == 3) {
     // reduction depth 3 = TMA-fed tiles (32-deep stages): tile tm x tn,
-    // micro-tile (tm / thread_shape[1]) x (tn / thread_shape[0])
+    // micro-tile (tm / thread_shape[1]) x (tn / thread_shape[0]);
+    // block_shape[1] > 1: the A tile multicast over that many CTAs along N
     const int64_t tm = o.tileSizes[0], tn = o.tileSizes[1], tx = o.threadShape[0], ty = o.threadShape[1];
+    const int64_t mc = o.blockShape[1];
     for (int i = 1; i < k::gemmVariantCount(); ++i) {
       const auto& v = k::gemmVariant(i);
-      if (v.tk == -5 && v.tm == tm && v.tn == tn && tx * v.rn == tn && ty * v.rm == tm) {
+      const bool kind = mc > 1 ? (v.tk == -6 && v.stages == mc) : v.tk == -5;
+      if (kind && v.tm == tm && v.tn == tn && tx * v.rn == tn && ty * v.rm == tm) {
         m.gemmVariant = i;
         m.gemmThreads = static_cast<int>(tx * ty);
         return;
@@ -234,7 +237,7 @@ void launchGemmDesc(const GemmDesc& g, const Mapping& m, void* const* in, void* 
     e = k::launchTcGemm(a, m.math, pl, s);
   } else if ((k::gemmVariant(m.gemmVariant).tk == 0 && !k::batchedOk(a)) ||
              (k::gemmVariant(m.gemmVariant).tk < 0 && k::gemmVariant(m.gemmVariant).tk > -5 && !k::slabOk(a)) ||
-             (k::gemmVariant(m.gemmVariant).tk == -5 && !k::gemmTmaOk(a))) {
+             (k::gemmVariant(m.gemmVariant).tk <= -5 && !k::gemmTmaOk(a))) {
     // the persistent batched and slab kernels need 16-byte aligned operands
     // (and the slab K <= 144); the tiled kernel computes the same bit-exact
     // chains without that need

@@ -103,8 +103,9 @@ def test_every_gemm_variant_identical(engine, oracle, golden, name):
     assert ran == len(variants) + 1
 
 
-TMA_VARIANTS = [(32, 32, 4, 4), (32, 32, 4, 2), (32, 64, 4, 4), (16, 32, 2, 4), (32, 16, 4, 2), (64, 32, 4, 4),
-                (32, 32, 2, 2)]
+TMA_VARIANTS = [(32, 32, 4, 4, 1), (32, 32, 4, 2, 1), (32, 64, 4, 4, 1), (16, 32, 2, 4, 1), (32, 16, 4, 2, 1),
+                (64, 32, 4, 4, 1), (32, 32, 2, 2, 1), (32, 32, 2, 2, 4), (32, 32, 4, 2, 4), (32, 16, 2, 2, 4),
+                (32, 32, 2, 2, 2)]
 
 
 @pytest.mark.parametrize("name", ["tmm_small", "tbmm_small", "c3_small", "mlp1_ragged", "c3_paper", "tmm_paper",
@@ -114,16 +115,18 @@ def test_tma_gemm_variants(engine, oracle, golden, name):
     instantiated tile, bit-exact against the reference's goldens: ragged
     M/N edges (TMA zero fill, masked stores), a partial last k stage
     (K % 32 != 0), batches, in/out C3. Operands whose rows are not 16-byte
-    multiples (mlp1_ragged) fall back to the tiled kernel, same bits."""
+    multiples (mlp1_ragged) fall back to the tiled kernel, same bits. mc > 1:
+    the A tile multicast over a cluster along N (grids padded to whole
+    clusters: tmm_small's 48 columns are 2 tiles of a 4-cluster)."""
     case, ins, seeded = case_inputs(oracle, golden, name)
     ref = oracle_outputs(oracle, case, ins, seeded)
-    for tm, tn, rm, rn in TMA_VARIANTS:
-        o = {"block_shape": [1, 1, 1], "fusion_strategy": "min" if case["def"] == "MLP1" else "max", "rng_seed": 0,
+    for tm, tn, rm, rn, mc in TMA_VARIANTS:
+        o = {"block_shape": [1, mc, 1], "fusion_strategy": "min" if case["def"] == "MLP1" else "max", "rng_seed": 0,
              "shared_memory_budget": 49152, "thread_shape": [tn // rn, tm // rm, 1], "tile_sizes": [tm, tn, 3],
              "unroll_copy_shared": False, "unroll_factor": 1, "use_private": True, "use_shared": True}
         got, h = run_on_gpu(engine, case["def"], ins, seeded, options=o)
         for k in case["outputs"]:
-            assert_exact(oracle, f"{name}/tma{tm}x{tn}r{rm}x{rn}", k, got[k], case["outputs"][k]["fnv"], ref[k])
+            assert_exact(oracle, f"{name}/tma{tm}x{tn}r{rm}x{rn}mc{mc}", k, got[k], case["outputs"][k]["fnv"], ref[k])
 
 
 @pytest.mark.parametrize("name", ["tbmm_small", "tbmm_paper"])
