@@ -628,10 +628,13 @@ MappingOptions defaultOptions(const Problem& p, int math) {
         break;
       }
       if (g.K > 128 && ctas(32, 32) >= 96) {
-        // long reductions with enough 32x32 tiles: 64-deep k stages (measured
-        // best of the 19 variants for C3 / TMM 128x1024x1024 on B200)
-        o.tileSizes = {32, 32, 64};
+        // long reductions with enough 32x32 tiles: the TMA-fed tiles (8 x 32-
+        // deep stages in flight; C3 and TMM 128x1024x1024 21.6 -> 16.9 us,
+        // profiles/r02_tma_sweep.txt); the tiled kernel's cp.async ring where
+        // the operands cannot take a tensor map (ops::launchGemmDesc)
+        o.tileSizes = {32, 32, 3};
         o.threadShape = {{16, 16, 1}};
+        o.blockShape = {{1, 1, 1}};
         o.unrollCopyShared = false;
         break;
       }
