@@ -722,7 +722,7 @@ def main():
     try:  # committed ncu --set full capture of the same kernel
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tj = json.load(f)["per_launch"].get(dom.name, {})
-            if tj.get("kernel") in (None, dom.kernel):
+            if tj.get("describe") in (None, dom.kernel):  # the capture is of this plan
                 traffic = tj.get("dram_bytes")
     except Exception:
         traffic = None
