@@ -16,17 +16,20 @@ from paper_1802_04730_b200 import ExecutionEngine  # noqa: E402
 
 NSTEP = int(os.environ.get("NSTEP", "26"))
 
-COMBOS = [  # r02: FC load modes in the step
-    {"2FCRelu": {"tile_sizes": [4, 8, 3]}},
-    {"MLP3": {"tile_sizes": [2, 1, 2]}},
+COMBOS = [  # r02: fewer, fuller FC CTAs so the step's kernels can share SMs
+    {"2FCRelu": {"tile_sizes": [8, 8, 1], "thread_shape": [128, 1, 1]}},
+    {"2FCRelu": {"tile_sizes": [8, 8, 1], "thread_shape": [128, 1, 1]}, "MLP3": {"tile_sizes": [8, 4, 1], "thread_shape": [64, 1, 1]}},
+    {"2FCRelu": {"tile_sizes": [8, 8, 1], "thread_shape": [128, 1, 1]}, "MLP3": {"tile_sizes": [8, 2, 1], "thread_shape": [64, 1, 1]}},
+    {"2FCRelu": {"tile_sizes": [16, 8, 1], "thread_shape": [256, 1, 1]}},
+    {"MLP3": {"tile_sizes": [8, 4, 1], "thread_shape": [64, 1, 1]}},
+    {"tbmm": {"tile_sizes": [13, 1, 2]}},
 ]
 
 VARIANTS = {
-    "2FCRelu": [None, {"tile_sizes": [8, 8, 1], "block_shape": [128, 1, 1]}, {"tile_sizes": [8, 16, 1]},
-                {"tile_sizes": [16, 16, 1], "block_shape": [128, 1, 1]}, {"tile_sizes": [8, 4, 1], "block_shape": [256, 1, 1]}],
-    "tbmm": [None, {"tile_sizes": [32, 32, 64], "thread_shape": [16, 16, 1]}, {"tile_sizes": [7, 4, 2]},
-             {"tile_sizes": [4, 4, 2]}],
-    "MLP3": [None, {"tile_sizes": [4, 4, 1]}, {"tile_sizes": [2, 2, 1]}],
+    "2FCRelu": [None, {"tile_sizes": [8, 8, 1], "thread_shape": [128, 1, 1]}, {"tile_sizes": [16, 8, 1], "thread_shape": [256, 1, 1]},
+                {"tile_sizes": [8, 4, 1], "thread_shape": [256, 1, 1]}],
+    "tbmm": [None],
+    "MLP3": [None, {"tile_sizes": [8, 4, 1], "thread_shape": [64, 1, 1]}, {"tile_sizes": [8, 2, 1], "thread_shape": [64, 1, 1]}],
 }
 
 
