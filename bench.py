@@ -220,10 +220,10 @@ class OpInstance:
 
 
 DOM_NOTES = {
-    "2FCRelu": "Bound by its sequential FFMA chain (1128 dependent steps per output), see chain_floor_us.",
-    "tbmm": "500 batches of 26x26 outputs, 72-step chains: one wave of CTAs whose time is load latency + "
-            "chain + store; its plan (two 64-deep k stages) is picked for overlap with the FC chains of the "
-            "forked step, not for its time alone (DESIGN.md section 8).",
+    "2FCRelu": "Bound by its sequential FFMA chain (1128 + 128 dependent steps per output) after a ~2.4 us "
+               "load prologue, not by bytes: see chain_floor_us / chain_floor_frac (DESIGN.md section 8).",
+    "tbmm": "500 batches of 26x26 outputs, 72-step chains: one wave of CTAs (slab kernel) whose loads and "
+            "chains overlap only chunk by chunk; cold-read floor for its 8.84 MB ~3.1 us (DESIGN.md section 5).",
     "MLP3": "Three short dependent layers (128, 64, 32 steps): latency bound, see chain_floor_us.",
 }
 
@@ -733,8 +733,17 @@ def main():
                 "algorithmic_bytes": int(dom.bytes), "launch_us": round(dom_t * 1e6, 3),
                 "share_of_step": round(dom_t / step_dev, 3), "peak_source": peak_src,
                 "note": "FFMA-exact fp32 kernels: no tensor-core roofline applies; HBM roofline over the "
-                        "kernel's algorithmic bytes (inputs once, outputs once). " + DOM_NOTES.get(dom.name, ""),
-                "chain_floor_us": round(chain_floor_us(dom), 3)}
+                        "kernel's algorithmic bytes (inputs once, outputs once). chain_floor_frac = the "
+                        "latency floor of its longest dependent FFMA chain / its time. " + DOM_NOTES.get(dom.name, ""),
+                "chain_floor_us": round(chain_floor_us(dom), 3),
+                "chain_floor_frac": round(chain_floor_us(dom) / (dom_t * 1e6), 4),
+                # every kernel of the step on both bounds (the dominant one above)
+                "by_kernel": {o.name: {"kernel": o.kernel, "launch_us": round(t * 1e6, 3),
+                                       "hbm_achieved_gbs": round(o.bytes / t / 1e9, 1),
+                                       "hbm_frac": round(o.bytes / t / 1e9 / hbm_peak, 4),
+                                       "chain_floor_us": round(chain_floor_us(o), 3),
+                                       "chain_floor_frac": round(chain_floor_us(o) / (t * 1e6), 4)}
+                              for o, t in per_op}}
     roofline_ops = {
         o.name: {"us": round(t * 1e6, 3), "gflops": round(o.flops / t / 1e9, 1),
                  "hbm_gbs": round(o.bytes / t / 1e9, 1), "hbm_frac": round(o.bytes / t / 1e9 / hbm_peak, 4),
