@@ -57,6 +57,7 @@ struct ShiftParams {
   int N, G, C, H, W, F, KH, KW, Mb;
   int Ho, Wo, tilesPerImg, items;  // items = G * N * tilesPerImg, split evenly over the grid
   int HP;  // halo pixels per tile (multiple of 8)
+  int tma;  // 1: halo tiles land by one TMA tensor copy into a staging buffer, then an on-chip transpose
 };
 
 template <int F, bool X3>
@@ -73,14 +74,16 @@ struct ShiftCfg {
                                                            : 512;
   __host__ __device__ static int stageFloats(int C, int HP) { return C * HP * (X3 ? 2 : 1); }
   __host__ __device__ static int bBytes(int KH, int KW, int C) { return KH * KW * (C / 8) * 32 * kN; }
+  __host__ __device__ static int stagingBytes(const ShiftParams& p) { return p.tma ? 2 * p.C * p.HP * 4 : 0; }
   __host__ __device__ static int smem(const ShiftParams& p) {
-    return 1024 + kStagesSh * stageFloats(p.C, p.HP) * 4 + 2 * bBytes(p.KH, p.KW, p.C) + 1024 +
+    return 1024 + kStagesSh * stageFloats(p.C, p.HP) * 4 + 2 * bBytes(p.KH, p.KW, p.C) + stagingBytes(p) + 1024 +
            8 * p.KH * p.KW * (p.C / 8) + 4 * p.Mb;
   }
 };
 
 template <int F, bool X3>
-__global__ void __launch_bounds__(kThreadsSh, 1) tc_gconv_shift_kernel(const ShiftParams p) {
+__global__ void __launch_bounds__(kThreadsSh, 1)
+    tc_gconv_shift_kernel(const ShiftParams p, const __grid_constant__ CUtensorMap tmI) {
   using Cfg = ShiftCfg<F, X3>;
   constexpr int S = kStagesSh;
   extern __shared__ uint8_t smraw[];
@@ -92,11 +95,13 @@ __global__ void __launch_bounds__(kThreadsSh, 1) tc_gconv_shift_kernel(const Shi
   uint8_t* bBank = sm + S * stF * 4;  // [2 banks][hi (+ lo)] of the CTA's first and last group
   constexpr int NB = Cfg::kN;
   const int bStride = Cfg::bBytes(p.KH, p.KW, C);
-  uint64_t* full = reinterpret_cast<uint64_t*>(bBank + 2 * bStride);
+  float* staging = reinterpret_cast<float*>(bBank + 2 * bStride);  // p.tma: [2][C][HP] as the TMA lands it
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(staging) + Cfg::stagingBytes(p));
   uint64_t* empty = full + S;
   uint64_t* tFull = empty + S;            // [kTmemBufs]
   uint64_t* tEmpty = tFull + kTmemBufs;   // [kTmemBufs]
-  uint32_t* tmemSlot = reinterpret_cast<uint32_t*>(tEmpty + kTmemBufs);
+  uint64_t* stFull = tEmpty + kTmemBufs;  // [2] staging buffer landed
+  uint32_t* tmemSlot = reinterpret_cast<uint32_t*>(stFull + 2);
   uint32_t* aOff16 = tmemSlot + 4;              // [K steps] A descriptor start offset (16-byte units)
   float* sBias = reinterpret_cast<float*>(aOff16 + taps * kcb);
 
@@ -147,6 +152,8 @@ __global__ void __launch_bounds__(kThreadsSh, 1) tc_gconv_shift_kernel(const Shi
       mbarInit(&tFull[b], 1);
       mbarInit(&tEmpty[b], 4);  // one arrive per epilogue warp
     }
+    mbarInit(&stFull[0], 1);
+    mbarInit(&stFull[1], 1);
     fenceBarrierInit();
   }
   if (warp == 2) tmemAlloc<Cfg::kTmemCols>(tmemSlot);
@@ -155,7 +162,70 @@ __global__ void __launch_bounds__(kThreadsSh, 1) tc_gconv_shift_kernel(const Shi
   tcFenceAfter();
   const uint32_t tmem = *tmemSlot;
 
-  if (warp >= 8) {
+  if (warp >= 8 && p.tma) {
+    // ---- builders, TMA path: tile lt's halo (C channel rows of HP
+    // consecutive input pixels, contiguous in every channel plane) lands in
+    // staging[lt & 1] by ONE tensor copy {HP px, C ch, 1} (zero-filled past
+    // the plane), issued two tiles ahead; the builders then transpose it on
+    // chip into the channel-block-major UMMA layout [C/4][HP][4] (+ the hi/lo
+    // split for 3xTF32). Round 1's builders issued 4-byte cp.async per
+    // element: ~4000 per tile, the kernel's bound (222 of 281 us with every
+    // MMA skipped).
+    const int b = threadIdx.x - 256;
+    const int n4 = HP / 4, items = n4 * (C / 4);  // (4-pixel group, 4-channel block) per item
+    const int nt = t1 - t0;
+    auto issue = [&](int lt) {
+      const int t = t0 + lt, g = t / tilesG, tt = t - g * tilesG, n = tt / p.tilesPerImg;
+      const int p0 = (tt - n * p.tilesPerImg) * 128;
+      uint64_t* bar = &stFull[lt & 1];
+      mbarExpectTx(bar, (uint32_t)(C * HP * 4));
+      tmaLoad3d(staging + (lt & 1) * C * HP, &tmI, p0, 0, n * p.G + g, bar);
+    };
+    if (b == 0) {
+      tmaPrefetch(&tmI);
+      for (int lt = 0; lt < min(2, nt); ++lt) issue(lt);
+    }
+    for (int lt = 0; lt < nt; ++lt) {
+      const int s = lt % S;
+      if (lt >= S) mbarWait(&empty[s], ((lt / S) - 1) & 1, 1);  // MMAs of tile lt - S done
+      mbarWait(&stFull[lt & 1], (lt >> 1) & 1, 5);
+      const float* src = staging + (lt & 1) * C * HP;
+      float* hiP = stages + s * stF;
+      for (int it = b; it < items; it += kBuildersSh) {
+        const int cb = it / n4, pg = it - cb * n4;  // consecutive lanes: consecutive pixel groups
+        float4 r[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) r[c] = *reinterpret_cast<const float4*>(src + (cb * 4 + c) * HP + pg * 4);
+        const float rv[4][4] = {{r[0].x, r[0].y, r[0].z, r[0].w},
+                                {r[1].x, r[1].y, r[1].z, r[1].w},
+                                {r[2].x, r[2].y, r[2].z, r[2].w},
+                                {r[3].x, r[3].y, r[3].z, r[3].w}};
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          const int j = (jj + pg) & 3;  // rotate the pixel order: fewer bank conflicts on the stores
+          float4 v = make_float4(rv[0][j], rv[1][j], rv[2][j], rv[3][j]);  // 4 channels of pixel pg*4+j
+          float4* dst = reinterpret_cast<float4*>(hiP + ((cb * HP) + pg * 4 + j) * 4);
+          if constexpr (X3) {
+            float4 h, l;
+            h.x = toTf32(v.x); h.y = toTf32(v.y); h.z = toTf32(v.z); h.w = toTf32(v.w);
+            l.x = toTf32(v.x - h.x); l.y = toTf32(v.y - h.y); l.z = toTf32(v.z - h.z); l.w = toTf32(v.w - h.w);
+            dst[0] = h;
+            dst[planeF / 4] = l;
+          } else {
+            *dst = v;
+          }
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kBuildersSh) : "memory");  // staging[lt & 1] fully read
+      if (b == 0 && lt + 2 < nt) {
+        fenceProxyAsyncSmem();
+        issue(lt + 2);
+      }
+      fenceProxyAsyncSmem();  // this lane's stage writes -> visible to the tensor core
+      __syncwarp();
+      if (lane == 0) mbarArrive(&full[s]);
+    }
+  } else if (warp >= 8) {
     // ---- builders
     const int b = threadIdx.x - 256, el = b & 3, qq = b >> 2;  // 64 pixels x 4 channels per pass
     auto load = [&](int t, int s) {
@@ -283,9 +353,28 @@ __global__ void __launch_bounds__(kThreadsSh, 1) tc_gconv_shift_kernel(const Shi
 }
 
 template <int F, bool X3>
-cudaError_t launchShift(const ShiftParams& p, cudaStream_t s) {
+cudaError_t launchShift(ShiftParams p, cudaStream_t s) {
   using Cfg = ShiftCfg<F, X3>;
   auto kern = tc_gconv_shift_kernel<F, X3>;
+  // the TMA halo path: planes whose rows of HP floats can be one tensor box
+  // (16-byte plane pitch, HP <= 256); else the per-element cp.async builders
+  CUtensorMap tmI{};
+  p.tma = 0;
+  const int64_t HW = (int64_t)p.H * p.W;
+  EncodeFn enc = encodeFn();
+  if (enc && HW % 4 == 0 && p.HP <= 256 && (reinterpret_cast<uintptr_t>(p.I) & 15) == 0 &&
+      Cfg::smem(ShiftParams{p.I, p.O, p.W1, p.bias, p.N, p.G, p.C, p.H, p.W, p.F, p.KH, p.KW, p.Mb, p.Ho, p.Wo,
+                            p.tilesPerImg, p.items, p.HP, 1}) <= 227 * 1024) {
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(HW), static_cast<cuuint64_t>(p.C),
+                          static_cast<cuuint64_t>(p.N) * p.G};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(HW) * 4, static_cast<cuuint64_t>(HW) * p.C * 4};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(p.HP), static_cast<cuuint32_t>(p.C), 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&tmI, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(p.I), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      p.tma = 1;
+  }
   const int smemBytes = Cfg::smem(p);
   if (smemBytes > 227 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kern), smemBytes);
@@ -296,7 +385,7 @@ cudaError_t launchShift(const ShiftParams& p, cudaStream_t s) {
   // one CTA per SM (one wave); a CTA's items must not span more than 2 groups
   const int tilesG = p.N * p.tilesPerImg;
   const int grid = std::max(std::min(sms, p.items), (p.items + tilesG - 1) / tilesG);
-  kern<<<grid, kThreadsSh, smemBytes, s>>>(p);
+  kern<<<grid, kThreadsSh, smemBytes, s>>>(p, tmI);
   return cudaGetLastError();
 }
 
