@@ -60,6 +60,16 @@ struct ShiftParams {
   int tma;  // 1: halo tiles land by one TMA tensor copy into a staging buffer, then an on-chip transpose
 };
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
 template <int F, bool X3>
 struct ShiftCfg {
   // 3xTF32 stacks B as [b_hi | b_lo] (N = 2F): a_hi*[b_hi|b_lo] and
@@ -189,30 +199,31 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
       const int s = lt % S;
       if (lt >= S) mbarWait(&empty[s], ((lt / S) - 1) & 1, 1);  // MMAs of tile lt - S done
       mbarWait(&stFull[lt & 1], (lt >> 1) & 1, 5);
-      const float* src = staging + (lt & 1) * C * HP;
-      float* hiP = stages + s * stF;
+      const uint32_t src = smem(staging + (lt & 1) * C * HP), hiP = smem(stages + s * stF);
       for (int it = b; it < items; it += kBuildersSh) {
         const int cb = it / n4, pg = it - cb * n4;  // consecutive lanes: consecutive pixel groups
         float4 r[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) r[c] = *reinterpret_cast<const float4*>(src + (cb * 4 + c) * HP + pg * 4);
-        const float rv[4][4] = {{r[0].x, r[0].y, r[0].z, r[0].w},
-                                {r[1].x, r[1].y, r[1].z, r[1].w},
-                                {r[2].x, r[2].y, r[2].z, r[2].w},
-                                {r[3].x, r[3].y, r[3].z, r[3].w}};
+        for (int c = 0; c < 4; ++c) r[c] = lds128(src + (uint32_t)(((cb * 4 + c) * HP + pg * 4) * 4));
+        const int rot = pg & 3;  // rotate the pixel order across lanes: fewer bank conflicts on the stores
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-          const int j = (jj + pg) & 3;  // rotate the pixel order: fewer bank conflicts on the stores
-          float4 v = make_float4(rv[0][j], rv[1][j], rv[2][j], rv[3][j]);  // 4 channels of pixel pg*4+j
-          float4* dst = reinterpret_cast<float4*>(hiP + ((cb * HP) + pg * 4 + j) * 4);
+          const int j = (jj + rot) & 3;
+          // the 4 channels of pixel pg*4 + j (selects, not a dynamically indexed array)
+          float4 v;
+          v.x = j == 0 ? r[0].x : j == 1 ? r[0].y : j == 2 ? r[0].z : r[0].w;
+          v.y = j == 0 ? r[1].x : j == 1 ? r[1].y : j == 2 ? r[1].z : r[1].w;
+          v.z = j == 0 ? r[2].x : j == 1 ? r[2].y : j == 2 ? r[2].z : r[2].w;
+          v.w = j == 0 ? r[3].x : j == 1 ? r[3].y : j == 2 ? r[3].z : r[3].w;
+          const uint32_t dst = hiP + (uint32_t)(((cb * HP) + pg * 4 + j) * 16);
           if constexpr (X3) {
             float4 h, l;
             h.x = toTf32(v.x); h.y = toTf32(v.y); h.z = toTf32(v.z); h.w = toTf32(v.w);
             l.x = toTf32(v.x - h.x); l.y = toTf32(v.y - h.y); l.z = toTf32(v.z - h.z); l.w = toTf32(v.w - h.w);
-            dst[0] = h;
-            dst[planeF / 4] = l;
+            sts128(dst, h);
+            sts128(dst + (uint32_t)planeF * 4, l);
           } else {
-            *dst = v;
+            sts128(dst, v);
           }
         }
       }
@@ -283,6 +294,14 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
     constexpr uint32_t idesc = idescTf32(128, NB);  // both operands K-major
     const uint32_t lboA = HP * 16, lboB = 16 * NB;
     const int nks = taps * kcb;
+    constexpr int kFastKs = 18;  // KH = KW = 3, C = 16
+    uint32_t fastOff[kFastKs];
+#pragma unroll
+    for (int ks = 0; ks < kFastKs; ++ks) {
+      const int tap = ks / 2, c8 = ks % 2, kh = tap / 3, kw = tap % 3;
+      fastOff[ks] = (uint32_t)((c8 * 2 * HP * 16 + (kh * p.W + kw) * 16) >> 4);
+    }
+    if (!(p.KH == 3 && p.KW == 3 && C == 16)) fastOff[0] = 0;  // (unused: nks != 18 or a different tap set)
     for (int lt = 0; lt < t1 - t0; ++lt) {
       const int s = lt % S, buf = lt % kTmemBufs, bank = (t0 + lt) / tilesG - gFirst;
       if (lt >= kTmemBufs) mbarWait(&tEmpty[buf], ((lt / kTmemBufs) - 1) & 1, 2);
@@ -292,12 +311,26 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
       const uint64_t ah0 = descKInterleave(aHi, lboA, 128), al0 = descKInterleave(aHi + planeF * 4, lboA, 128);
       const uint64_t b0 = descKInterleave(smem(bBank + bank * bStride), lboB, 128);
       const uint32_t d = tmem + buf * NB;
+      if (nks == kFastKs && p.KH == 3 && p.KW == 3 && C == 16) {
+        // the paper's 3x3, 16-channel groups: 18 K steps, offsets in registers
+        // (a shared-memory table read + 64-bit adds per MMA held the issue
+        // rate at 76-117 cycles per MMA, profiles/experiments/r01_gconv_shift_tuning.txt)
+#pragma unroll
+        for (int ks = 0; ks < kFastKs; ++ks) {
+          const uint64_t ao = fastOff[ks], bd = b0 + static_cast<uint64_t>(ks * 2 * NB);
+          if (electSync()) {
+            mmaTf32(d, ah0 + ao, bd, idesc, ks > 0);
+            if constexpr (X3) mmaTf32(d, al0 + ao, bd, idesc, 1);
+          }
+        }
+      } else {
 #pragma unroll 2
-      for (int ks = 0; ks < nks; ++ks) {
-        const uint64_t ao = aOff16[ks], bd = b0 + static_cast<uint64_t>(ks * 2 * NB);  // 32*NB bytes per step
-        if (electSync()) {
-          mmaTf32(d, ah0 + ao, bd, idesc, ks > 0);
-          if constexpr (X3) mmaTf32(d, al0 + ao, bd, idesc, 1);
+        for (int ks = 0; ks < nks; ++ks) {
+          const uint64_t ao = aOff16[ks], bd = b0 + static_cast<uint64_t>(ks * 2 * NB);  // 32*NB bytes per step
+          if (electSync()) {
+            mmaTf32(d, ah0 + ao, bd, idesc, ks > 0);
+            if constexpr (X3) mmaTf32(d, al0 + ao, bd, idesc, 1);
+          }
         }
       }
       if (electSync()) {
