@@ -40,6 +40,12 @@ constexpr int kThreadsSh = 512;
 constexpr int kBuildersSh = 256;
 constexpr int kStagesSh = 4;  // halo tiles in flight (ring)
 constexpr int kAheadSh = 2;   // tiles loaded ahead of the one being finalised
+// TMA path: a 3-deep ring of transposed tiles and 4 raw staging buffers, so
+// four tiles' input (64 KB) is in flight per SM: with two (32 KB) the SM
+// pulled ~14 GB/s (Little's law on a ~2 us load latency) and that set the
+// kernel's pace
+constexpr int kRingTma = 3;
+constexpr int kStagingBufs = 4;
 // One accumulator per tile: a tcgen05.mma from shared memory costs ~40 cycles
 // at N = 16 whatever the accumulator dependence (it is bound by reading the
 // 4 KB A operand, profiles/umma_rate.cu), so partial accumulators would only
@@ -84,9 +90,10 @@ struct ShiftCfg {
                                                            : 512;
   __host__ __device__ static int stageFloats(int C, int HP) { return C * HP * (X3 ? 2 : 1); }
   __host__ __device__ static int bBytes(int KH, int KW, int C) { return KH * KW * (C / 8) * 32 * kN; }
-  __host__ __device__ static int stagingBytes(const ShiftParams& p) { return p.tma ? 2 * p.C * p.HP * 4 : 0; }
+  __host__ __device__ static int stagingBytes(const ShiftParams& p) { return p.tma ? kStagingBufs * p.C * p.HP * 4 : 0; }
+  __host__ __device__ static int ring(const ShiftParams& p) { return p.tma ? kRingTma : kStagesSh; }
   __host__ __device__ static int smem(const ShiftParams& p) {
-    return 1024 + kStagesSh * stageFloats(p.C, p.HP) * 4 + 2 * bBytes(p.KH, p.KW, p.C) + stagingBytes(p) + 1024 +
+    return 1024 + ring(p) * stageFloats(p.C, p.HP) * 4 + 2 * bBytes(p.KH, p.KW, p.C) + stagingBytes(p) + 1024 +
            8 * p.KH * p.KW * (p.C / 8) + 4 * p.Mb;
   }
 };
@@ -95,7 +102,7 @@ template <int F, bool X3>
 __global__ void __launch_bounds__(kThreadsSh, 1)
     tc_gconv_shift_kernel(const ShiftParams p, const __grid_constant__ CUtensorMap tmI) {
   using Cfg = ShiftCfg<F, X3>;
-  constexpr int S = kStagesSh;
+  const int S = Cfg::ring(p);
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   const int C = p.C, HP = p.HP, taps = p.KH * p.KW, kcb = C / 8;
@@ -107,11 +114,11 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
   const int bStride = Cfg::bBytes(p.KH, p.KW, C);
   float* staging = reinterpret_cast<float*>(bBank + 2 * bStride);  // p.tma: [2][C][HP] as the TMA lands it
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(staging) + Cfg::stagingBytes(p));
-  uint64_t* empty = full + S;
-  uint64_t* tFull = empty + S;            // [kTmemBufs]
+  uint64_t* empty = full + kStagesSh;
+  uint64_t* tFull = empty + kStagesSh;    // [kTmemBufs]
   uint64_t* tEmpty = tFull + kTmemBufs;   // [kTmemBufs]
-  uint64_t* stFull = tEmpty + kTmemBufs;  // [2] staging buffer landed
-  uint32_t* tmemSlot = reinterpret_cast<uint32_t*>(stFull + 2);
+  uint64_t* stFull = tEmpty + kTmemBufs;  // [kStagingBufs] staging buffer landed
+  uint32_t* tmemSlot = reinterpret_cast<uint32_t*>(stFull + kStagingBufs);
   uint32_t* aOff16 = tmemSlot + 4;              // [K steps] A descriptor start offset (16-byte units)
   float* sBias = reinterpret_cast<float*>(aOff16 + taps * kcb);
 
@@ -162,8 +169,7 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
       mbarInit(&tFull[b], 1);
       mbarInit(&tEmpty[b], 4);  // one arrive per epilogue warp
     }
-    mbarInit(&stFull[0], 1);
-    mbarInit(&stFull[1], 1);
+    for (int i = 0; i < kStagingBufs; ++i) mbarInit(&stFull[i], 1);
     fenceBarrierInit();
   }
   if (warp == 2) tmemAlloc<Cfg::kTmemCols>(tmemSlot);
@@ -184,22 +190,23 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
     const int b = threadIdx.x - 256;
     const int n4 = HP / 4, items = n4 * (C / 4);  // (4-pixel group, 4-channel block) per item
     const int nt = t1 - t0;
+    constexpr int NS = kStagingBufs;
     auto issue = [&](int lt) {
       const int t = t0 + lt, g = t / tilesG, tt = t - g * tilesG, n = tt / p.tilesPerImg;
       const int p0 = (tt - n * p.tilesPerImg) * 128;
-      uint64_t* bar = &stFull[lt & 1];
+      uint64_t* bar = &stFull[lt % NS];
       mbarExpectTx(bar, (uint32_t)(C * HP * 4));
-      tmaLoad3d(staging + (lt & 1) * C * HP, &tmI, p0, 0, n * p.G + g, bar);
+      tmaLoad3d(staging + (lt % NS) * C * HP, &tmI, p0, 0, n * p.G + g, bar);
     };
     if (b == 0) {
       tmaPrefetch(&tmI);
-      for (int lt = 0; lt < min(2, nt); ++lt) issue(lt);
+      for (int lt = 0; lt < min(NS, nt); ++lt) issue(lt);
     }
     for (int lt = 0; lt < nt; ++lt) {
       const int s = lt % S;
       if (lt >= S) mbarWait(&empty[s], ((lt / S) - 1) & 1, 1);  // MMAs of tile lt - S done
-      mbarWait(&stFull[lt & 1], (lt >> 1) & 1, 5);
-      const uint32_t src = smem(staging + (lt & 1) * C * HP), hiP = smem(stages + s * stF);
+      mbarWait(&stFull[lt % NS], (lt / NS) & 1, 5);
+      const uint32_t src = smem(staging + (lt % NS) * C * HP), hiP = smem(stages + s * stF);
       for (int it = b; it < items; it += kBuildersSh) {
         const int cb = it / n4, pg = it - cb * n4;  // consecutive lanes: consecutive pixel groups
         float4 r[4];
@@ -227,10 +234,10 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
           }
         }
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(kBuildersSh) : "memory");  // staging[lt & 1] fully read
-      if (b == 0 && lt + 2 < nt) {
+      asm volatile("bar.sync 1, %0;" ::"n"(kBuildersSh) : "memory");  // staging[lt % NS] fully read
+      if (b == 0 && lt + NS < nt) {
         fenceProxyAsyncSmem();
-        issue(lt + 2);
+        issue(lt + NS);
       }
       fenceProxyAsyncSmem();  // this lane's stage writes -> visible to the tensor core
       __syncwarp();
