@@ -25,6 +25,7 @@
 // TMEM so tile t's epilogue overlaps tile t+1's MMAs. Not FFMA-exact:
 // selected by tensor-core math.
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.cuh"
 #include "sm100.cuh"
@@ -64,6 +65,7 @@ struct ShiftParams {
   int Ho, Wo, tilesPerImg, items;  // items = G * N * tilesPerImg, split evenly over the grid
   int HP;  // halo pixels per tile (multiple of 8)
   int tma;  // 1: halo tiles land by one TMA tensor copy into a staging buffer, then an on-chip transpose
+  int skip;  // diagnostics only (TCB_GCONV_SKIP env, ablations): 1 MMAs, 2 transposes, 4 output stores
 };
 
 __device__ __forceinline__ float4 lds128(uint32_t a) {
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
       if (lt >= S) mbarWait(&empty[s], ((lt / S) - 1) & 1, 1);  // MMAs of tile lt - S done
       mbarWait(&stFull[lt % NS], (lt / NS) & 1, 5);
       const uint32_t src = smem(staging + (lt % NS) * C * HP), hiP = smem(stages + s * stF);
-      for (int it = b; it < items; it += kBuildersSh) {
+      for (int it = (p.skip & 2) ? items : b; it < items; it += kBuildersSh) {
         const int cb = it / n4, pg = it - cb * n4;  // consecutive lanes: consecutive pixel groups
         float4 r[4];
 #pragma unroll
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
 #pragma unroll
         for (int ks = 0; ks < kFastKs; ++ks) {
           const uint64_t ao = fastOff[ks], bd = b0 + static_cast<uint64_t>(ks * 2 * NB);
-          if (electSync()) {
+          if (electSync() && !(p.skip & 1)) {
             mmaTf32(d, ah0 + ao, bd, idesc, ks > 0);
             if constexpr (X3) mmaTf32(d, al0 + ao, bd, idesc, 1);
           }
@@ -375,7 +377,7 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
       const int g = t / tilesG, tt = t - g * tilesG, n = tt / p.tilesPerImg;
       const int vp = (tt - n * p.tilesPerImg) * 128 + pix;
       const int h = vp / p.W, w = vp - h * p.W;
-      if (w < p.Wo && h < p.Ho) {
+      if (w < p.Wo && h < p.Ho && !(p.skip & 4)) {
         float* o = p.O + (((int64_t)n * p.G + g) * F) * p.Ho * p.Wo + (int64_t)h * p.Wo + w;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
@@ -404,7 +406,7 @@ cudaError_t launchShift(ShiftParams p, cudaStream_t s) {
   EncodeFn enc = encodeFn();
   if (enc && HW % 4 == 0 && p.HP <= 256 && (reinterpret_cast<uintptr_t>(p.I) & 15) == 0 &&
       Cfg::smem(ShiftParams{p.I, p.O, p.W1, p.bias, p.N, p.G, p.C, p.H, p.W, p.F, p.KH, p.KW, p.Mb, p.Ho, p.Wo,
-                            p.tilesPerImg, p.items, p.HP, 1}) <= 227 * 1024) {
+                            p.tilesPerImg, p.items, p.HP, 1, 0}) <= 227 * 1024) {
     cuuint64_t dims[3] = {static_cast<cuuint64_t>(HW), static_cast<cuuint64_t>(p.C),
                           static_cast<cuuint64_t>(p.N) * p.G};
     cuuint64_t strides[2] = {static_cast<cuuint64_t>(HW) * 4, static_cast<cuuint64_t>(HW) * p.C * 4};
@@ -468,6 +470,7 @@ cudaError_t launchTcGconvShift(const GconvArgs& a, int math, cudaStream_t s) {
   p.tilesPerImg = (p.Ho * p.W + 127) / 128;
   p.HP = ((128 + (a.KH - 1) * a.W + (a.KW - 1)) + 7) / 8 * 8;
   p.items = a.G * a.N * p.tilesPerImg;
+  if (const char* sk = std::getenv("TCB_GCONV_SKIP")) p.skip = std::atoi(sk);  // diagnostics only
   const bool x3 = math == kMath3xTf32;
   switch (a.F) {
     case 16: return x3 ? launchShift<16, true>(p, s) : launchShift<16, false>(p, s);
