@@ -46,7 +46,7 @@ constexpr int kAheadSh = 2;   // tiles loaded ahead of the one being finalised
 // pulled ~14 GB/s (Little's law on a ~2 us load latency) and that set the
 // kernel's pace
 constexpr int kRingTma = 3;
-constexpr int kStagingBufs = 8;
+constexpr int kStagingBufs = 4;
 // One accumulator per tile: a tcgen05.mma from shared memory costs ~40 cycles
 // at N = 16 whatever the accumulator dependence (it is bound by reading the
 // 4 KB A operand, profiles/umma_rate.cu), so partial accumulators would only
