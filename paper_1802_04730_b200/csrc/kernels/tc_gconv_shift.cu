@@ -41,12 +41,11 @@ constexpr int kThreadsSh = 512;
 constexpr int kBuildersSh = 256;
 constexpr int kStagesSh = 4;  // halo tiles in flight (ring)
 constexpr int kAheadSh = 2;   // tiles loaded ahead of the one being finalised
-// TMA path: a 3-deep ring of transposed tiles and 4 raw staging buffers, so
-// four tiles' input (64 KB) is in flight per SM: with two (32 KB) the SM
-// pulled ~14 GB/s (Little's law on a ~2 us load latency) and that set the
-// kernel's pace
-constexpr int kRingTma = 3;
-constexpr int kStagingBufs = 4;
+// TMA path: a 4-deep ring of transposed tiles and 2 raw staging buffers
+// (4 or 8 staging buffers with a 3-deep ring measured 211 us vs 203,
+// profiles/r02_tma_sweep.txt)
+constexpr int kRingTma = 4;
+constexpr int kStagingBufs = 2;
 // One accumulator per tile: a tcgen05.mma from shared memory costs ~40 cycles
 // at N = 16 whatever the accumulator dependence (it is bound by reading the
 // 4 KB A operand, profiles/umma_rate.cu), so partial accumulators would only
