@@ -644,6 +644,16 @@ int tcb_tune(tcb_engine* e, const char* name, const tcb_tensor* in, int nin, con
       if (j.has("session_log")) o.sessionLog = j.at("session_log").asStr();
       if (j.has("use_baselines")) o.useBaselines = j.at("use_baselines").asBool();
       if (j.has("math")) o.math = ops::mathFromName(j.at("math").asStr());
+      if (j.has("devices")) {
+        const Json& d = j.at("devices");
+        if (d.type() == Json::T::Str && d.asStr() == "all") {
+          int n = 0;
+          cudaOk(cudaGetDeviceCount(&n), "device count");
+          for (int i = 0; i < n; ++i) o.devices.push_back(i);
+        } else {
+          for (const auto& x : d.items()) o.devices.push_back(static_cast<int>(x.asInt()));
+        }
+      }
     }
     const std::string suffix = o.math ? std::string(" math=") + ops::mathName(o.math) : std::string();
     cache::Key key = cache::makeKey(s.v, e->paramShapes(s), MappingOptions{}, suffix);

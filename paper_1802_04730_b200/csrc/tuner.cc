@@ -8,8 +8,11 @@
 #include <cstring>
 #include <ctime>
 #include <fstream>
+#include <atomic>
+#include <memory>
 #include <optional>
 #include <random>
+#include <thread>
 
 #include "session.h"
 
@@ -300,25 +303,68 @@ TuneResult tune(const sem::Specialized& s, const ops::Problem& p, const cache::K
   };
   std::vector<Candidate> pop = seedPop(starting);
 
-  DeviceSession ds(s, o.seed ^ fnv1a64("session-inputs"));
-  // reference output: the family default mapping (always decodable)
-  std::optional<std::vector<std::vector<char>>> refOut;
-  {
+  // one scoring worker per listed device: its own session (the same seeded
+  // inputs) and its own reference output from the family default mapping
+  std::vector<int> devs = o.devices;
+  int cur = 0;
+  cudaOk(cudaGetDevice(&cur), "device");
+  if (devs.empty()) devs.push_back(cur);
+  struct Worker {
+    int dev;
+    std::unique_ptr<DeviceSession> ds;
+    std::optional<std::vector<std::vector<char>>> refOut;
+  };
+  std::vector<Worker> workers(devs.size());
+  for (size_t w = 0; w < devs.size(); ++w) {
+    workers[w].dev = devs[w];
+    cudaOk(cudaSetDevice(devs[w]), "device");
+    workers[w].ds = std::make_unique<DeviceSession>(s, o.seed ^ fnv1a64("session-inputs"));
     Candidate ref;
     ref.genome = ops::defaultOptions(p, o.math);
-    score(ref, p, ds, 1, refOut, o.math);
+    score(ref, p, *workers[w].ds, 1, workers[w].refOut, o.math);
     if (!ref.ok) fail(ErrorKind::NoViableCandidate, "the default mapping failed: " + ref.failure);
   }
+  cudaOk(cudaSetDevice(cur), "device");
+  TuneResult res;
+  res.perWorker.assign(workers.size(), 0);
+  // scores every candidate of a generation: workers take the next unscored
+  // index; each writes only its own candidates (the reference's per-slot
+  // writes, genetic.h:99-104); cache updates follow in candidate order
+  auto scoreAll = [&](std::vector<Candidate>& cands) {
+    if (workers.size() == 1) {
+      for (auto& cd : cands) score(cd, p, *workers[0].ds, o.timingIters, workers[0].refOut, o.math, o.coldL2);
+      res.perWorker[0] += cands.size();
+      return;
+    }
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> th;
+    std::vector<std::string> errs(workers.size());
+    for (size_t w = 0; w < workers.size(); ++w)
+      th.emplace_back([&, w] {
+        try {
+          cudaOk(cudaSetDevice(workers[w].dev), "device");
+          for (size_t i; (i = next.fetch_add(1)) < cands.size();) {
+            score(cands[i], p, *workers[w].ds, o.timingIters, workers[w].refOut, o.math, o.coldL2);
+            ++res.perWorker[w];
+          }
+        } catch (const std::exception& e) {
+          errs[w] = e.what();
+        }
+      });
+    for (auto& t : th) t.join();
+    cudaSetDevice(cur);
+    for (const auto& e : errs)
+      if (!e.empty()) fail(ErrorKind::Cuda, "tuner worker: " + e);
+  };
 
   const std::string session = "tune-" + hex16(fnv1a64(key.canonicalTc + std::to_string(o.seed)));
   std::ofstream log;
   if (!o.sessionLog.empty()) log.open(o.sessionLog, std::ios::app);
 
-  TuneResult res;
   std::optional<Candidate> best;
   for (size_t gen = 0;; ++gen) {
+    scoreAll(pop);
     for (auto& cd : pop) {
-      score(cd, p, ds, o.timingIters, refOut, o.math, o.coldL2);
       ++res.evaluated;
       if (!cd.ok) {
         ++res.failed;
@@ -338,8 +384,11 @@ TuneResult tune(const sem::Specialized& s, const ops::Problem& p, const cache::K
       }
     }
     if (log) {
+      std::string pw;
+      for (size_t w = 0; w < res.perWorker.size(); ++w) pw += (w ? "," : "") + std::to_string(res.perWorker[w]);
       log << "{\"generation\":" << gen << ",\"best_cost\":" << (best ? std::to_string(best->cost) : "null")
-          << ",\"genome\":" << (best ? best->genome.toJson() : "null") << "}\n";
+          << ",\"genome\":" << (best ? best->genome.toJson() : "null") << ",\"scored_per_device_worker\":[" << pw
+          << "]}\n";
     }
     if (gen == o.generations) break;
     double total = 0;

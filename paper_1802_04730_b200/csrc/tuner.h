@@ -39,12 +39,19 @@ struct TuneOptions {
   // ops::tcTolerance (different K splits sum in different orders), instead
   // of the FFMA modes' bit equality.
   int math = 0;
+  // Devices that score candidates in parallel, one host thread per entry
+  // (the reference scores candidates on a worker pool, genetic.cc:317-345;
+  // the paper tuned on 8 GPUs). Empty = the current
+  // device. A device may be listed twice (two workers sharing one GPU: the
+  // code path, not a timing setup).
+  std::vector<int> devices;
 };
 
 struct TuneResult {
   MappingOptions best;
   int64_t bestCost = 0;
   size_t evaluated = 0, failed = 0;
+  std::vector<size_t> perWorker;  // candidates scored by each device worker
 };
 
 TuneResult tune(const sem::Specialized& s, const ops::Problem& p, const cache::Key& key, const TuneOptions& o,

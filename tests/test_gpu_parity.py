@@ -479,6 +479,34 @@ def test_tuner_populates_cache_and_compile_replays(engine, oracle, golden, tmp_p
     tcb.cache_purge()
 
 
+@pytest.mark.parametrize("devices", [[0, 0], "all"])
+def test_tuner_parallel_device_workers(engine, oracle, golden, tmp_path, devices):
+    """Candidates scored in parallel by one host thread per listed device
+    (the reference's worker pool, genetic.cc:317-345). The test box has one
+    GPU, so [0, 0] runs two workers on it (the code path; their timings
+    interfere) and "all" one worker per visible device. Every candidate is
+    scored exactly once, the workers split them, and the winner is bit-exact."""
+    import paper_1802_04730_b200 as tcb
+    tcb.cache_purge()
+    log = tmp_path / "session.jsonl"
+    case, ins, seeded = case_inputs(oracle, golden, "tbmm_paper")
+    p = [to_dev(ins["X"]), to_dev(ins["Y"])]
+    z = torch.zeros((500, 26, 26), device="cuda")
+    best = engine.tune("tbmm", p, [z], population=10, generations=1, seed=4, timing_iters=2,
+                       session_log=str(log), devices=devices)
+    lines = [json.loads(x) for x in log.read_text().splitlines()]
+    per = lines[-1]["scored_per_device_worker"]
+    assert len(per) == (2 if devices == [0, 0] else torch.cuda.device_count())
+    assert sum(per) == 20  # 2 generations x 10 genomes, each scored once
+    if devices == [0, 0]:
+        assert min(per) > 0
+    h = engine.compile("tbmm", p, [z], best)
+    engine.run(h, p, [z])
+    torch.cuda.synchronize()
+    assert fnv_hex(oracle, z.cpu().numpy()) == case["outputs"]["Z"]["fnv"]
+    tcb.cache_purge()
+
+
 def test_paper_style_call(engine, oracle):
     """ee.tmm(A, B) allocates, compiles and runs (PAPER.md:2309-2326)."""
     rng = oracle.rng(5)
