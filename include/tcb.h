@@ -167,6 +167,12 @@ int tcb_shard_range(tcb_engine* e, uint64_t handle, int rank, int world, int64_t
 int tcb_run_shard(tcb_engine* e, uint64_t handle, const tcb_tensor* inputs, int n_inputs,
                   const tcb_tensor* outputs, int n_outputs, int rank, int world, void* stream, int flags);
 
+/* releases a compiled handle: its device staging buffers and error flag are
+ * freed after its last stream drains; the handle id is not reused and any
+ * later use of it fails with TCB_ERR_NAME. The caller must not release a
+ * handle another thread is running. */
+int tcb_release(tcb_engine* e, uint64_t handle);
+
 /* synchronises the handle's last stream and reports a device-side error
  * (IndexOutOfRange from a data-dependent subscript) raised since the last check */
 int tcb_check(tcb_engine* e, uint64_t handle);

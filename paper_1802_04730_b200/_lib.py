@@ -71,6 +71,7 @@ def _load():
         "tcb_run": (C.c_int, [C.c_void_p, C.c_uint64, T, C.c_int, T, C.c_int, C.c_void_p, C.c_int,
                               C.POINTER(C.c_int64)]),
         "tcb_check": (C.c_int, [C.c_void_p, C.c_uint64]),
+        "tcb_release": (C.c_int, [C.c_void_p, C.c_uint64]),
         "tcb_shard_range": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "tcb_run_shard": (C.c_int, [C.c_void_p, C.c_uint64, T, C.c_int, T, C.c_int, C.c_int, C.c_int,
@@ -129,7 +130,7 @@ EXPORTED = [
     "tcb_version", "tcb_last_error", "tcb_device_info", "tcb_measure_peaks", "tcb_engine_create", "tcb_engine_destroy",
     "tcb_define", "tcb_builtin_ops", "tcb_def_signature", "tcb_infer_outputs", "tcb_compile",
     "tcb_compile_ex",
-    "tcb_run", "tcb_shard_range", "tcb_run_shard", "tcb_check", "tcb_describe", "tcb_tune", "tcb_cache_load", "tcb_cache_save",
+    "tcb_run", "tcb_shard_range", "tcb_run_shard", "tcb_release", "tcb_check", "tcb_describe", "tcb_tune", "tcb_cache_load", "tcb_cache_save",
     "tcb_cache_size", "tcb_cache_purge", "tcb_cache_set_history", "tcb_cache_serialize",
     "tcb_cache_deserialize", "tcb_cache_lookup", "tcb_cache_inject", "tcb_canonical",
     "tcb_session_inputs", "tcb_fill_uniform", "tcb_options_validate", "tcb_options_normalize",

@@ -160,7 +160,8 @@ struct tcb_engine {
   }
 
   Compiled& handle(uint64_t h) {
-    if (h == 0 || h > handles.size()) fail(ErrorKind::Name, "unknown kernel handle " + std::to_string(h));
+    if (h == 0 || h > handles.size() || !handles[h - 1])
+      fail(ErrorKind::Name, "unknown (or released) kernel handle " + std::to_string(h));
     return *handles[h - 1];
   }
 };
@@ -596,6 +597,20 @@ int tcb_run_shard(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, cons
         fail(ErrorKind::IndexOutOfRange, "a data-dependent subscript escaped its tensor's extent");
       }
     }
+  });
+}
+
+int tcb_release(tcb_engine* e, uint64_t h) {
+  return guarded([&] {
+    std::unique_ptr<Compiled> dead;
+    {
+      std::lock_guard<std::mutex> g(e->mu);
+      e->handle(h);  // validates
+      dead = std::move(e->handles[h - 1]);
+    }
+    // its device staging / error flag are freed once its last run is done
+    if (dead->lastStream) cudaStreamSynchronize(dead->lastStream);
+    std::lock_guard<std::mutex> rg(dead->runMu);
   });
 }
 

@@ -772,7 +772,19 @@ GenePools genePools(const Problem& p, int math) {
     if (p.family == Family::Gconv) {
       g.tile0 = {128};
       g.tile1 = {static_cast<int64_t>(p.gconv.F)};
-      g.tile2 = {1, 2, 3};  // on-chip im2col | NHWC staging | shifted halo
+      // the shifted-halo kernel where it applies: the on-chip im2col and NHWC
+      // staging variants measured ~4x slower there (dead weight
+      // in the pool); they remain the fallback for shapes it cannot take
+      k::GconvArgs a{};
+      a.C = p.gconv.C;
+      a.H = p.gconv.H;
+      a.W = p.gconv.W;
+      a.F = p.gconv.F;
+      a.KH = p.gconv.KH;
+      a.KW = p.gconv.KW;
+      a.Mb = p.gconv.Mb;
+      if (k::tcGconvShiftSupported(a, math, nullptr)) g.tile2 = {3};
+      else g.tile2 = {1, 2};
       g.bz = {1};
     } else {
       g.tile0 = {128};

@@ -178,6 +178,11 @@ class ExecutionEngine:
     def check(self, handle):
         check(lib.tcb_check(self._h, handle))
 
+    def release(self, handle):
+        """Frees a compiled handle's device staging and error flag
+        (tcb_release); the handle must not be used afterwards."""
+        check(lib.tcb_release(self._h, handle))
+
     def prepare(self, handle, inputs, outputs) -> "PreparedRun":
         """Binds tensors to a compiled handle once, like the reference's
         caller building its DLTensor arrays once (execution_engine.h:93-101);

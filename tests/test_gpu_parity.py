@@ -507,6 +507,24 @@ def test_tuner_parallel_device_workers(engine, oracle, golden, tmp_path, devices
     tcb.cache_purge()
 
 
+def test_release_frees_handle(engine, oracle):
+    """tcb_release: the handle's staging is freed and the id stops working
+    (handles only grew)."""
+    from paper_1802_04730_b200 import TcError
+    rng = oracle.rng(6)
+    A, B = rng.f32((64, 32)), rng.f32((48, 32))
+    C = np.zeros((64, 48), np.float32)
+    h = engine.compile("tmm", [A, B], [C])
+    engine.run(h, [A, B], [C])  # host tensors: allocates the handle's staging
+    np.testing.assert_array_equal(C, oracle.tmm(A, B))
+    engine.release(h)
+    with pytest.raises(TcError) as ei:
+        engine.run(h, [A, B], [C])
+    assert ei.value.kind == "Name"
+    h2 = engine.compile("tmm", [A, B], [C])
+    assert h2 != h
+
+
 def test_paper_style_call(engine, oracle):
     """ee.tmm(A, B) allocates, compiles and runs (PAPER.md:2309-2326)."""
     rng = oracle.rng(5)
