@@ -147,29 +147,21 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN) + 32)
     for (int j = 0; j < RN; ++j) rb[j] = bBase + (uint32_t)((tx + j * TX) * 128);
     const int klim = min(kTK, a.K - kt * kTK);
     if (klim == kTK) {
-      // a register ring of 3 groups: group q+2's shared loads are issued
-      // before group q's FFMAs, so their latency hides behind two groups of
-      // chains (with one group ahead, 2 consumer warps per scheduler could
-      // not cover an LDS round trip: ncu warps-active 13.6%, FMA 28%)
-      float4 av[3][RM], bv[3][RN];
+      float4 av[2][RM], bv[2][RN];
 #pragma unroll
       for (int i = 0; i < RM; ++i) av[0][i] = ldsSw(ra[i], ty + i * TY, 0);
 #pragma unroll
       for (int j = 0; j < RN; ++j) bv[0][j] = ldsSw(rb[j], tx + j * TX, 0);
 #pragma unroll
-      for (int i = 0; i < RM; ++i) av[1][i] = ldsSw(ra[i], ty + i * TY, 1);
-#pragma unroll
-      for (int j = 0; j < RN; ++j) bv[1][j] = ldsSw(rb[j], tx + j * TX, 1);
-#pragma unroll
       for (int q = 0; q < kTK / 4; ++q) {
-        if (q + 2 < kTK / 4) {
+        if (q + 1 < kTK / 4) {  // next group's operands before this group's FFMAs
 #pragma unroll
-          for (int i = 0; i < RM; ++i) av[(q + 2) % 3][i] = ldsSw(ra[i], ty + i * TY, q + 2);
+          for (int i = 0; i < RM; ++i) av[(q + 1) & 1][i] = ldsSw(ra[i], ty + i * TY, q + 1);
 #pragma unroll
-          for (int j = 0; j < RN; ++j) bv[(q + 2) % 3][j] = ldsSw(rb[j], tx + j * TX, q + 2);
+          for (int j = 0; j < RN; ++j) bv[(q + 1) & 1][j] = ldsSw(rb[j], tx + j * TX, q + 1);
         }
-        const float4* x = av[q % 3];
-        const float4* y = bv[q % 3];
+        const float4* x = av[q & 1];
+        const float4* y = bv[q & 1];
 #pragma unroll
         for (int i = 0; i < RM; ++i)
 #pragma unroll
