@@ -155,7 +155,7 @@ class ClockSampler:
             except Exception as e:
                 self.err = f"{type(e).__name__}: {e}"
                 return
-            self.stop.wait(0.001)
+            self.stop.wait(0.0002)
 
     def __enter__(self):
         self.stop = threading.Event()
@@ -237,10 +237,17 @@ def chain_floor_us(op, fma_latency_cycles=4, mhz=1965.0):
     return steps.get(op.name, 0) * fma_latency_cycles / mhz
 
 
-def time_device(torch, fn, iters, stream):
-    """Device time of `iters` calls of fn(i) on `stream`, via CUDA events."""
+def time_device(torch, fn, iters, stream, lead_in=None):
+    """Device time of `iters` calls of fn(i) on `stream`, via CUDA events.
+    lead_in: untimed work enqueued just before the start event (after the
+    synchronize), so the GPU is already busy when the timed region opens and
+    the host's submission of the timed graphs is not counted as device time
+    (a 20-step graph launched onto an idle GPU exposed ~80 us of host submit
+    latency, profiles/r02_final)."""
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    if lead_in is not None:
+        lead_in()
     s.record(stream)
     for i in range(iters):
         fn(i)
@@ -569,8 +576,9 @@ def main():
         # ---- timed region: K steps, barrier + sync both sides, max over ranks
         barrier()
         torch.cuda.synchronize()
-        with ClockSampler(dev) as clk:
-            el = time_device(torch, lambda i: schedule[i].replay(), len(schedule), stream)
+        with ClockSampler(dev) as clk:  # (polls through the lead-in too: the GPU is under load throughout)
+            el = time_device(torch, lambda i: schedule[i].replay(), len(schedule), stream,
+                             lead_in=lambda: g_all.replay())
         torch.cuda.synchronize()
         barrier()
         el = max_over_ranks(el)
@@ -757,7 +765,8 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (U[-1,1) fp32, seeded)",
         "config": step_config(world),
         "timing": {"graphs": "K // %d replays of one CUDA graph of all %d input sets' steps + one graph of the "
-                             "K %% %d remaining steps (3 kernel launches per step)" % (nsets, nsets, nsets) + (
+                             "K %% %d remaining steps (3 kernel launches per step); an untimed %d-step graph "
+                             "replay leads into the start event" % (nsets, nsets, nsets, nsets) + (
                        ", operators serialised on one stream" if args.serial_step else
                        ", the 3 independent operators forked onto 3 streams and joined"),
                    "set_bytes": int(set_bytes), "nsets": nsets},
