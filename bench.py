@@ -155,7 +155,7 @@ class ClockSampler:
             except Exception as e:
                 self.err = f"{type(e).__name__}: {e}"
                 return
-            self.stop.wait(0.0002)
+            self.stop.wait(0.001)
 
     def __enter__(self):
         self.stop = threading.Event()
