@@ -577,8 +577,8 @@ def main():
         barrier()
         torch.cuda.synchronize()
         with ClockSampler(dev) as clk:  # (polls through the lead-in too: the GPU is under load throughout)
-            el = time_device(torch, lambda i: schedule[i].replay(), len(schedule), stream,
-                             lead_in=lambda: g_all.replay())
+            lead = None if os.environ.get("TCB_BENCH_NO_LEADIN") else (lambda: g_all.replay())
+            el = time_device(torch, lambda i: schedule[i].replay(), len(schedule), stream, lead_in=lead)
         torch.cuda.synchronize()
         barrier()
         el = max_over_ranks(el)
