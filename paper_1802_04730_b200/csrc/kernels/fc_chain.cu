@@ -43,7 +43,6 @@ struct FcPlan {
   int denseIn;              // input rows land unpadded with one copy (ald[0] == kred, conflict-free)
   int bulk;                 // 1: cp.async.bulk path, 2: 16-byte cp.async path, 0: cooperative loads
   int nch, kc4;             // cp.async path: layer 0 in nch chunks of kc4 float4s of the reduction
-  int tile[kMaxLayers];     // 2: this layer's chains run as 2x2 tiles per thread (chain22), 1: one per thread
 };
 
 __host__ __device__ inline int up4(int x) { return (x + 3) & ~3; }
@@ -175,53 +174,6 @@ __device__ __forceinline__ float chainSegment(unsigned xa, unsigned wa, int n, f
   for (; kk + 4 <= n; kk += 4) acc = fma4(lds4(xa + kk * 4), lds4(wa + kk * 4), acc);
   for (; kk < n; ++kk) acc = __fmaf_rn(lds1(xa + kk * 4), lds1(wa + kk * 4), acc);
   return acc;
-}
-
-// Four chains at once — rows xa0/xa1 x weight rows wa0/wa1 (a 2x2 tile of
-// outputs) — each still its own sequential k chain. Per 4-step group: four
-// shared loads for 16 FFMAs instead of two per 4 (chainSegment), halving the
-// LSU wavefronts per chain step; a 3-deep register ring of groups keeps the
-// loads two groups ahead. Reads up to 12 floats past n (plan slack).
-__device__ __forceinline__ void chain22(unsigned xa0, unsigned xa1, unsigned wa0, unsigned wa1, int n, float& a00,
-                                        float& a01, float& a10, float& a11) {
-  const int ng = n >> 2;
-  float4 X0[3], X1[3], W0[3], W1[3];
-#define TCB_LD22(g, s_)                   \
-  do {                                    \
-    X0[s_] = lds4(xa0 + (g) * 16);        \
-    X1[s_] = lds4(xa1 + (g) * 16);        \
-    W0[s_] = lds4(wa0 + (g) * 16);        \
-    W1[s_] = lds4(wa1 + (g) * 16);        \
-  } while (0)
-#define TCB_FMA22(s_)                     \
-  do {                                    \
-    a00 = fma4(X0[s_], W0[s_], a00);      \
-    a01 = fma4(X0[s_], W1[s_], a01);      \
-    a10 = fma4(X1[s_], W0[s_], a10);      \
-    a11 = fma4(X1[s_], W1[s_], a11);      \
-  } while (0)
-  TCB_LD22(0, 0);
-  TCB_LD22(1, 1);
-  int g = 0;
-  for (; g + 3 <= ng; g += 3) {
-    TCB_LD22(g + 2, 2);
-    TCB_FMA22(0);
-    TCB_LD22(g + 3, 0);
-    TCB_FMA22(1);
-    TCB_LD22(g + 4, 1);
-    TCB_FMA22(2);
-  }
-  if (g < ng) TCB_FMA22(0);
-  if (g + 1 < ng) TCB_FMA22(1);
-#undef TCB_LD22
-#undef TCB_FMA22
-  for (int kk = ng * 4; kk < n; ++kk) {
-    const float x0 = lds1(xa0 + kk * 4), x1 = lds1(xa1 + kk * 4), w0 = lds1(wa0 + kk * 4), w1 = lds1(wa1 + kk * 4);
-    a00 = __fmaf_rn(x0, w0, a00);
-    a01 = __fmaf_rn(x0, w1, a01);
-    a10 = __fmaf_rn(x1, w0, a10);
-    a11 = __fmaf_rn(x1, w1, a11);
-  }
 }
 
 #ifdef TCB_FC_TRACE
@@ -413,54 +365,6 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     if (p.bulk == 2 && l > 0) asyncWait(NL - 1 - l);
     FC_STAMP(3 + 3 * l);
     if (!last && l == 0 && cn > 1) asm volatile("barrier.cluster.wait;" ::: "memory");
-    if (p.tile[l] == 2) {
-      // 2x2 tiles: rows {rp, rp + R/2} x columns {cp, cp + cols/2}
-      const int hr = R >> 1, hc = cols >> 1, ntiles = hr * hc;
-      float bpre = 0.0f;
-#pragma unroll
-      for (int q = 0; q < kMaxLayers; ++q)
-        if (q == l) bpre = biasPre[q];
-      (void)bpre;
-      for (int base = 0; base < ntiles; base += T) {
-        const int t = base + tid;
-        const bool lt = t < ntiles;
-        const int rp = lt ? t % hr : 0, cp = lt ? t / hr : 0;
-        const int rr[2] = {rp, rp + hr}, cc[2] = {cp, cp + hc};
-        bool lv[2][2];
-        float acc[2][2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            lv[i][j] = lt && c0 + cc[j] < L.out;
-            acc[i][j] = lv[i][j] ? __ldg(L.bias + c0 + cc[j]) : 0.0f;
-          }
-        chain22(actBase + (unsigned)(rr[0] * ald) * 4u, actBase + (unsigned)(rr[1] * ald) * 4u,
-                wBase + (unsigned)(cc[0] * p.wld[l]) * 4u, wBase + (unsigned)(cc[1] * p.wld[l]) * 4u, L.kred,
-                acc[0][0], acc[0][1], acc[1][0], acc[1][1]);
-        FC_STAMP(16 + l);
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            if (!lv[i][j]) continue;
-            const int r = rr[i], c = cc[j];
-            const float v = fmaxf(acc[i][j], 0.0f);
-            if (r < rows) L.O[(int64_t)(row0 + r) * L.out + c0 + c] = v;
-            if (!last) {
-              float* dst = sm + p.offAct[l + 1] + r * p.ald[l + 1] + c0 + c;
-              if (cn > 1) {
-                for (int q = 0; q < cn; ++q) stAsyncCluster(dst, &bars[l + 1], q, v);
-              } else {
-                *dst = v;
-              }
-            }
-          }
-      }
-      FC_STAMP(4 + 3 * l);
-      if (!last && cn == 1) __syncthreads();
-      continue;
-    }
     const int nchains = R * cols;
     for (int base = 0; base < nchains; base += T) {
       // one (row, column) chain per thread and pass, row fastest; idle
@@ -509,16 +413,10 @@ __global__ void __launch_bounds__(kFcMaxThreads)
 
 // Builds the plan; returns the dynamic shared-memory size. Every operand
 // buffer is followed by >= 32 floats of slack (the chain prefetches ahead).
-static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads = 0, int tile = 1) {
+static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads = 0) {
   p = FcPlan{};
   p.cn = cn;
   p.R = R;
-  for (int l = 0; l < a.layers; ++l) {
-    const int cols = (a.L[l].out + cn - 1) / cn;
-    // 2x2 chain tiles where the layer's rows and column slice split evenly
-    // (the layer-0 cp.async chunk path keeps single chains)
-    p.tile[l] = (tile == 2 && R % 2 == 0 && cols % 2 == 0 && !(l == 0 && (loads == 2 || loads == 3))) ? 2 : 1;
-  }
   int off = 0;
   for (int l = 0; l < a.layers; ++l) {
     p.cols[l] = (a.L[l].out + cn - 1) / cn;
@@ -602,10 +500,10 @@ static void (*fcKernel(int layers))(FcChainArgs, FcPlan) {
   }
 }
 
-cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s, int loads, int tile) {
+cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s, int loads) {
   if (a.batch <= 0) return cudaSuccess;
   FcPlan p;
-  size_t smem = planFc(a, rows, cn, p, loads, tile);
+  size_t smem = planFc(a, rows, cn, p, loads);
   if (smem > 227 * 1024 || cn < 1 || cn > 16 || rows < 1) return cudaErrorInvalidConfiguration;
   if (threads < 32 || threads > kFcMaxThreads || threads % 32) return cudaErrorInvalidConfiguration;
   void (*kern)(FcChainArgs, FcPlan) = fcKernel(a.layers);

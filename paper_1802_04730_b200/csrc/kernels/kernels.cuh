@@ -95,9 +95,7 @@ struct FcChainArgs {
 };
 // loads: 0 = automatic (bulk copies), 1 = bulk copies, 2 = 16-byte cp.async
 // with layer 0 in reduction chunks, 3 = cp.async in one chunk
-// tile: 2 = 2x2 chain tiles per thread where the rows / column slices split evenly
-cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s, int loads = 0,
-                          int tile = 1);
+cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s, int loads = 0);
 size_t fcChainSmem(const FcChainArgs& a, int rows, int cn);
 int fcChainThreads(const FcChainArgs& a, int rows, int cn);  // single-pass block size
 // register-resident chains (fc_regs.cu): every layer kred <= 128, one CTA per

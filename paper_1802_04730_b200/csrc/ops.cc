@@ -304,8 +304,7 @@ std::string Mapping::describe() const {
       if (fused && fcKind == 1) os << "registers rows=" << rows;
       else if (fused)
         os << "cluster rows=" << rows << " cn=" << cn << " threads=" << threads
-           << (fcLoads == 1 ? " loads=bulk" : fcLoads == 2 ? " loads=cp.async" : fcLoads == 3 ? " loads=cp.async/1" : "")
-           << (fcTile == 2 ? " tiles=2x2" : "");
+           << (fcLoads == 1 ? " loads=bulk" : fcLoads == 2 ? " loads=cp.async" : fcLoads == 3 ? " loads=cp.async/1" : "");
       else os << "per-layer " << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
       break;
     case Family::Kru3: os << "fused dchunk=" << dchunk << " threads=" << threads; break;
@@ -497,8 +496,6 @@ Mapping decode(const Problem& p, const MappingOptions& o, int math) {
       // kernel with bulk-copy / cp.async loads
       if (o.tileSizes.size() > 2 && (o.tileSizes[2] == 3 || o.tileSizes[2] == 4 || o.tileSizes[2] == 5))
         m.fcLoads = o.tileSizes[2] == 3 ? 1 : o.tileSizes[2] == 4 ? 2 : 3;
-      // tile_sizes[2] == 6: 2x2 chain tiles per thread (bulk loads)
-      if (o.tileSizes.size() > 2 && o.tileSizes[2] == 6) m.fcTile = 2;
       if (o.tileSizes.size() > 2 && o.tileSizes[2] == 2) {
         // tile_sizes[2] == 2: register chains, tile_sizes[0] rows per CTA
         m.fcKind = 1;
@@ -813,7 +810,7 @@ GenePools genePools(const Problem& p, int math) {
       if (p.family == Family::FcChain) {
         g.tile0 = {1, 2, 4, 8, 16, 32, 64};
         g.tile1 = {1, 2, 4, 8, 16, 32, 64};
-        g.tile2 = {1, 2, 3, 4, 6, 16, 32, 64};  // fused: 1 = cluster kernel, 2 = register chains, 3/4 = cluster loads, 6 = 2x2 chain tiles
+        g.tile2 = {1, 2, 3, 4, 16, 32, 64};  // fused: 1 = cluster kernel, 2 = register chains, 3/4 = cluster loads
         g.tx = {4, 8, 16, 32, 64, 128, 256, 512};
         g.fusion = {Fusion::Max, Fusion::Min};
       }
@@ -991,7 +988,7 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
         check(k::launchFcRegs(a, m.rows, s), "FC chain (registers)");
         return;
       }
-      check(k::launchFcChain(a, m.rows, m.cn, m.threads, s, m.fcLoads, m.fcTile), "FC chain");
+      check(k::launchFcChain(a, m.rows, m.cn, m.threads, s, m.fcLoads), "FC chain");
       return;
     }
     case Family::Kru3: {

@@ -176,31 +176,6 @@ def test_fc_chain_cluster_variants(engine, oracle, golden, rows, cn, threads):
     assert ran >= 3
 
 
-@pytest.mark.parametrize("rows,cn,threads", [(4, 8, 32), (8, 8, 32), (8, 8, 64), (16, 8, 64), (8, 4, 64), (2, 2, 32),
-                                             (6, 3, 32)])
-def test_fc_chain_tiles(engine, oracle, golden, rows, cn, threads):
-    """2x2 chain tiles per thread in the cluster kernel (tile_sizes[2] == 6):
-    bit-exact on every golden FC case; layers whose rows or column slices
-    do not split evenly keep one chain per thread."""
-    from paper_1802_04730_b200 import TcError
-    ran = 0
-    for name in ["2fcrelu_small", "mlp3_small", "mlp3_paper", "mlp1_ragged", "2fcrelu_paper", "mlp1_paper"]:
-        case, ins, seeded = case_inputs(oracle, golden, name)
-        o = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0,
-             "shared_memory_budget": 49152, "thread_shape": [threads, 1, 1], "tile_sizes": [rows, cn, 6],
-             "unroll_copy_shared": False, "unroll_factor": 1, "use_private": False, "use_shared": True}
-        try:
-            got, h = run_on_gpu(engine, case["def"], ins, seeded, options=o)
-        except TcError as e:
-            assert e.kind == "MappingInvalid", str(e)
-            continue
-        assert "tiles=2x2" in engine.describe(h)["kernel"]
-        ran += 1
-        for k, rec in case["outputs"].items():
-            assert_exact(oracle, f"{name}/tiles{rows}x{cn}", k, got[k], rec["fnv"])
-    assert ran >= 3
-
-
 @pytest.mark.parametrize("rows", [1, 2, 4])
 def test_fc_regs_variants(engine, oracle, golden, rows):
     """Register-resident FC chains (fc_regs.cu, tile_sizes[2] == 2) at 1, 2 and
