@@ -16,13 +16,15 @@ from paper_1802_04730_b200 import ExecutionEngine  # noqa: E402
 
 NSTEP = int(os.environ.get("NSTEP", "26"))
 
-COMBOS = [  # r02: fewer, fuller FC CTAs so the step's kernels can share SMs
-    {"2FCRelu": {"tile_sizes": [8, 8, 1], "thread_shape": [128, 1, 1]}},
-    {"2FCRelu": {"tile_sizes": [8, 8, 1], "thread_shape": [128, 1, 1]}, "MLP3": {"tile_sizes": [8, 4, 1], "thread_shape": [64, 1, 1]}},
-    {"2FCRelu": {"tile_sizes": [8, 8, 1], "thread_shape": [128, 1, 1]}, "MLP3": {"tile_sizes": [8, 2, 1], "thread_shape": [64, 1, 1]}},
-    {"2FCRelu": {"tile_sizes": [16, 8, 1], "thread_shape": [256, 1, 1]}},
-    {"MLP3": {"tile_sizes": [8, 4, 1], "thread_shape": [64, 1, 1]}},
+COMBOS = [  # r02: step plans (footprint-light TBMM plans beside the FC chains)
+    {"tbmm": {"tile_sizes": [4, 1, 2]}},
     {"tbmm": {"tile_sizes": [13, 1, 2]}},
+    {"tbmm": {"tile_sizes": [4, 2, 2], "thread_shape": [32, 1, 1], "block_shape": [1, 1, 1]}},
+    {"tbmm": {"tile_sizes": [32, 32, 32], "thread_shape": [16, 16, 1], "block_shape": [1, 1, 1]}},
+    {"tbmm": {"tile_sizes": [4, 1, 2]}, "MLP3": {"tile_sizes": [2, 4, 1], "thread_shape": [64, 1, 1]}},
+    {"tbmm": {"tile_sizes": [4, 1, 2]}, "MLP3": {"tile_sizes": [4, 2, 1], "thread_shape": [64, 1, 1]}},
+    {"tbmm": {"tile_sizes": [4, 1, 2]}, "MLP3": {"tile_sizes": [1, 1, 2], "thread_shape": [64, 1, 1]}},
+    {"tbmm": {"tile_sizes": [4, 1, 2]}, "2FCRelu": {"tile_sizes": [4, 8, 1], "thread_shape": [64, 1, 1], "unroll_copy_shared": True}},
 ]
 
 VARIANTS = {
