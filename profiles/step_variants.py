@@ -18,13 +18,6 @@ NSTEP = int(os.environ.get("NSTEP", "26"))
 
 COMBOS = [  # r02: step plans (footprint-light TBMM plans beside the FC chains)
     {"tbmm": {"tile_sizes": [4, 1, 2]}},
-    {"tbmm": {"tile_sizes": [13, 1, 2]}},
-    {"tbmm": {"tile_sizes": [4, 2, 2], "thread_shape": [32, 1, 1], "block_shape": [1, 1, 1]}},
-    {"tbmm": {"tile_sizes": [32, 32, 32], "thread_shape": [16, 16, 1], "block_shape": [1, 1, 1]}},
-    {"tbmm": {"tile_sizes": [4, 1, 2]}, "MLP3": {"tile_sizes": [2, 4, 1], "thread_shape": [64, 1, 1]}},
-    {"tbmm": {"tile_sizes": [4, 1, 2]}, "MLP3": {"tile_sizes": [4, 2, 1], "thread_shape": [64, 1, 1]}},
-    {"tbmm": {"tile_sizes": [4, 1, 2]}, "MLP3": {"tile_sizes": [1, 1, 2], "thread_shape": [64, 1, 1]}},
-    {"tbmm": {"tile_sizes": [4, 1, 2]}, "2FCRelu": {"tile_sizes": [4, 8, 1], "thread_shape": [64, 1, 1], "unroll_copy_shared": True}},
 ]
 
 VARIANTS = {
@@ -40,7 +33,9 @@ def main():
     dev = torch.device("cuda", 0)
     ops = {n: bench.OpInstance(ee, torch, n, s, sd, NSTEP, dev, 1 + i) for i, (n, s, sd) in enumerate(bench.STEP_OPS)}
     main_s = torch.cuda.Stream()
-    side = [torch.cuda.Stream() for _ in range(3)]
+    # PRIO="a,b,c": stream priorities of the tbmm / 2FCRelu / MLP3 side streams (lower = higher priority)
+    prio = [int(x) for x in os.environ.get("PRIO", "0,0,0").split(",")]
+    side = [torch.cuda.Stream(priority=p) for p in prio]
 
     def graph_of(group):
         def body():
