@@ -71,6 +71,13 @@ TC_OPS = [("tmm 128x1024x1024", "3xtf32"), ("tmm 128x1024x1024", "tf32"),
           ("3KRU M=256 16^3->32^3", "3xtf32"), ("3KRU M=256 16^3->32^3", "tf32"),
           ("gconv paper 32,32,16,16,14x14", "tf32"), ("gconv paper 32,32,32,32,7x7", "tf32")]
 INT_PARAMS = {"2LUT": {1, 3}, "1LUT": {1}}
+# Plans passed explicitly for the forked step (merged over each op's default
+# options), measured over the step, not each op alone
+# (profiles/r02_step_variants.txt): the 4-rows-per-warp slab is slower alone
+# (9.6 vs 6.9 us) but its lighter CTAs share SMs with the FC chains better
+# (step 16.2 -> 15.6 us). The library defaults stay the standalone-best
+# plans.
+STEP_PLANS = {"tbmm": {"tile_sizes": [4, 1, 2]}}
 
 
 def step_set_bytes():
@@ -182,7 +189,7 @@ class ClockSampler:
 class OpInstance:
     """One TC op bound to device tensors (a rotating set of input copies)."""
 
-    def __init__(self, ee, torch, name, pshapes, seeded, nsets, dev, seed, host_init=True, math="ffma"):
+    def __init__(self, ee, torch, name, pshapes, seeded, nsets, dev, seed, host_init=True, math="ffma", plan=None):
         self.ee, self.torch, self.name = ee, torch, name
         _, rets = ee.signature(name)
         ints = INT_PARAMS.get(name, set())
@@ -204,7 +211,10 @@ class OpInstance:
             os_ = [torch.rand(s, generator=g, device=dev) * 2 - 1 if i in self.inout else
                    torch.zeros(s, device=dev) for i, s in enumerate(oshapes)]
             self.sets.append((ps, os_))
-        self.handle = ee.compile(name, self.sets[0][0], self.sets[0][1], math=math)
+        opts = None
+        if plan:
+            opts = dict(ee.default_options(name, self.sets[0][0], self.sets[0][1]), **plan)
+        self.handle = ee.compile(name, self.sets[0][0], self.sets[0][1], opts, math=math)
         d = ee.describe(self.handle)
         self.flops, self.bytes, self.kernel = d["flops"], d["bytes"], d["kernel"]
 
@@ -506,8 +516,8 @@ def main():
 
     # rotating input sets larger than L2 (inputs AND weights rotate)
     nsets = max(2, int(np.ceil(2 * L2_BYTES / step_set_bytes())))
-    ops = [OpInstance(ee, torch, n, s, sd, nsets, dev, 1 + i + 100 * rank) for i, (n, s, sd) in
-           enumerate(STEP_OPS)]
+    ops = [OpInstance(ee, torch, n, s, sd, nsets, dev, 1 + i + 100 * rank, plan=STEP_PLANS.get(n)) for i, (n, s, sd)
+           in enumerate(STEP_OPS)]
     set_bytes = sum(o.set_bytes() for o in ops)
     flops_step = sum(o.flops for o in ops)
     stream = torch.cuda.Stream(device=dev)
@@ -672,7 +682,8 @@ def main():
             ps, os_ = o.sets[0]
             hp = [x.cpu().pin_memory() for x in ps]
             ho = [x.cpu().pin_memory() for x in os_]
-            hh = ee.compile(o.name, hp, ho)
+            plan = STEP_PLANS.get(o.name)
+            hh = ee.compile(o.name, hp, ho, dict(ee.default_options(o.name, hp, ho), **plan) if plan else None)
             host.append((hh, hp, ho))
             h2d += sum(x.numel() * 4 for x in hp) + sum(x.numel() * 4 for i, x in enumerate(ho) if i in o.inout)
             d2h += sum(x.numel() * 4 for x in ho)
@@ -769,7 +780,8 @@ def main():
                              "replay leads into the start event" % (nsets, nsets, nsets, nsets) + (
                        ", operators serialised on one stream" if args.serial_step else
                        ", the 3 independent operators forked onto 3 streams and joined"),
-                   "set_bytes": int(set_bytes), "nsets": nsets},
+                   "set_bytes": int(set_bytes), "nsets": nsets,
+                   "step_plans": STEP_PLANS},
         "e2e": {"value": round(e2e_value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "us_per_step": round(e2e_t / ke * 1e6, 2),
                 "timing": "host wall clock, median of 5 blocks of %d steps; each step = the 3 tcb_run calls with "
