@@ -101,6 +101,10 @@ int fcChainThreads(const FcChainArgs& a, int rows, int cn);  // single-pass bloc
 // register-resident chains (fc_regs.cu): every layer kred <= 128, one CTA per
 // `rows` (1, 2, 4) batch rows, one warp group per layer, weights in registers
 bool fcRegsSupported(const FcChainArgs& a, int rows, const char** why);
+// one-kernel tcgen05 FC chain (tc_fc_fused.cu): every layer in one CTA per
+// 128 rows, activations TMEM -> shared memory -> next layer's A operand
+bool tcFcFusedSupported(const FcChainArgs& a, int math, const char** why);
+cudaError_t launchTcFcFused(const FcChainArgs& a, int math, cudaStream_t s);
 cudaError_t launchFcRegs(const FcChainArgs& a, int rows, cudaStream_t s);
 
 // ------------------------------------------------------------------ KRU

@@ -117,6 +117,23 @@ void decodeTc(const Problem& p, const MappingOptions& o, Mapping& m) {
     }
   }
   m.fused = false;
+  if (p.family == Family::FcChain && !(o.tileSizes.size() > 2 && o.tileSizes[2] == 1)) {
+    // the one-kernel chain where every layer fits it (tile_sizes[2] == 1
+    // asks for the per-layer tc_gemm launches instead)
+    k::FcChainArgs a{};
+    a.layers = static_cast<int>(p.fc.layers.size());
+    a.ldi = p.fc.ldi;
+    a.batch = p.fc.batch;
+    for (int l = 0; l < a.layers; ++l) {
+      a.L[l].out = p.fc.layers[l].out;
+      a.L[l].kred = p.fc.layers[l].kred;
+      a.L[l].ldw = p.fc.layers[l].ldw;
+    }
+    if (k::tcFcFusedSupported(a, m.math, nullptr)) {  // (null pointers pass the alignment checks)
+      m.tcFused = true;
+      return;
+    }
+  }
   int64_t bn = o.tileSizes.size() > 1 ? o.tileSizes[1] : 0;
   int64_t sp = o.blockShape[2];
   if (bn <= 1) {
@@ -284,6 +301,7 @@ std::string Mapping::describe() const {
       return os.str() + (gconvVariant == 1   ? " implicit-GEMM (on-chip im2col)"
                          : gconvVariant == 2 ? " implicit-GEMM (shifted halo)"
                                              : " implicit-GEMM (NHWC staging)");
+    if (family == Family::FcChain && tcFused) return os.str() + " fused chain (TMEM -> next layer's A in smem)";
     if (tcAuto) os << " planned";
     else os << " bn=" << tc.bn << " splits=" << tc.splits;
     if (family == Family::FcChain) os << " per-layer";
@@ -945,6 +963,24 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
     case Family::Gemm: launchGemmDesc(p.gemm, m, in, out, s); return;
     case Family::FcChain: {
       const FcDesc& f = p.fc;
+      if (m.math != k::kMathFfma && m.tcFused) {
+        k::FcChainArgs a{};
+        a.I = static_cast<const float*>(ptr(f.I));
+        a.ldi = f.ldi;
+        a.batch = f.batch;
+        a.layers = static_cast<int>(f.layers.size());
+        for (int l = 0; l < a.layers; ++l) {
+          const auto& L = f.layers[l];
+          a.L[l].W = static_cast<const float*>(ptr(L.W));
+          a.L[l].bias = static_cast<const float*>(ptr(L.bias));
+          a.L[l].O = static_cast<float*>(ptr(L.O));
+          a.L[l].out = L.out;
+          a.L[l].kred = L.kred;
+          a.L[l].ldw = L.ldw;
+        }
+        check(k::launchTcFcFused(a, m.math, s), "fused tensor-core FC chain");
+        return;
+      }
       if (!m.fused) {
         // one GEMM per layer: init = bias, epilogue = ReLU; layer l>0 reads
         // layer l-1's global output

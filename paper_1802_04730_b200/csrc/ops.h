@@ -83,6 +83,7 @@ struct Mapping {
   int math = k::kMathFfma;
   k::TcPlan tc;  // tensor-core tile plan (math != FFMA); per-layer plans are derived at launch
   bool tcAuto = true;
+  bool tcFused = false;  // FC chains in tensor-core math: the one-kernel chain (tc_fc_fused.cu)
   // Gemm (and unfused FC layers)
   int gemmVariant = 4, gemmThreads = 0;
   // FcChain
