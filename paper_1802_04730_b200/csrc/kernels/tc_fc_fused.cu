@@ -293,7 +293,7 @@ bool tcFcFusedSupported(const FcChainArgs& a, int math, const char** why) {
     if (L.out > 256 || L.out < 1) return no("fused tensor-core FC chain: at most 256 outputs per layer");
     if (L.ldw % 4 || !al16(L.W)) return no("fused tensor-core FC chain: 16-byte weight rows");
     if (l + 1 < a.layers && a.L[l + 1].kred > up16(L.out)) return no("fused tensor-core FC chain: layer widths");
-    if (L.out % 4 || !al16(L.O)) return no("fused tensor-core FC chain: 16-byte output rows");
+    if (L.out % 4 == 0 && !al16(L.O)) return no("fused tensor-core FC chain: 16-byte aligned outputs");
     cols += up16(L.out);
   }
   if (a.ldi % 4 || !al16(a.I)) return no("fused tensor-core FC chain: 16-byte input rows");
