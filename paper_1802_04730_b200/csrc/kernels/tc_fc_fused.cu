@@ -71,6 +71,21 @@ __device__ __forceinline__ void splitPlane(float* hi, float* lo, int bytes, int 
   }
 }
 
+#ifdef TCB_TCFC_TRACE
+// diagnostic build only (profiles/tcfc_trace.cu): globaltimer stamps of CTA 0
+__device__ unsigned long long g_tcfc_trace[8];
+#define TCFC_STAMP(ev)                                              \
+  do {                                                              \
+    unsigned long long t_;                                          \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));         \
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_tcfc_trace[ev] = t_; \
+  } while (0)
+#else
+#define TCFC_STAMP(ev) \
+  do {                 \
+  } while (0)
+#endif
+
 template <int NL, bool X3>
 __global__ void __launch_bounds__(128, 1)
     tc_fc_fused_kernel(const __grid_constant__ CUtensorMap tIn, const __grid_constant__ CUtensorMap tW0,
@@ -80,6 +95,7 @@ __global__ void __launch_bounds__(128, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int row0 = blockIdx.x * kRowsTc;
+  TCFC_STAMP(0);
   // regions: A hi [, A lo], then per layer B hi [, B lo]
   uint8_t* aHi = sm;
   uint8_t* aLo = sm + p.aBytes;
@@ -111,6 +127,7 @@ __global__ void __launch_bounds__(128, 1)
         tmaLoad3d(sm + p.bOff[l] + c * p.Np[l] * 128, tw[l], c * 32, 0, 0, landed);
   }
   mbarWait(landed, 0, 0);
+  TCFC_STAMP(1);
   if constexpr (X3) {
     splitPlane(reinterpret_cast<float*>(aHi), reinterpret_cast<float*>(aLo), p.K[0] / 32 * kRowsTc * 128, tid, 128);
 #pragma unroll
@@ -120,6 +137,7 @@ __global__ void __launch_bounds__(128, 1)
     fenceProxyAsyncSmem();
     __syncthreads();
   }
+  TCFC_STAMP(2);
 
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
@@ -150,6 +168,7 @@ __global__ void __launch_bounds__(128, 1)
       __syncwarp();
     }
     mbarWait(mmaDone, l & 1, 1);
+    TCFC_STAMP(3 + 2 * l);
     tcFenceAfter();
     // ---- epilogue: TMEM lane = row; + bias, ReLU, store, next layer's A
     const int row = warp * 32 + lane, grow = row0 + row;
@@ -194,6 +213,7 @@ __global__ void __launch_bounds__(128, 1)
     fenceProxyAsyncSmem();  // the next layer's A, written by the generic proxy, for the tensor core
     tcFenceBefore();
     __syncthreads();
+    TCFC_STAMP(4 + 2 * l);
   }
   if (warp == 0) {
     tcFenceAfter();
