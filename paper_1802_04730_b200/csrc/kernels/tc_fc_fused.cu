@@ -86,8 +86,10 @@ __device__ unsigned long long g_tcfc_trace[8];
   } while (0)
 #endif
 
+constexpr int kThreadsFc = 512;  // 16 warps: elementwise passes and the epilogues use all of them
+
 template <int NL, bool X3>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(kThreadsFc, 1)
     tc_fc_fused_kernel(const __grid_constant__ CUtensorMap tIn, const __grid_constant__ CUtensorMap tW0,
                        const __grid_constant__ CUtensorMap tW1, const __grid_constant__ CUtensorMap tW2,
                        const __grid_constant__ FusedPlan p) {
@@ -103,6 +105,7 @@ __global__ void __launch_bounds__(128, 1)
   uint64_t* landed = bars;
   uint64_t* mmaDone = bars + 1;
   uint32_t* tmemSlot = reinterpret_cast<uint32_t*>(bars + 2);
+  float* sBias = reinterpret_cast<float*>(bars + 4);  // [NL][256]: every layer's bias, zero past N_l
   constexpr int kCols = 256;  // all layers' accumulators side by side: sum of N_l padded to 16 (<= 256, checked)
   if (tid == 0) {
     mbarInit(landed, 1);
@@ -110,6 +113,9 @@ __global__ void __launch_bounds__(128, 1)
     fenceBarrierInit();
   }
   if (warp == 0) tmemAlloc<kCols>(tmemSlot);
+#pragma unroll
+  for (int l = 0; l < NL; ++l)
+    for (int n = tid; n < 256; n += kThreadsFc) sBias[l * 256 + n] = n < p.N[l] ? __ldg(p.bias[l] + n) : 0.0f;
   tcFenceBefore();
   __syncthreads();
   tcFenceAfter();
@@ -129,11 +135,12 @@ __global__ void __launch_bounds__(128, 1)
   mbarWait(landed, 0, 0);
   TCFC_STAMP(1);
   if constexpr (X3) {
-    splitPlane(reinterpret_cast<float*>(aHi), reinterpret_cast<float*>(aLo), p.K[0] / 32 * kRowsTc * 128, tid, 128);
+    splitPlane(reinterpret_cast<float*>(aHi), reinterpret_cast<float*>(aLo), p.K[0] / 32 * kRowsTc * 128, tid,
+               kThreadsFc);
 #pragma unroll
     for (int l = 0; l < NL; ++l)
       splitPlane(reinterpret_cast<float*>(sm + p.bOff[l]), reinterpret_cast<float*>(sm + p.bOff[l] + p.bBytes[l]),
-                 p.bBytes[l], tid, 128);
+                 p.bBytes[l], tid, kThreadsFc);
     fenceProxyAsyncSmem();
     __syncthreads();
   }
@@ -170,11 +177,13 @@ __global__ void __launch_bounds__(128, 1)
     mbarWait(mmaDone, l & 1, 1);
     TCFC_STAMP(3 + 2 * l);
     tcFenceAfter();
-    // ---- epilogue: TMEM lane = row; + bias, ReLU, store, next layer's A
-    const int row = warp * 32 + lane, grow = row0 + row;
+    // ---- epilogue: warp w reads TMEM lane quarter w % 4 (rows) and the
+    // 16-column groups w / 4, w / 4 + 4, ...; + bias, ReLU, store, next A
+    const int q4 = warp & 3, row = q4 * 32 + lane, grow = row0 + row;
     const bool last = l + 1 == NL;
-    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16) + p.tcol[l];
-    for (int c0 = 0; c0 < Np; c0 += 16) {
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q4 * 32) << 16) + p.tcol[l];
+    const float* bl = sBias + l * 256;
+    for (int c0 = (warp >> 2) * 16; c0 < Np; c0 += (kThreadsFc / 128) * 16) {
       float v[16];
       tmemLoad16(trow + c0, v);
       tmemLoadWait();
@@ -185,7 +194,7 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int n = c0 + j + q;
-          op[q] = n < p.N[l] ? fmaxf(v[j + q] + __ldg(p.bias[l] + n), 0.0f) : 0.0f;
+          op[q] = n < p.N[l] ? fmaxf(v[j + q] + bl[n], 0.0f) : 0.0f;
         }
         const int n = c0 + j;
         if (grow < p.batch && n < p.N[l]) {
@@ -278,7 +287,7 @@ int planFused(const FcChainArgs& a, bool x3, FusedPlan& p) {
     p.tcol[l] = col;
     col += x3 ? p.Np[l] : p.Np[l];
   }
-  return off + 64 + 1024;  // + barriers/slot, + alignment slack
+  return off + 64 + 4 * kFcMaxL * 256 + 1024;  // + barriers/slot, biases, alignment slack
 }
 
 template <int NL, bool X3>
@@ -292,7 +301,7 @@ cudaError_t launchFusedT(const FcChainArgs& a, cudaStream_t s) {
   auto kern = tc_fc_fused_kernel<NL, X3>;
   cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kern), smemBytes);
   if (e != cudaSuccess) return e;
-  kern<<<(a.batch + kRowsTc - 1) / kRowsTc, 128, smemBytes, s>>>(tIn, tw[0], tw[1], tw[2], p);
+  kern<<<(a.batch + kRowsTc - 1) / kRowsTc, kThreadsFc, smemBytes, s>>>(tIn, tw[0], tw[1], tw[2], p);
   return cudaGetLastError();
 }
 
