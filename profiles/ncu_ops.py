@@ -58,7 +58,8 @@ def main():
         given = [seeded.get(i) for i in range(len(rets))]
         oshapes = ee.infer_output_tensor_info(name, shapes, given)
         outs = [torch.rand(s, device="cuda") for s in oshapes]
-        h = ee.compile(name, ps, outs, opts, math=math)
+        o = dict(ee.default_options(name, ps, outs), **opts) if opts else None  # as bench.py's STEP_PLANS
+        h = ee.compile(name, ps, outs, o, math=math)
         print(a, ee.describe(h)["kernel"], flush=True)
         for _ in range(reps):
             ee.run(h, ps, outs)
