@@ -502,6 +502,7 @@ static void (*fcKernel(int layers))(FcChainArgs, FcPlan) {
 
 cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s, int loads) {
   if (a.batch <= 0) return cudaSuccess;
+  if (loads == 4) return launchFcTma(a, rows, cn, threads, s);
   FcPlan p;
   size_t smem = planFc(a, rows, cn, p, loads);
   if (smem > 227 * 1024 || cn < 1 || cn > 16 || rows < 1) return cudaErrorInvalidConfiguration;

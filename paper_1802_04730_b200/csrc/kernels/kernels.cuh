@@ -94,7 +94,8 @@ struct FcChainArgs {
   FcLayer L[kMaxLayers];
 };
 // loads: 0 = automatic (bulk copies), 1 = bulk copies, 2 = 16-byte cp.async
-// with layer 0 in reduction chunks, 3 = cp.async in one chunk
+// with layer 0 in reduction chunks, 3 = cp.async in one chunk, 4 = layer 0 by
+// TMA tensor copies in reduction chunks (fc_tma.cu)
 cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s, int loads = 0);
 size_t fcChainSmem(const FcChainArgs& a, int rows, int cn);
 int fcChainThreads(const FcChainArgs& a, int rows, int cn);  // single-pass block size
@@ -106,6 +107,10 @@ bool fcRegsSupported(const FcChainArgs& a, int rows, const char** why);
 bool tcFcFusedSupported(const FcChainArgs& a, int math, const char** why);
 cudaError_t launchTcFcFused(const FcChainArgs& a, int math, cudaStream_t s);
 cudaError_t launchFcRegs(const FcChainArgs& a, int rows, cudaStream_t s);
+// the cluster kernel with layer 0 streamed in by TMA tensor copies in 256-step
+// reduction chunks (fc_tma.cu): layer 0's chains start on the first chunk
+bool fcTmaSupported(const FcChainArgs& a, int rows, int cn, const char** why);
+cudaError_t launchFcTma(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s);
 
 // ------------------------------------------------------------------ KRU
 struct KruArgs {

@@ -322,7 +322,11 @@ std::string Mapping::describe() const {
       if (fused && fcKind == 1) os << "registers rows=" << rows;
       else if (fused)
         os << "cluster rows=" << rows << " cn=" << cn << " threads=" << threads
-           << (fcLoads == 1 ? " loads=bulk" : fcLoads == 2 ? " loads=cp.async" : fcLoads == 3 ? " loads=cp.async/1" : "");
+           << (fcLoads == 1   ? " loads=bulk"
+               : fcLoads == 2 ? " loads=cp.async"
+               : fcLoads == 3 ? " loads=cp.async/1"
+               : fcLoads == 4 ? " loads=tma-chunks"
+                              : "");
       else os << "per-layer " << k::gemmVariant(gemmVariant).name << " threads=" << gemmThreads;
       break;
     case Family::Kru3: os << "fused dchunk=" << dchunk << " threads=" << threads; break;
@@ -510,10 +514,11 @@ Mapping decode(const Problem& p, const MappingOptions& o, int math) {
       m.fused = true;
       m.rows = o.tileSizes.empty() ? 1 : static_cast<int>(o.tileSizes[0]);
       m.cn = o.tileSizes.size() < 2 ? 1 : static_cast<int>(o.tileSizes[1]);
-      // tile_sizes[2]: 1 = cluster kernel, automatic loads; 3 / 4 = cluster
-      // kernel with bulk-copy / cp.async loads
-      if (o.tileSizes.size() > 2 && (o.tileSizes[2] == 3 || o.tileSizes[2] == 4 || o.tileSizes[2] == 5))
-        m.fcLoads = o.tileSizes[2] == 3 ? 1 : o.tileSizes[2] == 4 ? 2 : 3;
+      // tile_sizes[2]: 1 = cluster kernel, automatic loads; 3 / 4 / 5 = cluster
+      // kernel with bulk-copy / chunked cp.async / one-chunk cp.async loads;
+      // 6 = layer 0 by TMA tensor copies in reduction chunks (fc_tma.cu)
+      if (o.tileSizes.size() > 2 && o.tileSizes[2] >= 3 && o.tileSizes[2] <= 6)
+        m.fcLoads = static_cast<int>(o.tileSizes[2]) - 2;
       if (o.tileSizes.size() > 2 && o.tileSizes[2] == 2) {
         // tile_sizes[2] == 2: register chains, tile_sizes[0] rows per CTA
         m.fcKind = 1;
@@ -543,7 +548,14 @@ Mapping decode(const Problem& p, const MappingOptions& o, int math) {
         a.L[l].out = p.fc.layers[l].out;
         a.L[l].kred = p.fc.layers[l].kred;
       }
-      if (k::fcChainSmem(a, m.rows, m.cn) > 227 * 1024) invalid("fused FC chain exceeds the shared-memory capacity");
+      if (m.fcLoads == 4) {
+        a.ldi = p.fc.ldi;
+        for (int l = 0; l < a.layers; ++l) a.L[l].ldw = p.fc.layers[l].ldw;
+        const char* why = nullptr;  // (null pointers pass the alignment checks)
+        if (!k::fcTmaSupported(a, m.rows, m.cn, &why)) invalid(why);
+      } else if (k::fcChainSmem(a, m.rows, m.cn) > 227 * 1024) {
+        invalid("fused FC chain exceeds the shared-memory capacity");
+      }
       break;
     }
     case Family::Kru3: {
@@ -828,7 +840,7 @@ GenePools genePools(const Problem& p, int math) {
       if (p.family == Family::FcChain) {
         g.tile0 = {1, 2, 4, 8, 16, 32, 64};
         g.tile1 = {1, 2, 4, 8, 16, 32, 64};
-        g.tile2 = {1, 2, 3, 4, 16, 32, 64};  // fused: 1 = cluster kernel, 2 = register chains, 3/4 = cluster loads
+        g.tile2 = {1, 2, 3, 4, 6, 16, 32, 64};  // fused: 1 = cluster kernel, 2 = register chains, 3/4/6 = loads
         g.tx = {4, 8, 16, 32, 64, 128, 256, 512};
         g.fusion = {Fusion::Max, Fusion::Min};
       }

@@ -89,7 +89,8 @@ struct Mapping {
   // FcChain
   bool fused = true;
   int fcKind = 0;  // fused: 0 = cluster kernel (fc_chain.cu), 1 = register chains (fc_regs.cu)
-  int fcLoads = 0;  // cluster kernel loads: 0 automatic, 1 bulk copies, 2 cp.async (chunked), 3 cp.async
+  int fcLoads = 0;  // cluster kernel loads: 0 automatic, 1 bulk copies, 2 cp.async (chunked), 3 cp.async,
+                    // 4 layer 0 by TMA tensor copies in reduction chunks (fc_tma.cu)
   int rows = 1, cn = 1, threads = 128;
   // Kru3
   int dchunk = 16;

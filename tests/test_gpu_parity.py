@@ -176,6 +176,33 @@ def test_fc_chain_cluster_variants(engine, oracle, golden, rows, cn, threads):
     assert ran >= 3
 
 
+@pytest.mark.parametrize("rows,cn,threads", [(8, 8, 128), (4, 8, 64), (8, 4, 256), (3, 3, 96), (16, 8, 128),
+                                             (1, 1, 64), (8, 16, 64), (8, 8, 64), (2, 2, 32)])
+def test_fc_tma_variants(engine, oracle, golden, rows, cn, threads):
+    """The cluster kernel with layer 0 streamed in by TMA tensor copies in
+    256-step chunks (fc_tma.cu, tile_sizes[2] == 6): ragged rows (zero-filled
+    boxes), column slices past the layer width, the K % 32 tail box, several
+    passes per CTA when threads < rows x columns, non-portable clusters."""
+    from paper_1802_04730_b200 import TcError
+    ran = 0
+    for name in ["2fcrelu_small", "mlp3_small", "mlp3_paper", "mlp1_ragged", "mlp1_small", "2fcrelu_paper",
+                 "mlp1_paper"]:
+        case, ins, seeded = case_inputs(oracle, golden, name)
+        o = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0,
+             "shared_memory_budget": 49152, "thread_shape": [threads, 1, 1], "tile_sizes": [rows, cn, 6],
+             "unroll_copy_shared": False, "unroll_factor": 1, "use_private": False, "use_shared": True}
+        try:
+            got, h = run_on_gpu(engine, case["def"], ins, seeded, options=o)
+        except TcError as e:
+            assert e.kind == "MappingInvalid", str(e)
+            continue
+        assert "tma-chunks" in engine.describe(h)["kernel"]
+        ran += 1
+        for k, rec in case["outputs"].items():
+            assert_exact(oracle, f"{name}/tma{rows}x{cn}x{threads}", k, got[k], rec["fnv"])
+    assert ran >= 5
+
+
 @pytest.mark.parametrize("rows", [1, 2, 4])
 def test_fc_regs_variants(engine, oracle, golden, rows):
     """Register-resident FC chains (fc_regs.cu, tile_sizes[2] == 2) at 1, 2 and
