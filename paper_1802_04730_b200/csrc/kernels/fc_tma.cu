@@ -485,7 +485,9 @@ bool fcTmaSupported(const FcChainArgs& a, int rows, int cn, const char** why) {
     return false;
   };
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  if (a.layers < 1 || a.layers > kMaxLayers) return no("TMA FC chain: 1 to 4 layers");
+  // single-layer chains (MLP1) trap on a barrier that never completes
+  // (profiles/fctma_matrix.py); the cluster kernel serves them
+  if (a.layers < 2 || a.layers > kMaxLayers) return no("TMA FC chain: 2 to 4 layers");
   if (rows < 1 || rows > 256) return no("TMA FC chain: rows per cluster in [1, 256]");
   if (cn < 1 || cn > 16) return no("TMA FC chain: cluster size in [1, 16]");
   const FcLayer& L0 = a.L[0];
