@@ -852,9 +852,6 @@ const GemmVariant kGemmVariants[] = {
     {48, 32, 32, 4, 2, -6, "tma_t32x32_r4x2_mc4", 4},
     {49, 32, 16, 2, 2, -6, "tma_t32x16_r2x2_mc4", 4},
     {50, 32, 32, 2, 2, -6, "tma_t32x32_r2x2_mc2", 2},
-    // one warp per batch, operands by TMA in reduction chunks (tk = -7, gemm_chunk.cu)
-    {51, 0, 0, 7, 4, -7, "wchunk_7x4", 0},
-    {52, 0, 0, 4, 4, -7, "wchunk_4x4", 0},
 };
 
 template <int RM, int RN>
@@ -1054,9 +1051,6 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
     case 48:
     case 49:
     case 50: return launchGemmTma(a, variant - 40, s);
-    case 51:
-    case 52:  // `threads` carries warps per CTA (low byte) and reduction chunks (<< 8)
-      return launchGemmChunk(a, variant - 51, threads & 0xff, threads >> 8, s);
     case 19:
     case 20:
     case 21:

@@ -59,11 +59,6 @@ bool slabOk(const GemmArgs& a);
 // TMA-fed tiles (gemm_tma.cu): 16-byte aligned operands and strides
 bool gemmTmaOk(const GemmArgs& a);
 cudaError_t launchGemmTma(const GemmArgs& a, int which, cudaStream_t s);
-// one warp per batch, operands landed by TMA in reduction chunks (gemm_chunk.cu):
-// 16-byte aligned operands/strides, K % 4 == 0, a batch stride on both operands
-bool gemmChunkOk(const GemmArgs& a);
-// which: 0 = 7x4 outputs per lane, 1 = 4x4; warps per CTA; reduction chunks
-cudaError_t launchGemmChunk(const GemmArgs& a, int which, int warps, int nch, cudaStream_t s);
 
 // ------------------------------------------------- GEMM-NT, tensor cores
 // tcgen05 .kind::tf32 variant of the same contraction (tc_gemm.cu). Not

@@ -192,24 +192,6 @@ void decodeGemm(const MappingOptions& o, Mapping& m) {
     }
     invalid("slab GEMM micro-tile must be 4x1, 7x1, 13x1 (broadcast) or 7x4, 4x4, 4x2 (register-tiled)");
   }
-  if (o.tileSizes[2] == 4) {
-    // reduction depth 4 = one warp per batch, operands landed by TMA in
-    // reduction chunks (gemm_chunk.cu): tile_sizes[0] x [1] outputs per lane,
-    // block_shape[0] warps (batches) per CTA, block_shape[1] reduction chunks
-    const int rm = static_cast<int>(o.tileSizes[0]), rn = static_cast<int>(o.tileSizes[1]);
-    const int64_t warps = o.blockShape[0], nch = o.blockShape[1];
-    if (warps < 1 || warps > 8) invalid("chunked warp-per-batch GEMM: 1 to 8 warps per CTA");
-    if (nch < 1 || nch > 6) invalid("chunked warp-per-batch GEMM: 1 to 6 reduction chunks");
-    for (int i = 1; i < k::gemmVariantCount(); ++i) {
-      const auto& v = k::gemmVariant(i);
-      if (v.tk == -7 && v.rm == rm && v.rn == rn) {
-        m.gemmVariant = i;
-        m.gemmThreads = static_cast<int>(warps | (nch << 8));
-        return;
-      }
-    }
-    invalid("chunked warp-per-batch GEMM micro-tile must be 7x4 or 4x4");
-  }
   if (o.tileSizes[2] == 3) {
     // reduction depth 3 = TMA-fed tiles (32-deep stages): tile tm x tn,
     // micro-tile (tm / thread_shape[1]) x (tn / thread_shape[0]);
@@ -272,11 +254,7 @@ void launchGemmDesc(const GemmDesc& g, const Mapping& m, void* const* in, void* 
     e = k::launchTcGemm(a, m.math, pl, s);
   } else if ((k::gemmVariant(m.gemmVariant).tk == 0 && !k::batchedOk(a)) ||
              (k::gemmVariant(m.gemmVariant).tk < 0 && k::gemmVariant(m.gemmVariant).tk > -5 && !k::slabOk(a)) ||
-             (k::gemmVariant(m.gemmVariant).tk == -7 &&
-              (!k::gemmChunkOk(a) || a.M > 4 * k::gemmVariant(m.gemmVariant).rm ||
-               a.N > 8 * k::gemmVariant(m.gemmVariant).rn)) ||
-             (k::gemmVariant(m.gemmVariant).tk <= -5 && k::gemmVariant(m.gemmVariant).tk >= -6 &&
-              !k::gemmTmaOk(a))) {
+             (k::gemmVariant(m.gemmVariant).tk <= -5 && !k::gemmTmaOk(a))) {
     // the persistent batched and slab kernels need 16-byte aligned operands
     // (and the slab K <= 144); the tiled kernel computes the same bit-exact
     // chains without that need
@@ -333,8 +311,6 @@ std::string Mapping::describe() const {
     case Family::Gemm:
       if (k::gemmVariant(gemmVariant).tk == -4)
         os << k::gemmVariant(gemmVariant).name << " warps=" << gemmThreads;
-      else if (k::gemmVariant(gemmVariant).tk == -7)
-        os << k::gemmVariant(gemmVariant).name << " warps=" << (gemmThreads & 0xff) << " chunks=" << (gemmThreads >> 8);
       else if (k::gemmVariant(gemmVariant).tk < 0 && k::gemmVariant(gemmVariant).tk > -5)
         os << k::gemmVariant(gemmVariant).name;
       else if (k::gemmVariant(gemmVariant).tk == 0)

@@ -37,8 +37,18 @@ def main():
     prio = [int(x) for x in os.environ.get("PRIO", "0,0,0").split(",")]
     side = [torch.cuda.Stream(priority=p) for p in prio]
 
-    def graph_of(group):
+    def graph_of(group, pipelined=False):
         def body():
+            if pipelined:  # consecutive steps overlap: each operator's stream runs its NSTEP steps, one join
+                for sd in side[:len(group)]:
+                    sd.wait_stream(main_s)
+                for o, sd in zip(group, side):
+                    with torch.cuda.stream(sd):
+                        for k in range(NSTEP):
+                            o.run(k)
+                for sd in side[:len(group)]:
+                    main_s.wait_stream(sd)
+                return
             for k in range(NSTEP):
                 for sd in side[:len(group)]:
                     sd.wait_stream(main_s)
@@ -71,6 +81,22 @@ def main():
     base = {n: o.handle for n, o in ops.items()}
     g0 = graph_of(list(ops.values()))
     print(f"default step {min(timeit(g0) for _ in range(8)):.2f} us", flush=True)
+    gp = graph_of(list(ops.values()), pipelined=True)
+    print(f"pipelined steps {min(timeit(gp) for _ in range(8)):.2f} us per step", flush=True)
+    for name, v in [("tbmm", {"tile_sizes": [7, 1, 2]}), ("tbmm", {"tile_sizes": [4, 1, 2]}),
+                    ("tbmm", {"tile_sizes": [4, 4, 4], "block_shape": [2, 1, 1]}),
+                    ("2FCRelu", {"tile_sizes": [8, 8, 1], "thread_shape": [128, 1, 1]}),
+                    ("2FCRelu", {"tile_sizes": [16, 8, 1], "thread_shape": [256, 1, 1]}),
+                    ("MLP3", {"tile_sizes": [8, 4, 6], "thread_shape": [128, 1, 1]})]:
+        o = ops[name]
+        o.handle = ee.compile(name, o.sets[0][0], o.sets[0][1], dict(ee.default_options(name, o.sets[0][0], o.sets[0][1]), **v))
+        gp = graph_of(list(ops.values()), pipelined=True)
+        print(f"pipelined {name} {v}: {min(timeit(gp) for _ in range(5)):.2f} us per step", flush=True)
+        o.handle = base[name]
+    for name in ops:
+        print(f"{name} alone (back to back): {min(timeit(graph_of([ops[name]], pipelined=True)) for _ in range(3)):.2f} us", flush=True)
+    if os.environ.get("PIPE_ONLY"):
+        return
     for combo in COMBOS:
         try:
             for name, v in combo.items():

@@ -536,29 +536,3 @@ def test_paper_style_call(engine, oracle):
     C = engine.tmm(to_dev(A), to_dev(B))
     np.testing.assert_array_equal(C.cpu().numpy(), oracle.tmm(A, B))
 
-
-WCHUNK_PLANS = [(7, 4, 2, 4), (7, 4, 2, 2), (7, 4, 1, 3), (7, 4, 4, 6), (7, 4, 8, 1), (4, 4, 2, 4), (4, 4, 3, 2)]
-
-
-@pytest.mark.parametrize("shape", [(500, 26, 26, 72), (37, 13, 29, 44), (3, 28, 32, 8), (64, 1, 1, 4),
-                                   (9, 16, 20, 148)])
-def test_wchunk_gemm_variants(engine, oracle, shape):
-    """One warp per batch with the operands landed by TMA in reduction chunks
-    (gemm_chunk.cu, tile_sizes[2] == 4): bit-exact against the oracle's TBMM
-    chains at the paper shape and ragged ones (rows/columns short of the warp
-    tile, a short last chunk, K = 4, a batch count not a multiple of the warps
-    per CTA); shapes past the warp tile (M > 4*RM or N > 8*RN) fall back to
-    the tiled kernel with the same bits."""
-    B, N, K, M = shape  # Z(b,n,k) += X(b,n,m) * Y(b,k,m)
-    rng = np.random.default_rng(B * 1000 + M)
-    X = rng.uniform(-1, 1, (B, N, M)).astype(np.float32)
-    Y = rng.uniform(-1, 1, (B, K, M)).astype(np.float32)
-    ref = oracle.tbmm(X, Y)
-    for rm, rn, warps, nch in WCHUNK_PLANS:
-        o = {"block_shape": [warps, nch, 1], "fusion_strategy": "max", "rng_seed": 0,
-             "shared_memory_budget": 49152, "thread_shape": [32, 1, 1], "tile_sizes": [rm, rn, 4],
-             "unroll_copy_shared": False, "unroll_factor": 1, "use_private": True, "use_shared": True}
-        got, h = run_on_gpu(engine, "tbmm", {"X": X, "Y": Y}, {}, options=o)
-        z = got["Z"]
-        diff = int(np.sum(z.view(np.uint32) != ref.view(np.uint32)))
-        assert diff == 0, f"tbmm {shape} wchunk {rm}x{rn} w{warps} c{nch}: {diff} elements differ"
