@@ -179,6 +179,18 @@ __device__ __forceinline__ void mmaTf32(uint32_t tmemD, uint64_t a, uint64_t b, 
       "l"(a), "l"(b), "r"(idesc), "r"(accum)
       : "memory");
 }
+// the same MMA with A read from TMEM (lane = row, one 32-bit column per k)
+__device__ __forceinline__ void mmaTf32Tmem(uint32_t tmemD, uint32_t tmemA, uint64_t b, uint32_t idesc,
+                                            uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmemD),
+      "r"(tmemA), "l"(b), "r"(idesc), "r"(accum)
+      : "memory");
+}
 // one lane of the (converged) warp: issue tcgen05.mma from a warp-uniform
 // branch (elect.sync) instead of `lane == 0`, so the operands stay in uniform
 // registers and each MMA issues without a per-lane waterfall (~40 vs ~100
@@ -215,7 +227,25 @@ __device__ __forceinline__ void tmemLoad16(uint32_t taddr, float* v) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmemLoadWait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// thread i of the warp writes lane (base lane + i), columns c..c+31
+__device__ __forceinline__ void tmemStore32(uint32_t taddr, const float* v) {
+  const uint32_t* r = reinterpret_cast<const uint32_t*>(v);
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmemStoreWait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// the tf32 value a tcgen05 .kind::tf32 MMA takes from an fp32 operand: the top
+// 19 bits (round toward zero). The 3xTF32 split of every kernel is
+// hi = rzTf32(x) (what the MMA would read from x itself), lo = toTf32(x - hi)
+// (x - hi is exact in fp32), so a kernel may feed raw x as hi.
+__device__ __forceinline__ float rzTf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 // fp32 → tf32 (round to nearest, ties away), result in a 32-bit container with the low 13 bits zero
 __device__ __forceinline__ float toTf32(float x) {
   uint32_t r;

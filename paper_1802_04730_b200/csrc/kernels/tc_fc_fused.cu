@@ -61,12 +61,12 @@ __device__ __forceinline__ uint32_t swOff(int row, int k) {
 __device__ __forceinline__ void splitPlane(float* hi, float* lo, int bytes, int tid, int nthreads) {
   float4* h4 = reinterpret_cast<float4*>(hi);
   float4* l4 = reinterpret_cast<float4*>(lo);
+  // hi stays the landed fp32 plane (the MMA reads its top 19 bits = rzTf32)
   for (int j = tid; j < bytes / 16; j += nthreads) {
     const float4 x = h4[j];
-    float4 h, l;
-    h.x = toTf32(x.x); h.y = toTf32(x.y); h.z = toTf32(x.z); h.w = toTf32(x.w);
-    l.x = toTf32(x.x - h.x); l.y = toTf32(x.y - h.y); l.z = toTf32(x.z - h.z); l.w = toTf32(x.w - h.w);
-    h4[j] = h;
+    float4 l;
+    l.x = toTf32(x.x - rzTf32(x.x)); l.y = toTf32(x.y - rzTf32(x.y));
+    l.z = toTf32(x.z - rzTf32(x.z)); l.w = toTf32(x.w - rzTf32(x.w));
     l4[j] = l;
   }
 }
@@ -208,10 +208,10 @@ __global__ void __launch_bounds__(kThreadsFc, 1)
         if (!last && n < p.K[l + 1]) {  // layer l+1's A operand (its K = this N)
           const uint32_t off = swOff(row, n);
           if constexpr (X3) {
-            float4 h, lo;
-            h.x = toTf32(o.x); h.y = toTf32(o.y); h.z = toTf32(o.z); h.w = toTf32(o.w);
-            lo.x = toTf32(o.x - h.x); lo.y = toTf32(o.y - h.y); lo.z = toTf32(o.z - h.z); lo.w = toTf32(o.w - h.w);
-            *reinterpret_cast<float4*>(aHi + off) = h;
+            float4 lo;  // hi: o itself (the MMA reads rzTf32(o))
+            lo.x = toTf32(o.x - rzTf32(o.x)); lo.y = toTf32(o.y - rzTf32(o.y));
+            lo.z = toTf32(o.z - rzTf32(o.z)); lo.w = toTf32(o.w - rzTf32(o.w));
+            *reinterpret_cast<float4*>(aHi + off) = o;
             *reinterpret_cast<float4*>(aLo + off) = lo;
           } else {
             *reinterpret_cast<float4*>(aHi + off) = o;

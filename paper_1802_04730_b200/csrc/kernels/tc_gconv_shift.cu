@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
       const int ks = tap * kcb + (c >> 3), half = (c >> 2) & 1, el = c & 3;
       auto at = [&](int r) { return bb + ks * 32 * NB + half * 16 * NB + (r >> 3) * 128 + (r & 7) * 16 + el * 4; };
       if constexpr (X3) {
-        const float h = toTf32(v);
+        const float h = rzTf32(v);
         *reinterpret_cast<float*>(at(f)) = h;
         *reinterpret_cast<float*>(at(F + f)) = toTf32(v - h);
       } else {
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
           const uint32_t dst = hiP + (uint32_t)(((cb * HP) + pg * 4 + j) * 16);
           if constexpr (X3) {
             float4 h, l;
-            h.x = toTf32(v.x); h.y = toTf32(v.y); h.z = toTf32(v.z); h.w = toTf32(v.w);
+            h.x = rzTf32(v.x); h.y = rzTf32(v.y); h.z = rzTf32(v.z); h.w = rzTf32(v.w);
             l.x = toTf32(v.x - h.x); l.y = toTf32(v.y - h.y); l.z = toTf32(v.z - h.z); l.w = toTf32(v.w - h.w);
             sts128(dst, h);
             sts128(dst + (uint32_t)planeF * 4, l);
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(kThreadsSh, 1)
         for (int e = b; e < planeF / 4; e += kBuildersSh) {
           const float4 x = hi[e];
           float4 h, l;
-          h.x = toTf32(x.x); h.y = toTf32(x.y); h.z = toTf32(x.z); h.w = toTf32(x.w);
+          h.x = rzTf32(x.x); h.y = rzTf32(x.y); h.z = rzTf32(x.z); h.w = rzTf32(x.w);
           l.x = toTf32(x.x - h.x); l.y = toTf32(x.y - h.y); l.z = toTf32(x.z - h.z); l.w = toTf32(x.w - h.w);
           hi[e] = h;
           lo[e] = l;

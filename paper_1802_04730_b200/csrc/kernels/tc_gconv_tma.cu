@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gconv_nhwc_kernel(const Params
       const int atom = k >> 5, j = (k & 31) >> 2, el = k & 3, rg = f >> 3, r = f & 7;
       const int off = atom * F * 128 + rg * 1024 + r * 128 + ((j ^ r) << 4) + el * 4;
       if constexpr (X3) {
-        const float h = toTf32(v);
+        const float h = rzTf32(v);
         *reinterpret_cast<float*>(bHi + off) = h;
         *reinterpret_cast<float*>(bLo + off) = toTf32(v - h);
       } else {
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gconv_nhwc_kernel(const Params
       if constexpr (X3) {
         float4* hp = reinterpret_cast<float4*>(aSt + st * C_::kStageBytes + chunk);
         float4 x = *hp, hh, ll;
-        hh.x = toTf32(x.x); hh.y = toTf32(x.y); hh.z = toTf32(x.z); hh.w = toTf32(x.w);
+        hh.x = rzTf32(x.x); hh.y = rzTf32(x.y); hh.z = rzTf32(x.z); hh.w = rzTf32(x.w);
         ll.x = toTf32(x.x - hh.x); ll.y = toTf32(x.y - hh.y); ll.z = toTf32(x.z - hh.z); ll.w = toTf32(x.w - hh.w);
         *hp = hh;
         *reinterpret_cast<float4*>(aSt + st * C_::kStageBytes + kStep + chunk) = ll;

@@ -10,10 +10,15 @@
 // Structure (one CTA = one 128 x BN output tile of one K split):
 //   warp 0       TMA producer: 128x32 A and BNx32 B fp32 boxes, SWIZZLE_128B,
 //                into an S-stage shared-memory ring (mbarrier full/empty);
-//   warps 4..7   (3xTF32 only) split each landed fp32 tile in place into
-//                hi = tf32(x) and lo = tf32(x - hi) (a second buffer);
+//   warps 4..7   (3xTF32 only) split each landed fp32 k-block: A's hi =
+//                rz(x) and lo = tf32(x - rz(x)) go to TMEM (the MMA's A
+//                operand, so the tensor core re-reads only B from shared
+//                memory); B's hi is the landed tile itself (the MMA uses the
+//                top 19 bits of fp32 operands, rzTf32), its lo goes to a
+//                second buffer;
 //   warp 1       one elected lane issues tcgen05.mma.kind::tf32 (M=128,
-//                N=BN, K=8 per instruction; 3xTF32: lo*hi + hi*lo + hi*hi)
+//                N=BN, K=8 per instruction; 3xTF32: lo*hi + hi*lo + hi*hi,
+//                A from TMEM)
 //                into a TMEM accumulator, tcgen05.commit frees the stage;
 //   warp 2       allocates / frees the TMEM columns;
 //   warps 4..7   epilogue: tcgen05.ld the accumulator (lane = row) into a
@@ -60,18 +65,29 @@ template <int BN, bool X3>
 struct TcCfg {
   static constexpr int kABytes = kBM * kBK * 4;
   static constexpr int kBBytes = BN * kBK * 4;
-  static constexpr int kStage = (kABytes + kBBytes) * (X3 ? 2 : 1);
+  // a stage: the landed fp32 A and B k-blocks (+ B's lo half for 3xTF32;
+  // A's hi and lo halves go to TMEM, the MMA's A operand there)
+  static constexpr int kStage = kABytes + kBBytes + (X3 ? kBBytes : 0);
   static constexpr int kPartLd = BN + 4;  // partial tile row stride (floats)
   static constexpr int kPartBytes = kBM * kPartLd * 4;
   static constexpr int kBudget = 200 * 1024;
-  static constexpr int kStagesRaw = kBudget / kStage;
+  static constexpr int kAccCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int kStagesSm = kBudget / kStage;
+  // 3xTF32: every stage owns 2 x 32 TMEM columns (A hi | A lo) after the accumulator
+  static constexpr int kStagesTm = X3 ? (512 - kAccCols) / (2 * kBK) : 8;
+  static constexpr int kStagesRaw = kStagesSm < kStagesTm ? kStagesSm : kStagesTm;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kRing = kStages * kStage > kPartBytes ? kStages * kStage : kPartBytes;
   static constexpr int kSmem = 1024 + kRing + 256;
-  static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int kTmemCols = X3 ? 512 : kAccCols;
   static_assert(kStages >= 2, "stage ring too small");
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 is a multiple of 16 in [16, 256]");
 };
+
+// the low part of the 3xTF32 split (sm100.cuh rzTf32): the MMA takes hi from
+// the raw fp32 tile itself
+__device__ __forceinline__ float lo1(float x) { return toTf32(x - rzTf32(x)); }
+__device__ __forceinline__ float4 loPart(float4 x) { return make_float4(lo1(x.x), lo1(x.y), lo1(x.z), lo1(x.w)); }
 
 template <int BN, bool X3>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -82,8 +98,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   auto aBig = [&](int s) { return sm + s * Cfg::kStage; };
   auto bBig = [&](int s) { return sm + s * Cfg::kStage + Cfg::kABytes; };
-  auto aLo = [&](int s) { return sm + s * Cfg::kStage + Cfg::kABytes + Cfg::kBBytes; };
-  auto bLo = [&](int s) { return sm + s * Cfg::kStage + 2 * Cfg::kABytes + Cfg::kBBytes; };
+  auto bLo = [&](int s) { return sm + s * Cfg::kStage + Cfg::kABytes + Cfg::kBBytes; };
+  // 3xTF32: TMEM columns of stage s's A operand, hi at +0, lo at +kBK
+  auto aCol = [&](int s) { return static_cast<uint32_t>(Cfg::kAccCols + s * 2 * kBK); };
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + Cfg::kRing);
   uint64_t* conv = full + S;
   uint64_t* empty = conv + S;
@@ -143,10 +160,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
           const uint32_t acc = (i | kk) != 0;
           if constexpr (X3) {
-            const uint32_t al = smem(aLo(s)), bl = smem(bLo(s));
-            mmaTf32(tmem, descSw128(al + off), descSw128(bbg + off), idesc, acc);
-            mmaTf32(tmem, descSw128(ab + off), descSw128(bl + off), idesc, 1);
-            mmaTf32(tmem, descSw128(ab + off), descSw128(bbg + off), idesc, 1);
+            // A from TMEM (lane = row, column = k): the tensor core re-reads
+            // only B from shared memory for the three products
+            const uint32_t bl = smem(bLo(s)), ahi = tmem + aCol(s) + kk * 8, alo = ahi + kBK;
+            mmaTf32Tmem(tmem, alo, descSw128(bbg + off), idesc, acc);
+            mmaTf32Tmem(tmem, ahi, descSw128(bl + off), idesc, 1);
+            mmaTf32Tmem(tmem, ahi, descSw128(bbg + off), idesc, 1);
           } else {
             mmaTf32(tmem, descSw128(ab + off), descSw128(bbg + off), idesc, acc);
           }
@@ -161,24 +180,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = 0; i < nk; ++i) {
         const int s = i % S;
         mbarWait(&full[s], (i / S) & 1, 4);
-        float4* a = reinterpret_cast<float4*>(aBig(s));
-        float4* al = reinterpret_cast<float4*>(aLo(s));
-        for (int j = et; j < Cfg::kABytes / 16; j += 128) {
-          float4 x = a[j], h, l;
-          h.x = toTf32(x.x); h.y = toTf32(x.y); h.z = toTf32(x.z); h.w = toTf32(x.w);
-          l.x = toTf32(x.x - h.x); l.y = toTf32(x.y - h.y); l.z = toTf32(x.z - h.z); l.w = toTf32(x.w - h.w);
-          a[j] = h;
-          al[j] = l;
+        // A: thread `row` reads its landed fp32 row of the k-block (128-byte
+        // swizzled: 16-byte unit j at j ^ (row & 7)) and writes hi = rz(x)
+        // and lo = tf32(x - rz(x)) into its TMEM lane (warp w % 4 owns lanes
+        // 32(w % 4)..+31); x - rz(x) is exact in fp32
+        {
+          const int row = et;
+          const float4* ar = reinterpret_cast<const float4*>(aBig(s) + row * 128);
+          float hi[kBK], lo[kBK];
+#pragma unroll
+          for (int j = 0; j < kBK / 4; ++j) {
+            const float4 x = ar[j ^ (row & 7)];
+            const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              hi[4 * j + e] = rzTf32(xs[e]);
+              lo[4 * j + e] = toTf32(xs[e] - hi[4 * j + e]);
+            }
+          }
+          const uint32_t tl = tmem + (static_cast<uint32_t>((warp - 4) * 32) << 16) + aCol(s);
+          tmemStore32(tl, hi);
+          tmemStore32(tl + kBK, lo);
         }
-        float4* bv = reinterpret_cast<float4*>(bBig(s));
+        // B: hi is the landed tile itself (the MMA reads rzTf32 of it); lo to
+        // the stage's second buffer
+        const float4* bv = reinterpret_cast<const float4*>(bBig(s));
         float4* bl = reinterpret_cast<float4*>(bLo(s));
-        for (int j = et; j < Cfg::kBBytes / 16; j += 128) {
-          float4 x = bv[j], h, l;
-          h.x = toTf32(x.x); h.y = toTf32(x.y); h.z = toTf32(x.z); h.w = toTf32(x.w);
-          l.x = toTf32(x.x - h.x); l.y = toTf32(x.y - h.y); l.z = toTf32(x.z - h.z); l.w = toTf32(x.w - h.w);
-          bv[j] = h;
-          bl[j] = l;
-        }
+        for (int j = et; j < Cfg::kBBytes / 16; j += 128) bl[j] = loPart(bv[j]);
+        tmemStoreWait();
+        tcFenceBefore();
         fenceProxyAsyncSmem();
         mbarArrive(&conv[s]);
       }

@@ -89,14 +89,14 @@ __global__ void __launch_bounds__(kThreadsKru) tc_kru3_kernel(const KruArgs a) {
   __syncthreads();
   if constexpr (X3) {  // split: A1 lo plane; B rows [n, 2n) = lo of rows [0, n)
     for (int e = tid; e < 256 * kR; e += kThreadsKru) {
-      const float x = A1[e], h = toTf32(x);
+      const float x = A1[e], h = rzTf32(x);
       A1[e] = h;
       A1[256 * kR + e] = toTf32(x - h);
     }
     auto splitB = [&](float* B, int n) {
       for (int e = tid; e < n * kR; e += kThreadsKru) {
         const int row = e / kR, k = e - row * kR;
-        const float x = B[kmIdx(row, k, 2 * n)], h = toTf32(x);
+        const float x = B[kmIdx(row, k, 2 * n)], h = rzTf32(x);
         B[kmIdx(row, k, 2 * n)] = h;
         B[kmIdx(n + row, k, 2 * n)] = toTf32(x - h);
       }
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kThreadsKru) tc_kru3_kernel(const KruArgs a) {
   };
   auto putA = [&](float* A, int rows, int row, int k, float x) {  // next step's A (hi [, lo])
     if constexpr (X3) {
-      const float h = toTf32(x);
+      const float h = rzTf32(x);
       A[kmIdx(row, k, rows)] = h;
       A[rows * kR + kmIdx(row, k, rows)] = toTf32(x - h);
     } else {

@@ -8,9 +8,11 @@ feed the tensor cores, accumulated in fp64:
   tf32    the MMA reads fp32 operands straight from shared memory and uses
           their top 19 bits (the low 13 mantissa bits are ignored, i.e.
           round toward zero); product sums in fp64.
-  3xtf32  hi = cvt.rna.tf32(x), lo = cvt.rna.tf32(x - hi) (sm100.cuh
-          toTf32); the kernels issue lo*hi + hi*lo + hi*hi into one fp32
-          accumulator (tc_gemm.cu); lo*lo is dropped. Product sums in fp64.
+  3xtf32  hi = the top 19 bits of x (rz: what the MMA itself takes from a
+          raw fp32 operand, so the kernels may feed x as hi), lo =
+          cvt.rna.tf32(x - hi) (sm100.cuh rzTf32 / toTf32); the kernels
+          issue lo*hi + hi*lo + hi*hi into one fp32 accumulator
+          (tc_gemm.cu); lo*lo is dropped. Product sums in fp64.
 
 What separates a kernel's output from the emulation is then only the fp32
 rounding of the accumulator (~K * 2^-24 of the partial-sum magnitude per MMA
@@ -37,7 +39,7 @@ def tf32_rna(x):
 
 def split3(x):
     x = np.asarray(x, np.float32)
-    hi = tf32_rna(x)
+    hi = tf32_rz(x)
     lo = tf32_rna((x - hi).astype(np.float32))  # x - hi is exact in fp32
     return hi.astype(np.float64), lo.astype(np.float64)
 
