@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     if (p.bulk == 2 && l > 0) asyncWait(NL - 1 - l);
     FC_STAMP(3 + 3 * l);
     if (!last && l == 0 && cn > 1) asm volatile("barrier.cluster.wait;" ::: "memory");
+    if (l == 0) FC_STAMP(20);
     const int nchains = R * cols;
     for (int base = 0; base < nchains; base += T) {
       // one (row, column) chain per thread and pass, row fastest; idle

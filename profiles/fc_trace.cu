@@ -53,7 +53,7 @@ static void run(const char* label, FcChainArgs a, int rows, int cn, int threads)
   printf("%s: %s  %.2f us  (%d CTAs)\n", label, cudaGetErrorString(err), ms * 1e3, nblk);
   const char* names[24] = {"start", "bar_init", "copies_issued", "L0_data", "L0_done", "init_fence", "L1_data",
                            "L1_done", "cta_sync", "L2_data", "L2_done", "cl_arrive", "expects", "-", "-", "end",
-                           "L0_chain", "L1_chain", "L2_chain", "L3_chain", "-", "-", "-", "-"};
+                           "L0_chain", "L1_chain", "L2_chain", "L3_chain", "L0_clwait", "-", "-", "-"};
   unsigned long long g0 = ~0ull, g1 = 0;
   for (int b = 0; b < nblk; ++b) {
     if (tr[b][13]) g0 = std::min(g0, tr[b][13]);
@@ -64,7 +64,7 @@ static void run(const char* label, FcChainArgs a, int rows, int cn, int threads)
   std::sort(st.begin(), st.end());
   printf("  globaltimer: first CTA start -> last CTA end %.2f us; CTA start skew median %lld max %lld ns\n",
          (g1 - g0) * 1e-3, st[st.size() / 2], st.back());
-  const int order[] = {1, 5, 8, 11, 12, 2, 3, 16, 4, 6, 17, 7, 9, 18, 10, 19, 15};
+  const int order[] = {1, 5, 8, 11, 12, 2, 3, 20, 16, 4, 6, 17, 7, 9, 18, 10, 19, 15};
   for (int ev : order) {
     std::vector<long long> d;
     for (int b = 0; b < nblk; ++b)
