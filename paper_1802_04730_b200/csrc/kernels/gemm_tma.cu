@@ -46,16 +46,6 @@ __device__ __forceinline__ float ldsSw1(uint32_t rowBase, int r, int k) {
   return v;
 }
 
-// multicast tensor copy: the box lands at the same offset in every CTA of
-// ctaMask and completes `bytes` on each one's barrier at the same offset
-__device__ __forceinline__ void tmaLoad3dMc(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar,
-                                            uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
-      "[%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem(bar)), "h"(mask)
-      : "memory");
-}
 // arrive on the mbarrier at the same offset in cluster CTA `rank`
 __device__ __forceinline__ void mbarArriveRemote(uint64_t* bar, uint32_t rank) {
   asm volatile(

@@ -205,6 +205,16 @@ __device__ __forceinline__ void mmaCommit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem(bar))
                : "memory");
 }
+// multicast tensor copy: the box lands at the same offset in every CTA of
+// ctaMask and completes its bytes on each one's barrier at the same offset
+__device__ __forceinline__ void tmaLoad3dMc(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar,
+                                            uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], "
+      "[%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem(bar)), "h"(mask)
+      : "memory");
+}
 // 32 lanes x 32 columns of fp32: thread i of the warp gets lane (base lane + i), columns c..c+31
 __device__ __forceinline__ void tmemLoad32(uint32_t taddr, float* v) {
   uint32_t* r = reinterpret_cast<uint32_t*>(v);
