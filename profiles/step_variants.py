@@ -79,8 +79,18 @@ def main():
         return e0.elapsed_time(e1) * 1e3 / (n * NSTEP)
 
     base = {n: o.handle for n, o in ops.items()}
+    for name, v in bench.STEP_PLANS.items():  # the bench's step plans
+        o = ops[name]
+        o.handle = base[name] = ee.compile(name, o.sets[0][0], o.sets[0][1],
+                                           dict(ee.default_options(name, o.sets[0][0], o.sets[0][1]), **v))
     g0 = graph_of(list(ops.values()))
     print(f"default step {min(timeit(g0) for _ in range(8)):.2f} us", flush=True)
+    import itertools
+    for order in itertools.permutations(list(ops)):
+        g = graph_of([ops[n] for n in order])
+        print(f"fork order {order}: {min(timeit(g) for _ in range(6)):.2f} us", flush=True)
+    if os.environ.get("ORDER_ONLY"):
+        return
     gp = graph_of(list(ops.values()), pipelined=True)
     print(f"pipelined steps {min(timeit(gp) for _ in range(8)):.2f} us per step", flush=True)
     for name, v in [("tbmm", {"tile_sizes": [7, 1, 2]}), ("tbmm", {"tile_sizes": [4, 1, 2]}),
