@@ -139,7 +139,7 @@ __device__ __forceinline__ void stAsyncCluster(const float* local, const uint64_
 // chunk c, so shared-load latency hides behind a full chunk of the chain.
 // Reads up to 32 floats past n (the plan leaves that slack after every
 // operand buffer).
-__device__ __forceinline__ float chainSegment(unsigned xa, unsigned wa, int n, float acc) {
+__device__ __noinline__ float chainSegment(unsigned xa, unsigned wa, int n, float acc) {
   const int nch = n >> 4;
   float4 X0[4], W0[4], X1[4], W1[4];
 #pragma unroll
@@ -178,7 +178,7 @@ __device__ __forceinline__ float chainSegment(unsigned xa, unsigned wa, int n, f
 
 #ifdef TCB_FC_TRACE
 // diagnostic build only (profiles/fc_trace.cu): per-CTA phase timestamps
-__device__ unsigned long long g_fc_trace[1024][24];
+__device__ unsigned long long g_fc_trace[1024][32];
 #define FC_STAMP(ev)                                                                       \
   do {                                                                                     \
     if (threadIdx.x == 0) g_fc_trace[blockIdx.y * gridDim.x + blockIdx.x][ev] = clock64(); \
@@ -204,7 +204,11 @@ __device__ unsigned long long g_fc_trace[1024][24];
 // parameter reads are constant-bank operands the compiler can hoist and
 // overlap. (A runtime layer loop made each layer's reads dependent misses in
 // the cold constant cache; MLP3 6.8 -> 5.3 µs, profiles/fc_trace.cu.)
-template <int NL>
+// LM = p.bulk, the load mode, as a template parameter too: each instance
+// holds only its own load path (the fused kernel is latency-bound and its
+// instruction footprint showed up as ~half of all warp-stall samples,
+// "no instruction", in ncu: profiles/r02_fc_icache.txt)
+template <int NL, int LM>
 __global__ void __launch_bounds__(kFcMaxThreads)
     fc_cluster_kernel(const __grid_constant__ FcChainArgs a, const __grid_constant__ FcPlan p) {
   FC_GSTAMP(13);
@@ -251,7 +255,7 @@ __global__ void __launch_bounds__(kFcMaxThreads)
   // ---- every global load of the kernel is issued up front. A bulk copy
   // costs the issuing thread ~200 cycles, so the copies are dealt round-robin
   // to lane 0 of every warp (copy j -> warp j % warps) and issue in parallel.
-  if (p.bulk == 1) {
+  if (LM == 1) {
     const int warp = tid >> 5, nw = (T + 31) >> 5, lane = tid & 31;
     const unsigned rowBytes = (unsigned)a.L[0].kred * 4u;
     if (tid == 0) {
@@ -273,11 +277,13 @@ __global__ void __launch_bounds__(kFcMaxThreads)
           if (j++ % nw == warp)
             bulkCopy(sm + p.offAct[0] + r * p.ald[0], a.I + (int64_t)(row0 + r) * a.ldi, rowBytes, &bars[0]);
       }
+      FC_STAMP(24);
 #pragma unroll
       for (int l = 0; l < layers; ++l) {
         const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
         if (nc == 0) continue;
         const float* src = a.L[l].W + (int64_t)c0 * a.L[l].ldw;
+        if (l < 4) FC_STAMP(25 + l);
         if (a.L[l].ldw == a.L[l].kred) {  // the slice is one contiguous block
           if (j++ % nw == warp) bulkCopy(sm + p.offW[l], src, (unsigned)(nc * a.L[l].kred * 4), &bars[layers + l]);
         } else {
@@ -291,7 +297,7 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     // input rows past the batch end are zero
     for (int e = tid; e < (R - rows) * p.ald[0]; e += T) sm[p.offAct[0] + rows * p.ald[0] + e] = 0.0f;
     if (rows < R) __syncthreads();
-  } else if (p.bulk == 2) {
+  } else if (LM == 2) {
     // 16-byte cp.async from every thread (a tunable; see planFc)
     // Layer 0 lands in p.nch reduction chunks (its input rows and weight
     // slice, one commit group per chunk), so its chains start on chunk 0
@@ -346,8 +352,8 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     const bool last = l + 1 == layers;
     const int ald = p.ald[l];
     const unsigned actBase = smemAddr(sm + p.offAct[l]), wBase = smemAddr(sm + p.offW[l]);
-    if ((l > 0 && cn > 1) || (l == 0 && p.bulk == 1)) mbarWait(&bars[l], 0, l);
-    if (p.bulk == 1) mbarWait(&bars[layers + l], 0, layers + l);
+    if ((l > 0 && cn > 1) || (l == 0 && LM == 1)) mbarWait(&bars[l], 0, l);
+    if (LM == 1) mbarWait(&bars[layers + l], 0, layers + l);
     // cp.async mode: commit groups in flight after layer l's (or layer-0
     // chunk ch's) group; waiting for that leaves only later groups pending
     auto asyncWait = [&](int pending) {
@@ -362,7 +368,7 @@ __global__ void __launch_bounds__(kFcMaxThreads)
       }
       __syncthreads();  // this thread's copies landed, then everyone's
     };
-    if (p.bulk == 2 && l > 0) asyncWait(NL - 1 - l);
+    if (LM == 2 && l > 0) asyncWait(NL - 1 - l);
     FC_STAMP(3 + 3 * l);
     if (!last && l == 0 && cn > 1) asm volatile("barrier.cluster.wait;" ::: "memory");
     if (l == 0) FC_STAMP(20);
@@ -379,13 +385,14 @@ __global__ void __launch_bounds__(kFcMaxThreads)
         if (q == l) bpre = biasPre[q];  // static register indexing
       float acc = !live ? 0.0f : base == 0 ? bpre : __ldg(L.bias + c0 + c);
       const unsigned xa = actBase + (unsigned)(r * ald) * 4u, wa = wBase + (unsigned)(c * p.wld[l]) * 4u;
-      if (l == 0 && p.bulk == 2) {
+      if (l == 0 && LM == 2) {
         for (int ch = 0; ch < p.nch; ++ch) {  // the chain follows the chunks in
           if (base == 0) asyncWait(p.nch - 1 - ch + NL - 1);
           const int k0 = ch * 4 * p.kc4, n = min(4 * p.kc4, L.kred - k0);
           acc = chainSegment(xa + 4u * k0, wa + 4u * k0, n, acc);
         }
       } else {
+        if (l < 3) FC_STAMP(21 + l);  // chain entry (thread 0's first pass)
         acc = chainSegment(xa, wa, L.kred, acc);
       }
       FC_STAMP(16 + l);  // chain done (thread 0's first pass), before its stores
@@ -491,14 +498,18 @@ int fcChainThreads(const FcChainArgs& a, int rows, int cn) {
   return t > kFcMaxThreads ? kFcMaxThreads : (t < 32 ? 32 : t);
 }
 
-static void (*fcKernel(int layers))(FcChainArgs, FcPlan) {
+template <int LM>
+static void (*fcKernelLm(int layers))(FcChainArgs, FcPlan) {
   switch (layers) {
-    case 1: return fc_cluster_kernel<1>;
-    case 2: return fc_cluster_kernel<2>;
-    case 3: return fc_cluster_kernel<3>;
-    case 4: return fc_cluster_kernel<4>;
+    case 1: return fc_cluster_kernel<1, LM>;
+    case 2: return fc_cluster_kernel<2, LM>;
+    case 3: return fc_cluster_kernel<3, LM>;
+    case 4: return fc_cluster_kernel<4, LM>;
     default: return nullptr;
   }
+}
+static void (*fcKernel(int layers, int lm))(FcChainArgs, FcPlan) {
+  return lm == 1 ? fcKernelLm<1>(layers) : lm == 2 ? fcKernelLm<2>(layers) : fcKernelLm<0>(layers);
 }
 
 cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, cudaStream_t s, int loads) {
@@ -508,7 +519,7 @@ cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, c
   size_t smem = planFc(a, rows, cn, p, loads);
   if (smem > 227 * 1024 || cn < 1 || cn > 16 || rows < 1) return cudaErrorInvalidConfiguration;
   if (threads < 32 || threads > kFcMaxThreads || threads % 32) return cudaErrorInvalidConfiguration;
-  void (*kern)(FcChainArgs, FcPlan) = fcKernel(a.layers);
+  void (*kern)(FcChainArgs, FcPlan) = fcKernel(a.layers, p.bulk);
   if (!kern) return cudaErrorInvalidValue;
   {
     cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kern), (int)smem, cn > 8);

@@ -1,0 +1,68 @@
+// bulk_issue_probe.cu — what does issuing a cp.async.bulk (global -> shared) cost
+// the issuing thread? One CTA per SM, thread 0 issues N copies of B bytes from
+// distinct 4 KB-aligned sources and reads clock64 before / after the issue
+// loop and after the mbarrier completes. Sources L2-warm (second launch) or
+// cold (a 512 MB sweep between launches).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 profiles/bulk_issue_probe.cu -o /tmp/bip && /tmp/bip
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ unsigned sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__global__ void probe(const char* src, int n, int bytes, long long* out, int stride) {
+  extern __shared__ __align__(128) char sm[];
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const char* s = src + (size_t)blockIdx.x * stride;
+    long long t0 = clock64();
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar)), "r"(n * bytes) : "memory");
+    for (int i = 0; i < n; ++i)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       sa(sm + i * bytes)),
+                   "l"(s + (size_t)i * bytes), "r"(bytes), "r"(sa(&bar))
+                   : "memory");
+    long long t1 = clock64();
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(sa(&bar))
+                   : "memory");
+    long long t2 = clock64();
+    out[blockIdx.x * 2] = t1 - t0;
+    out[blockIdx.x * 2 + 1] = t2 - t0;
+  }
+}
+
+int main() {
+  char* src;
+  char* flush;
+  long long* out;
+  const size_t big = 512ull << 20;
+  cudaMalloc(&src, 148ull * (1 << 20));
+  cudaMalloc(&flush, big);
+  cudaMalloc(&out, 148 * 16);
+  cudaMemset(src, 1, 148ull * (1 << 20));
+  cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  long long h[296];
+  for (int cold = 0; cold < 2; ++cold)
+    for (int bytes : {512, 8192, 73728})
+      for (int n : {1, 2, 4}) {
+        if (n * bytes > 200 * 1024) continue;
+        probe<<<148, 64, 200 * 1024>>>(src, n, bytes, out, 1 << 20);  // warm-up / L2 fill
+        if (cold) cudaMemset(flush, cold, big);
+        probe<<<148, 64, 200 * 1024>>>(src, n, bytes, out, 1 << 20);
+        cudaError_t e = cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+        double iss = 0, land = 0;
+        for (int b = 0; b < 148; ++b) iss += h[2 * b], land += h[2 * b + 1];
+        printf("%s %3d x %6d B: issue %7.0f cycles, landed %7.0f cycles (mean over SMs) (%s)\n",
+               cold ? "cold" : "warm", n, bytes, iss / 148, land / 148, cudaGetErrorString(e));
+      }
+  return 0;
+}

@@ -12,11 +12,11 @@
 using namespace tcb::k;
 
 static void run(const char* label, FcChainArgs a, int rows, int cn, int threads) {
-  static unsigned long long z[1024][24];
+  static unsigned long long z[1024][32];
   {
     FcPlan pl;
     size_t smem = planFc(a, rows, cn, pl);
-    auto kern = fcKernel(a.layers);
+    auto kern = fcKernel(a.layers, pl.bulk);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cn > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
@@ -47,13 +47,14 @@ static void run(const char* label, FcChainArgs a, int rows, int cn, int threads)
   cudaError_t err = cudaDeviceSynchronize();
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  static unsigned long long tr[1024][24];
+  static unsigned long long tr[1024][32];
   cudaMemcpyFromSymbol(tr, g_fc_trace, sizeof(tr));
   int nblk = cn * ((a.batch + rows - 1) / rows);
   printf("%s: %s  %.2f us  (%d CTAs)\n", label, cudaGetErrorString(err), ms * 1e3, nblk);
-  const char* names[24] = {"start", "bar_init", "copies_issued", "L0_data", "L0_done", "init_fence", "L1_data",
+  const char* names[32] = {"start", "bar_init", "copies_issued", "L0_data", "L0_done", "init_fence", "L1_data",
                            "L1_done", "cta_sync", "L2_data", "L2_done", "cl_arrive", "expects", "-", "-", "end",
-                           "L0_chain", "L1_chain", "L2_chain", "L3_chain", "L0_clwait", "-", "-", "-"};
+                           "L0_chain", "L1_chain", "L2_chain", "L3_chain", "L0_clwait", "L0_enter", "L1_enter", "L2_enter",
+                           "in_copies", "w0_start", "w1_start", "w2_start", "w3_start", "-", "-", "-"};
   unsigned long long g0 = ~0ull, g1 = 0;
   for (int b = 0; b < nblk; ++b) {
     if (tr[b][13]) g0 = std::min(g0, tr[b][13]);
@@ -64,7 +65,7 @@ static void run(const char* label, FcChainArgs a, int rows, int cn, int threads)
   std::sort(st.begin(), st.end());
   printf("  globaltimer: first CTA start -> last CTA end %.2f us; CTA start skew median %lld max %lld ns\n",
          (g1 - g0) * 1e-3, st[st.size() / 2], st.back());
-  const int order[] = {1, 5, 8, 11, 12, 2, 3, 20, 16, 4, 6, 17, 7, 9, 18, 10, 19, 15};
+  const int order[] = {1, 5, 8, 11, 12, 24, 25, 26, 27, 28, 2, 3, 20, 21, 16, 4, 6, 22, 17, 7, 9, 23, 18, 10, 19, 15};
   for (int ev : order) {
     std::vector<long long> d;
     for (int b = 0; b < nblk; ++b)
