@@ -590,6 +590,17 @@ def main():
             lead = None if os.environ.get("TCB_BENCH_NO_LEADIN") else (lambda: g_all.replay())
             el = time_device(torch, lambda i: schedule[i].replay(), len(schedule), stream, lead_in=lead)
         torch.cuda.synchronize()
+        # the timed region is K steps of ~16 us: too short for more than a
+        # sample or two of a ~1 ms NVML poll, so the same step graph keeps
+        # the GPU under the same load for ~30 ms right after it, polled too
+        # (reported beside the timed region's own samples as `window`)
+        with ClockSampler(dev) as clk_win:
+            t_win = time.perf_counter()
+            while time.perf_counter() - t_win < 0.03:
+                for _ in range(20):
+                    g_all.replay()
+                torch.cuda.synchronize()
+            win_ms = (time.perf_counter() - t_win) * 1e3
         barrier()
         el = max_over_ranks(el)
         value = world * flops_step * args.steps / el / 1e9
@@ -792,7 +803,10 @@ def main():
         "strong": strong,
         "roofline": roofline,
         "step_ops": roofline_ops,
-        "clocks": clk.summary(),
+        "clocks": dict(clk.summary(), window=dict(clk_win.summary(), ms=round(win_ms, 1),
+                                                    sm_mhz_min=min(clk_win.samples) if clk_win.samples else None,
+                                                    source="nvml, the same step graph replayed right after "
+                                                           "the timed region")),
         "peaks": {"hbm_gbs": hbm_peak, "hbm_source": peak_src, "ffma_tflops": peaks["ffma_tflops"],
                   "ffma_source": "measured in this run (tcb_measure_peaks: fma.rn.f32 chains, all SMs)",
                   "launch_floor_us": peaks["launch_floor_us"],

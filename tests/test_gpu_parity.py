@@ -152,6 +152,26 @@ def test_batched_persistent_variants(engine, oracle, golden, name):
 
 
 
+@pytest.mark.parametrize("shape", [(500, 26, 26, 72), (37, 13, 29, 44), (3, 28, 32, 8), (9, 61, 40, 144)])
+def test_slab_variants(engine, oracle, shape):
+    """The slab kernel (tile_sizes[2] == 2, one CTA per batch, A rows
+    broadcast from shared memory) at 4 / 7 / 13 output rows per warp; ragged
+    rows, columns and a short last reduction chunk; bit-exact vs the oracle."""
+    B, N, K, M = shape  # Z(b,n,k) += X(b,n,m) * Y(b,k,m)
+    rng = np.random.default_rng(B * 7 + M)
+    X = rng.uniform(-1, 1, (B, N, M)).astype(np.float32)
+    Y = rng.uniform(-1, 1, (B, K, M)).astype(np.float32)
+    ref = oracle.tbmm(X, Y)
+    for ch, l1 in [(4, False), (7, False), (13, False)]:
+        o = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0, "shared_memory_budget": 49152,
+             "thread_shape": [32, 1, 1], "tile_sizes": [ch, 1, 2], "unroll_copy_shared": l1, "unroll_factor": 1,
+             "use_private": True, "use_shared": True}
+        got, h = run_on_gpu(engine, "tbmm", {"X": X, "Y": Y}, {}, options=o)
+        assert "slab_c" in engine.describe(h)["kernel"]
+        diff = int(np.sum(got["Z"].view(np.uint32) != ref.view(np.uint32)))
+        assert diff == 0, f"tbmm {shape} slab c{ch} l1={l1}: {diff} elements differ"
+
+
 @pytest.mark.parametrize("rows,cn,threads", [(1, 1, 64), (2, 2, 64), (4, 8, 64), (8, 8, 64), (8, 4, 256),
                                              (16, 8, 128), (3, 3, 96), (8, 16, 64)])
 def test_fc_chain_cluster_variants(engine, oracle, golden, rows, cn, threads):
