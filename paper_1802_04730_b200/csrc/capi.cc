@@ -81,8 +81,13 @@ struct Compiled {
   int* dErr = nullptr;
   cudaStream_t lastStream = nullptr;
   // staging for TCB_HOST tensors
-  std::vector<void*> dIn, dOut;
+  // host runs alternate between two staging sets, so an async host run can
+  // land its inputs while the previous one (on another stream) still runs
+  // its kernel or returns its outputs
+  static constexpr int kStagingSets = 2;
+  std::vector<void*> dInSet[kStagingSets], dOutSet[kStagingSets];
   std::vector<size_t> inBytes, outBytes;
+  int stagingNext = 0;
   std::vector<bool> outInout;
   // the compiled tensor signature, flattened once (tcb_run's per-call check
   // compares against it without map lookups or allocations)
@@ -96,14 +101,16 @@ struct Compiled {
   std::once_flag sigOnce;
   // recorded after a host run's last read of the staging buffers (its D2H);
   // the next host run, on any stream, waits for it before overwriting them
-  cudaEvent_t stagingFree = nullptr;
-  bool stagingPending = false;
+  cudaEvent_t stagingFree[kStagingSets] = {};
+  bool stagingPending[kStagingSets] = {};
   std::mutex runMu;
   ~Compiled() {
-    if (stagingFree) cudaEventDestroy(stagingFree);
+    for (int k = 0; k < kStagingSets; ++k) {
+      if (stagingFree[k]) cudaEventDestroy(stagingFree[k]);
+      for (void* p : dInSet[k]) cudaFree(p);
+      for (void* p : dOutSet[k]) cudaFree(p);
+    }
     if (dErr) cudaFree(dErr);
-    for (void* p : dIn) cudaFree(p);
-    for (void* p : dOut) cudaFree(p);
   }
 };
 
@@ -351,29 +358,35 @@ int deviceSms() {
 namespace {
 
 // device staging buffers of a handle run on host tensors
-void ensureStaging(Compiled& c) {
+void ensureStaging(Compiled& c, int set) {
   const auto& params = c.spec.v.def.params;
   const auto& rets = c.spec.v.def.rets;
   const int nin = static_cast<int>(params.size()), nout = static_cast<int>(rets.size());
-  if (c.dIn.empty()) {
+  if (c.inBytes.empty()) {
     auto inout = sem::inoutReturns(c.spec.v);
     for (int i = 0; i < nin; ++i) {
       size_t b = 4;
       if (!params[i].scalar())
         for (auto x : c.spec.shapes.at(params[i].name)) b *= static_cast<size_t>(x);
-      void* p = nullptr;
-      cudaOk(cudaMalloc(&p, b), "cudaMalloc");
-      c.dIn.push_back(p);
       c.inBytes.push_back(b);
     }
     for (int i = 0; i < nout; ++i) {
       size_t b = 4;
       for (auto x : c.spec.shapes.at(rets[i])) b *= static_cast<size_t>(x);
-      void* p = nullptr;
-      cudaOk(cudaMalloc(&p, b), "cudaMalloc");
-      c.dOut.push_back(p);
       c.outBytes.push_back(b);
       c.outInout.push_back(std::find(inout.begin(), inout.end(), rets[i]) != inout.end());
+    }
+  }
+  if (c.dInSet[set].empty()) {
+    for (int i = 0; i < nin; ++i) {
+      void* p = nullptr;
+      cudaOk(cudaMalloc(&p, c.inBytes[i]), "cudaMalloc");
+      c.dInSet[set].push_back(p);
+    }
+    for (int i = 0; i < nout; ++i) {
+      void* p = nullptr;
+      cudaOk(cudaMalloc(&p, c.outBytes[i]), "cudaMalloc");
+      c.dOutSet[set].push_back(p);
     }
   }
 }
@@ -459,12 +472,15 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
     // host tensors: mapped pinned buffers up to zeroCopyMax() move in one
     // segment-copy launch per direction; the rest (pageable or large) by DMA
     k::SegCopyArgs up{}, down{};
+    const int set = host ? c.stagingNext : 0;
     if (host) {
-      ensureStaging(c);
-      if (!c.stagingFree) cudaOk(cudaEventCreateWithFlags(&c.stagingFree, cudaEventDisableTiming), "event");
+      c.stagingNext = (c.stagingNext + 1) % Compiled::kStagingSets;
+      ensureStaging(c, set);
+      if (!c.stagingFree[set])
+        cudaOk(cudaEventCreateWithFlags(&c.stagingFree[set], cudaEventDisableTiming), "event");
       // an earlier async host run (possibly on another stream) may still be
-      // reading these staging buffers
-      if (c.stagingPending) cudaOk(cudaStreamWaitEvent(s, c.stagingFree, 0), "stream wait");
+      // reading this staging set
+      if (c.stagingPending[set]) cudaOk(cudaStreamWaitEvent(s, c.stagingFree[set], 0), "stream wait");
       auto stage = [&](k::SegCopyArgs& a, void* dst, const void* src, const void* mapped, size_t bytes,
                        cudaMemcpyKind kind) {
         if (mapped && a.n < k::kMaxSeg && static_cast<int64_t>(bytes) <= zeroCopyMax() && bytes % 4 == 0) {
@@ -477,12 +493,12 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
         }
       };
       for (int i = 0; i < nin; ++i) {
-        din[i] = c.dIn[i];
+        din[i] = c.dInSet[set][i];
         if (!params[i].scalar())
           stage(up, din[i], in[i].data, mappedHost(in[i].data), c.inBytes[i], cudaMemcpyHostToDevice);
       }
       for (int i = 0; i < nout; ++i) {
-        dout[i] = c.dOut[i];
+        dout[i] = c.dOutSet[set][i];
         outMapped[i] = mappedHost(out[i].data);
         if (c.outInout[i]) stage(up, dout[i], out[i].data, outMapped[i], c.outBytes[i], cudaMemcpyHostToDevice);
       }
@@ -507,8 +523,8 @@ int tcb_run(tcb_engine* e, uint64_t h, const tcb_tensor* in, int nin, const tcb_
           cudaOk(cudaMemcpyAsync(out[i].data, dout[i], c.outBytes[i], cudaMemcpyDeviceToHost, s), "D2H");
       }
       cudaOk(k::launchSegCopy(down, deviceSms(), s), "host copy");
-      cudaOk(cudaEventRecord(c.stagingFree, s), "record");
-      c.stagingPending = (flags & TCB_RUN_ASYNC) != 0;
+      cudaOk(cudaEventRecord(c.stagingFree[set], s), "record");
+      c.stagingPending[set] = (flags & TCB_RUN_ASYNC) != 0;
       if (!(flags & TCB_RUN_ASYNC)) cudaOk(cudaStreamSynchronize(s), "sync");
     }
     if (profile) {
