@@ -10,30 +10,41 @@
 
 __device__ __forceinline__ unsigned sa(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-__global__ void probe(const char* src, int n, int bytes, long long* out, int stride) {
+// mode 0: one mbarrier, sources i*bytes apart; 1: one mbarrier per copy;
+// 2: one mbarrier, sources 64 MB apart (distinct pages / allocations)
+__global__ void probe(const char* src, int n, int bytes, long long* out, int stride, int mode) {
   extern __shared__ __align__(128) char sm[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bars[8];
   if (threadIdx.x == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar)));
+    for (int i = 0; i < 8; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bars[i])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     const char* s = src + (size_t)blockIdx.x * stride;
     long long t0 = clock64();
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar)), "r"(n * bytes) : "memory");
-    for (int i = 0; i < n; ++i)
+    if (mode == 1) {
+      for (int i = 0; i < n; ++i)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bars[i])), "r"(bytes) : "memory");
+    } else {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bars[0])), "r"(n * bytes) : "memory");
+    }
+    for (int i = 0; i < n; ++i) {
+      const char* g = mode == 2 ? s + (size_t)i * (64ull << 20) : s + (size_t)i * bytes;
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                        sa(sm + i * bytes)),
-                   "l"(s + (size_t)i * bytes), "r"(bytes), "r"(sa(&bar))
+                   "l"(g), "r"(bytes), "r"(sa(&bars[mode == 1 ? i : 0]))
                    : "memory");
+    }
     long long t1 = clock64();
-    unsigned done = 0;
-    while (!done)
-      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                   : "=r"(done)
-                   : "r"(sa(&bar))
-                   : "memory");
+    for (int i = 0; i < (mode == 1 ? n : 1); ++i) {
+      unsigned done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(sa(&bars[i]))
+                     : "memory");
+    }
     long long t2 = clock64();
     out[blockIdx.x * 2] = t1 - t0;
     out[blockIdx.x * 2 + 1] = t2 - t0;
@@ -45,24 +56,25 @@ int main() {
   char* flush;
   long long* out;
   const size_t big = 512ull << 20;
-  cudaMalloc(&src, 148ull * (1 << 20));
+  cudaMalloc(&src, 148ull * (1 << 20) + 5 * (64ull << 20));
   cudaMalloc(&flush, big);
   cudaMalloc(&out, 148 * 16);
-  cudaMemset(src, 1, 148ull * (1 << 20));
+  cudaMemset(src, 1, 148ull * (1 << 20) + 5 * (64ull << 20));
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   long long h[296];
+  for (int mode = 0; mode < 3; ++mode)
   for (int cold = 0; cold < 2; ++cold)
-    for (int bytes : {512, 8192, 73728})
+    for (int bytes : {512, 8192})
       for (int n : {1, 2, 4}) {
         if (n * bytes > 200 * 1024) continue;
-        probe<<<148, 64, 200 * 1024>>>(src, n, bytes, out, 1 << 20);  // warm-up / L2 fill
+        probe<<<148, 64, 200 * 1024>>>(src, n, bytes, out, 1 << 20, mode);  // warm-up / L2 fill
         if (cold) cudaMemset(flush, cold, big);
-        probe<<<148, 64, 200 * 1024>>>(src, n, bytes, out, 1 << 20);
+        probe<<<148, 64, 200 * 1024>>>(src, n, bytes, out, 1 << 20, mode);
         cudaError_t e = cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
         double iss = 0, land = 0;
         for (int b = 0; b < 148; ++b) iss += h[2 * b], land += h[2 * b + 1];
-        printf("%s %3d x %6d B: issue %7.0f cycles, landed %7.0f cycles (mean over SMs) (%s)\n",
-               cold ? "cold" : "warm", n, bytes, iss / 148, land / 148, cudaGetErrorString(e));
+        printf("mode %d %s %3d x %6d B: issue %7.0f cycles, landed %7.0f cycles (mean over SMs) (%s)\n",
+               mode, cold ? "cold" : "warm", n, bytes, iss / 148, land / 148, cudaGetErrorString(e));
       }
   return 0;
 }
