@@ -72,12 +72,12 @@ TC_OPS = [("tmm 128x1024x1024", "3xtf32"), ("tmm 128x1024x1024", "tf32"),
           ("gconv paper 32,32,16,16,14x14", "tf32"), ("gconv paper 32,32,32,32,7x7", "tf32")]
 INT_PARAMS = {"2LUT": {1, 3}, "1LUT": {1}}
 # Plans passed explicitly for the forked step (merged over each op's default
-# options), measured over the step, not each op alone
-# (profiles/r02_step_variants.txt): the 4-rows-per-warp slab is slower alone
-# (9.6 vs 6.9 us) but its lighter CTAs share SMs with the FC chains better
-# (step 16.2 -> 15.6 us). The library defaults stay the standalone-best
-# plans.
-STEP_PLANS = {"tbmm": {"tile_sizes": [4, 1, 2]}}
+# options), measured over the step, not each op alone. Empty since the
+# 9-rows-per-warp slab became the TBMM default: it is the best plan alone
+# (6.7 us) and in the step (15.2 us; the 4-row slab that was the step plan:
+# 16.0 us after the FC kernel changes, profiles/r02_slab_rows.txt). The
+# library defaults are the standalone-best plans.
+STEP_PLANS = {}
 
 
 def step_set_bytes():

@@ -852,6 +852,10 @@ const GemmVariant kGemmVariants[] = {
     {48, 32, 32, 4, 2, -6, "tma_t32x32_r4x2_mc4", 4},
     {49, 32, 16, 2, 2, -6, "tma_t32x16_r2x2_mc4", 4},
     {50, 32, 32, 2, 2, -6, "tma_t32x32_r2x2_mc2", 2},
+    // more broadcast-slab row counts per warp (tk = -1)
+    {51, 0, 0, 5, 1, -1, "slab_c5", 0},
+    {52, 0, 0, 6, 1, -1, "slab_c6", 0},
+    {53, 0, 0, 9, 1, -1, "slab_c9", 0},
 };
 
 template <int RM, int RN>
@@ -1051,6 +1055,11 @@ cudaError_t launchGemm(const GemmArgs& a, int variant, int threads, cudaStream_t
     case 48:
     case 49:
     case 50: return launchGemmTma(a, variant - 40, s);
+    case 51:
+    case 52:
+    case 53:
+      if (!slabOk(a)) return cudaErrorInvalidValue;
+      return variant == 51 ? launchSlabCh<5>(a, s) : variant == 52 ? launchSlabCh<6>(a, s) : launchSlabCh<9>(a, s);
     case 19:
     case 20:
     case 21:

@@ -190,7 +190,7 @@ void decodeGemm(const MappingOptions& o, Mapping& m) {
         return;
       }
     }
-    invalid("slab GEMM micro-tile must be 4x1, 7x1, 13x1 (broadcast) or 7x4, 4x4, 4x2 (register-tiled)");
+    invalid("slab GEMM micro-tile must be 4x1 to 7x1, 9x1, 13x1 (broadcast) or 7x4, 4x4, 4x2 (register-tiled)");
   }
   if (o.tileSizes[2] == 3) {
     // reduction depth 3 = TMA-fed tiles (32-deep stages): tile tm x tn,
@@ -651,8 +651,10 @@ MappingOptions defaultOptions(const Problem& p, int math) {
       o.unrollCopyShared = g.K > 128;
       if (g.batch > 1 && g.K % 4 == 0 && g.K <= 144 && g.M <= 64 && g.N <= 256) {
         // many small batches (TBMM 500 x 26x26x72): the slab kernel, one
-        // CTA per batch, 7 output rows per warp
-        o.tileSizes = {g.M <= 16 ? 4 : 7, 1, 2};
+        // CTA per batch, 9 output rows per warp (3 warps for 26 rows; 6.7 us
+        // alone vs 6.8 for 7 rows, 15.2 vs 15.7 us in the bench step,
+        // profiles/r02_slab_rows.txt)
+        o.tileSizes = {g.M <= 16 ? 4 : 9, 1, 2};
         o.threadShape = {{32, 1, 1}};
         o.unrollCopyShared = false;
         break;

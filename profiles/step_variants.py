@@ -16,8 +16,12 @@ from paper_1802_04730_b200 import ExecutionEngine  # noqa: E402
 
 NSTEP = int(os.environ.get("NSTEP", "26"))
 
-COMBOS = [  # r02: step plans (footprint-light TBMM plans beside the FC chains)
+COMBOS = [  # r02: TBMM slab rows per warp in the step
     {"tbmm": {"tile_sizes": [4, 1, 2]}},
+    {"tbmm": {"tile_sizes": [7, 1, 2]}},
+    {"tbmm": {"tile_sizes": [9, 1, 2]}},
+    {"tbmm": {"tile_sizes": [13, 1, 2]}},
+    {"tbmm": {"tile_sizes": [5, 1, 2]}},
 ]
 
 VARIANTS = {
@@ -86,15 +90,12 @@ def main():
     g0 = graph_of(list(ops.values()))
     print(f"default step {min(timeit(g0) for _ in range(8)):.2f} us", flush=True)
     import itertools
-    for order in itertools.permutations(list(ops)):
+    for order in itertools.permutations(list(ops)) if os.environ.get("ORDER_ONLY") else []:
         g = graph_of([ops[n] for n in order])
         print(f"fork order {order}: {min(timeit(g) for _ in range(6)):.2f} us", flush=True)
     if os.environ.get("ORDER_ONLY"):
         return
-    gp = graph_of(list(ops.values()), pipelined=True)
-    print(f"pipelined steps {min(timeit(gp) for _ in range(8)):.2f} us per step", flush=True)
-    for name, v in [("tbmm", {"tile_sizes": [7, 1, 2]}), ("tbmm", {"tile_sizes": [4, 1, 2]}),
-                    ("tbmm", {"tile_sizes": [4, 4, 4], "block_shape": [2, 1, 1]}),
+    for name, v in [] if not os.environ.get("PIPE") else [("tbmm", {"tile_sizes": [7, 1, 2]}), ("tbmm", {"tile_sizes": [4, 1, 2]}),
                     ("2FCRelu", {"tile_sizes": [8, 8, 1], "thread_shape": [128, 1, 1]}),
                     ("2FCRelu", {"tile_sizes": [16, 8, 1], "thread_shape": [256, 1, 1]}),
                     ("MLP3", {"tile_sizes": [8, 4, 6], "thread_shape": [128, 1, 1]})]:
@@ -103,8 +104,11 @@ def main():
         gp = graph_of(list(ops.values()), pipelined=True)
         print(f"pipelined {name} {v}: {min(timeit(gp) for _ in range(5)):.2f} us per step", flush=True)
         o.handle = base[name]
-    for name in ops:
-        print(f"{name} alone (back to back): {min(timeit(graph_of([ops[name]], pipelined=True)) for _ in range(3)):.2f} us", flush=True)
+    if os.environ.get("PIPE"):
+        gp = graph_of(list(ops.values()), pipelined=True)
+        print(f"pipelined steps {min(timeit(gp) for _ in range(8)):.2f} us per step", flush=True)
+        for name in ops:
+            print(f"{name} alone (back to back): {min(timeit(graph_of([ops[name]], pipelined=True)) for _ in range(3)):.2f} us", flush=True)
     if os.environ.get("PIPE_ONLY"):
         return
     for combo in COMBOS:

@@ -155,14 +155,15 @@ def test_batched_persistent_variants(engine, oracle, golden, name):
 @pytest.mark.parametrize("shape", [(500, 26, 26, 72), (37, 13, 29, 44), (3, 28, 32, 8), (9, 61, 40, 144)])
 def test_slab_variants(engine, oracle, shape):
     """The slab kernel (tile_sizes[2] == 2, one CTA per batch, A rows
-    broadcast from shared memory) at 4 / 7 / 13 output rows per warp; ragged
-    rows, columns and a short last reduction chunk; bit-exact vs the oracle."""
+    broadcast from shared memory) at 4 to 7, 9 and 13 output rows per warp;
+    ragged rows, columns and a short last reduction chunk; bit-exact vs the
+    oracle."""
     B, N, K, M = shape  # Z(b,n,k) += X(b,n,m) * Y(b,k,m)
     rng = np.random.default_rng(B * 7 + M)
     X = rng.uniform(-1, 1, (B, N, M)).astype(np.float32)
     Y = rng.uniform(-1, 1, (B, K, M)).astype(np.float32)
     ref = oracle.tbmm(X, Y)
-    for ch, l1 in [(4, False), (7, False), (13, False)]:
+    for ch, l1 in [(4, False), (5, False), (6, False), (7, False), (9, False), (13, False)]:
         o = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0, "shared_memory_budget": 49152,
              "thread_shape": [32, 1, 1], "tile_sizes": [ch, 1, 2], "unroll_copy_shared": l1, "unroll_factor": 1,
              "use_private": True, "use_shared": True}
