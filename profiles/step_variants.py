@@ -25,10 +25,10 @@ COMBOS = [  # r02: TBMM slab rows per warp in the step
 ]
 
 VARIANTS = {
-    "2FCRelu": [None, {"tile_sizes": [8, 8, 1], "thread_shape": [128, 1, 1]}, {"tile_sizes": [16, 8, 1], "thread_shape": [256, 1, 1]},
-                {"tile_sizes": [8, 4, 1], "thread_shape": [256, 1, 1]}],
-    "tbmm": [None],
-    "MLP3": [None, {"tile_sizes": [8, 4, 1], "thread_shape": [64, 1, 1]}, {"tile_sizes": [8, 2, 1], "thread_shape": [64, 1, 1]}],
+    "2FCRelu": [None, {"tile_sizes": [4, 16, 1], "thread_shape": [64, 1, 1]}, {"tile_sizes": [2, 8, 1], "thread_shape": [32, 1, 1]},
+                {"tile_sizes": [4, 4, 1], "thread_shape": [128, 1, 1]}, {"tile_sizes": [2, 16, 1], "thread_shape": [32, 1, 1]}],
+    "MLP3": [None, {"tile_sizes": [2, 4, 1], "thread_shape": [32, 1, 1]}, {"tile_sizes": [4, 8, 1], "thread_shape": [64, 1, 1]},
+             {"tile_sizes": [8, 4, 6], "thread_shape": [128, 1, 1]}, {"tile_sizes": [4, 2, 1], "thread_shape": [64, 1, 1]}],
 }
 
 
