@@ -230,10 +230,14 @@ class OpInstance:
 
 
 DOM_NOTES = {
-    "2FCRelu": "Bound by its sequential FFMA chain (1128 + 128 dependent steps per output) after a ~2.4 us "
-               "load prologue, not by bytes: see chain_floor_us / chain_floor_frac (DESIGN.md section 8).",
-    "tbmm": "500 batches of 26x26 outputs, 72-step chains: one wave of CTAs (slab kernel) whose loads and "
-            "chains overlap only chunk by chunk; cold-read floor for its 8.84 MB ~3.1 us (DESIGN.md section 5).",
+    "2FCRelu": "Latency bound, not byte bound: every output is one sequential FFMA chain of 1128 + 128 dependent "
+               "steps (chain_floor_us at 4 cycles a step); it runs ~6.3 cycles a step because two CTAs share an "
+               "SM and their LDS.128 operand reads saturate its shared-memory pipe (one CTA per SM: ~5.0, "
+               "profiles/r02_chain_probe2.txt), after a ~1.5 us load prologue (DESIGN.md section 8).",
+    "tbmm": "500 batches of 26x26 outputs, 72-step chains: one wave of CTAs (slab kernel, 9 rows per warp); its "
+            "8.84 MB land in ~2-2.5 us (cold-read floor ~3.1 us with launch) and the exact chains need ~1.5-2 us "
+            "of SM time at the measured 0.5-0.6 warp-FFMA per cycle per SMSP, overlapped only chunk by chunk "
+            "(DESIGN.md sections 5 and 12).",
     "MLP3": "Three short dependent layers (128, 64, 32 steps): latency bound, see chain_floor_us.",
 }
 
