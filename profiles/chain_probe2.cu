@@ -114,6 +114,96 @@ __global__ void probe(float* out, long long* cyc, int K) {
   if (lt == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
+// 2 x 2 chains per thread: rows r, r+2 of X and columns c, c+8 of W share loads
+__device__ __noinline__ void chain22(unsigned xa0, unsigned xa1, unsigned wa0, unsigned wa1, int n, float* acc) {
+  float a00 = acc[0], a01 = acc[1], a10 = acc[2], a11 = acc[3];
+  float4 X0 = lds4(xa0), X1 = lds4(xa1), W0 = lds4(wa0), W1 = lds4(wa1);
+  for (int k = 4; k <= n; k += 4) {
+    float4 x0 = X0, x1 = X1, w0 = W0, w1 = W1;
+    if (k < n) {
+      X0 = lds4(xa0 + k * 4); X1 = lds4(xa1 + k * 4); W0 = lds4(wa0 + k * 4); W1 = lds4(wa1 + k * 4);
+    }
+    a00 = fma4(x0, w0, a00); a01 = fma4(x0, w1, a01); a10 = fma4(x1, w0, a10); a11 = fma4(x1, w1, a11);
+  }
+  acc[0] = a00; acc[1] = a01; acc[2] = a10; acc[3] = a11;
+}
+
+// 1 x 2 chains per thread: one X row, columns c and c+8 of W (the X read shared)
+__device__ __noinline__ void chain12(unsigned xa, unsigned wa0, unsigned wa1, int n, float* acc) {
+  float a0 = acc[0], a1 = acc[1];
+  const int nch = n >> 4;
+  float4 X0[4], V0[4], U0[4], X1[4], V1[4], U1[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    X0[i] = lds4(xa + i * 16);
+    V0[i] = lds4(wa0 + i * 16);
+    U0[i] = lds4(wa1 + i * 16);
+  }
+  for (int c = 0; c + 2 <= nch; c += 2) {
+    const unsigned o = c * 64;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      X1[i] = lds4(xa + o + 64 + i * 16);
+      V1[i] = lds4(wa0 + o + 64 + i * 16);
+      U1[i] = lds4(wa1 + o + 64 + i * 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a0 = fma4(X0[i], V0[i], a0);
+      a1 = fma4(X0[i], U0[i], a1);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      X0[i] = lds4(xa + o + 128 + i * 16);
+      V0[i] = lds4(wa0 + o + 128 + i * 16);
+      U0[i] = lds4(wa1 + o + 128 + i * 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a0 = fma4(X1[i], V1[i], a0);
+      a1 = fma4(X1[i], U1[i], a1);
+    }
+  }
+  acc[0] = a0;
+  acc[1] = a1;
+}
+
+__global__ void probe12(float* out, long long* cyc, int K) {
+  extern __shared__ __align__(16) float sm[];
+  const int R = 4, C = 16;
+  float* X = sm;
+  float* Wt = sm + R * K + 64;
+  for (int e = threadIdx.x; e < (R + C) * K + 256; e += blockDim.x) sm[e] = 1e-3f * (e % 97);
+  __syncthreads();
+  const int r = threadIdx.x % R, c = threadIdx.x / R;  // 32 threads: c in 0..7, columns c and c+8
+  float acc[2] = {0, 0};
+  long long t0 = clock64();
+  chain12((unsigned)__cvta_generic_to_shared(X + r * K), (unsigned)__cvta_generic_to_shared(Wt + c * K),
+          (unsigned)__cvta_generic_to_shared(Wt + (c + 8) * K), K, acc);
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc[0] + acc[1];
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
+__global__ void probe22(float* out, long long* cyc, int K) {
+  extern __shared__ __align__(16) float sm[];
+  const int R = 4, C = 16;
+  float* X = sm;
+  float* Wt = sm + R * K + 64;
+  for (int e = threadIdx.x; e < (R + C) * K + 128; e += blockDim.x) sm[e] = 1e-3f * (e % 97);
+  __syncthreads();
+  // 16 threads: r in {0,1} (+2), c in 0..7 (+8)
+  const int r = threadIdx.x % 2, c = threadIdx.x / 2;
+  float acc[4] = {0, 0, 0, 0};
+  long long t0 = clock64();
+  chain22((unsigned)__cvta_generic_to_shared(X + r * K), (unsigned)__cvta_generic_to_shared(X + (r + 2) * K),
+          (unsigned)__cvta_generic_to_shared(Wt + c * K), (unsigned)__cvta_generic_to_shared(Wt + (c + 8) * K), K,
+          acc);
+  long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc[0] + acc[1] + acc[2] + acc[3];
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+
 int main() {
   float* out;
   long long* cyc;
@@ -133,6 +223,32 @@ int main() {
       double s = 0;
       for (int i = 0; i < ctas; ++i) s += h[i];
       printf("%-22s %3d CTAs x 64 thr: %.2f cycles/step (%s)\n", names[v], ctas, s / ctas / K, cudaGetErrorString(e));
+    }
+  }
+  {
+    cudaFuncSetAttribute(probe22, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    long long h[296];
+    for (int ctas : {148, 256, 296}) {
+      probe22<<<ctas, 16, smem>>>(out, cyc, K);
+      probe22<<<ctas, 16, smem>>>(out, cyc, K);
+      cudaError_t e = cudaMemcpy(h, cyc, ctas * 8, cudaMemcpyDeviceToHost);
+      double s = 0;
+      for (int i = 0; i < ctas; ++i) s += h[i];
+      printf("chain22 (2x2 per thread, 16-thread CTAs), %3d CTAs: %.2f cycles/step (%s)\n", ctas, s / ctas / K,
+             cudaGetErrorString(e));
+    }
+  }
+  {
+    cudaFuncSetAttribute(probe12, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    long long h[296];
+    for (int ctas : {148, 256, 296}) {
+      probe12<<<ctas, 32, smem>>>(out, cyc, K);
+      probe12<<<ctas, 32, smem>>>(out, cyc, K);
+      cudaError_t e = cudaMemcpy(h, cyc, ctas * 8, cudaMemcpyDeviceToHost);
+      double s = 0;
+      for (int i = 0; i < ctas; ++i) s += h[i];
+      printf("chain12 (1 row x 2 columns per thread, 32-thread CTAs), %3d CTAs: %.2f cycles/step (%s)\n", ctas,
+             s / ctas / K, cudaGetErrorString(e));
     }
   }
   // placement: 2 CTAs per SM (296 x 64 threads) vs 4-warp CTAs whose chain warps pick an SMSP pair
