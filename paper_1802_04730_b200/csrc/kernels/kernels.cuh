@@ -106,6 +106,10 @@ bool fcRegsSupported(const FcChainArgs& a, int rows, const char** why);
 // 128 rows, activations TMEM -> shared memory -> next layer's A operand
 bool tcFcFusedSupported(const FcChainArgs& a, int math, const char** why);
 cudaError_t launchTcFcFused(const FcChainArgs& a, int math, cudaStream_t s);
+// two FC layers in one tcgen05 launch (tc_gemm.cu): layer 1 split-K over a
+// cluster, layer 2 in rank 0 from the reduced rows (2FCRelu at K = 1128)
+bool tcFc2Supported(const FcChainArgs& a, int math, const char** why);
+cudaError_t launchTcFc2(const FcChainArgs& a, int math, int sms, cudaStream_t s);
 cudaError_t launchFcRegs(const FcChainArgs& a, int rows, cudaStream_t s);
 // the cluster kernel with layer 0 streamed in by TMA tensor copies in 256-step
 // reduction chunks (fc_tma.cu): layer 0's chains start on the first chunk

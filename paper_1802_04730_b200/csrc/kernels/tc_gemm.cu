@@ -59,9 +59,15 @@ struct TcParams {
   // batches [t*packP, t*packP + packP) stacked along M (rows of M each) and
   // along N; only the diagonal blocks are stored. 0 = no packing.
   int packP, batch;
+  // fused second FC layer (tcFc2): O2 = relu(O1 . W2^T + bias2), O1 being this
+  // GEMM's bias + ReLU output; N2p = N2 rounded up to 16, K2p = K2 = N (a
+  // multiple of 32)
+  float* O2;
+  const float* bias2;
+  int N2, N2p, K2p;
 };
 
-template <int BN, bool X3>
+template <int BN, bool X3, bool L2 = false>
 struct TcCfg {
   static constexpr int kABytes = kBM * kBK * 4;
   static constexpr int kBBytes = BN * kBK * 4;
@@ -77,9 +83,15 @@ struct TcCfg {
   static constexpr int kStagesTm = X3 ? (512 - kAccCols) / (2 * kBK) : 8;
   static constexpr int kStagesRaw = kStagesSm < kStagesTm ? kStagesSm : kStagesTm;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kRing = kStages * kStage > kPartBytes ? kStages * kStage : kPartBytes;
+  static constexpr int kRingRaw = kStages * kStage > kPartBytes ? kStages * kStage : kPartBytes;
+  // L2: the partial tile, A2 (K2p <= 128) and W2 (N2p <= 128 TF32 / 64 3xTF32, + its lo plane)
+  static constexpr int kL2Bytes = 69632 + 65536 + 65536;
+  static constexpr int kRing = L2 && kL2Bytes > kRingRaw ? kL2Bytes : kRingRaw;
   static constexpr int kSmem = 1024 + kRing + 256;
-  static constexpr int kTmemCols = X3 ? 512 : kAccCols;
+  // L2 (fused second layer, BN <= 128): layer 2's A operand hi / lo (3xTF32)
+  // at TMEM columns 128 / 256, its accumulator at 384
+  static constexpr int kTmemCols = (X3 || L2) ? 512 : kAccCols;
+  static constexpr int kA2Off = (kPartBytes + 1023) / 1024 * 1024;  // L2: layer 2's A (rank 0), after the partial tile
   static_assert(kStages >= 2, "stage ring too small");
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 is a multiple of 16 in [16, 256]");
 };
@@ -89,10 +101,17 @@ struct TcCfg {
 __device__ __forceinline__ float lo1(float x) { return toTf32(x - rzTf32(x)); }
 __device__ __forceinline__ float4 loPart(float4 x) { return make_float4(lo1(x.x), lo1(x.y), lo1(x.z), lo1(x.w)); }
 
-template <int BN, bool X3>
+// swizzled K-major SW128 offset of element (row, k) of a 128-row operand
+// (k-blocks of 32 fp32, 128-byte rows, 16-byte unit j of row r at j ^ (r & 7))
+__device__ __forceinline__ uint32_t swOff128(int row, int k) {
+  return (uint32_t)((k >> 5) * (kBM * 128) + row * 128 + ((((k & 31) >> 2) ^ (row & 7)) << 4) + ((k & 3) << 2));
+}
+
+template <int BN, bool X3, bool L2 = false>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
-  using Cfg = TcCfg<BN, X3>;
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmW2, TcParams p) {
+  using Cfg = TcCfg<BN, X3, L2>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -105,7 +124,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* conv = full + S;
   uint64_t* empty = conv + S;
   uint64_t* tmemFull = empty + S;
-  uint32_t* tmemSlot = reinterpret_cast<uint32_t*>(tmemFull + 1);
+  uint64_t* b2Full = tmemFull + 1;  // L2: W2 landed (rank 0)
+  uint64_t* l2Done = tmemFull + 2;  // L2: layer-2 MMAs complete (rank 0)
+  uint64_t* a2Full = tmemFull + 3;  // L2: every peer's O1 rows landed in rank 0's A2
+  uint32_t* tmemSlot = reinterpret_cast<uint32_t*>(tmemFull + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nt = blockIdx.x, mt = blockIdx.y;
@@ -120,11 +142,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbarInit(&empty[s], 1);
     }
     mbarInit(tmemFull, 1);
+    mbarInit(b2Full, 1);
+    mbarInit(l2Done, 1);
+    mbarInit(a2Full, 1);
+    // rank 0's A2 receives every other rank's rows by bulk copy
+    if (L2 && split == 0)
+      mbarExpectTx(a2Full, (unsigned)((kBM - kBM / p.splits) * p.K2p * 4));
     fenceBarrierInit();
   }
   if (warp == 0 && lane == 0) {
     tmaPrefetch(&tmA);
     tmaPrefetch(&tmB);
+    if (L2) tmaPrefetch(&tmW2);
   }
   if (warp == 2) tmemAlloc<Cfg::kTmemCols>(tmemSlot);
   tcFenceBefore();
@@ -216,6 +245,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // accumulator → shared partial tile (the ring is idle once tmemFull fires)
     mbarWait(tmemFull, 0, 3);
     tcFenceAfter();
+    if (L2 && split == 0 && warp == 4 && lane == 0) {
+      // layer 2's weights land behind layer 1's epilogue, after A2 (the
+      // partial tile and A2 sit below them; the ring is idle)
+      const int nkb2 = p.K2p / kBK;
+      uint8_t* b2 = sm + Cfg::kA2Off + nkb2 * kBM * 128;
+      mbarExpectTx(b2Full, (unsigned)(nkb2 * p.N2p * 128));
+      for (int kb = 0; kb < nkb2; ++kb) tmaLoad3d(b2 + kb * p.N2p * 128, &tmW2, kb * kBK, 0, 0, b2Full);
+    }
     const int q = warp - 4, row = q * 32 + lane;
     float* part = reinterpret_cast<float*>(sm) + row * Cfg::kPartLd;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
@@ -301,10 +338,130 @@ __global__ void __launch_bounds__(kThreads, 1)
         else if (p.init == kInitBias) v = p.bias[n0 + j] + v;
         if (p.relu) v = fmaxf(v, 0.f);
         cp[j] = v;
+        if (L2)  // layer 2's A operand, K-major SW128: this CTA's rows, locally
+          *reinterpret_cast<float*>(sm + Cfg::kA2Off + swOff128(m, n0 + j)) = v;
+      }
+    }
+  }
+  if constexpr (L2) {
+    // this CTA's O1 rows go to rank 0's A2 by one bulk copy per 32-column
+    // block (16 rows x 128 B, contiguous under the swizzle): 4-byte remote
+    // stores from every rank queued ~1 per cycle at rank 0 (6.4 us)
+    if (split > 0) {
+      fenceProxyAsyncSmem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int R = kBM / p.splits;
+        const uint32_t src = smem(sm + Cfg::kA2Off) + split * R * 128;
+        const uint32_t bar0 = mapa(smem(a2Full), 0);
+        for (int kb = 0; kb < p.K2p / kBK; ++kb)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  mapa(src + kb * kBM * 128, 0)),
+              "r"(src + kb * kBM * 128), "r"((unsigned)(R * 128)), "r"(bar0)
+              : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       }
     }
   }
   if (p.splits > 1) clusterSync();  // peers may still be reading this CTA's partial
+  if constexpr (L2) {
+    if (p.splits == 1) __syncthreads();
+    if (split == 0) {
+      // ---- the fused second layer, in rank 0: M = 128 rows of O1 (A2, every
+      // rank's reduced rows), N = N2p, K = K2p
+      const int nkb2 = p.K2p / kBK;
+      uint8_t* a2 = sm + Cfg::kA2Off;
+      uint8_t* b2 = a2 + nkb2 * kBM * 128;
+      uint8_t* b2lo = b2 + nkb2 * p.N2p * 128;
+      const uint32_t acc2 = tmem + 384u;
+      mbarWait(b2Full, 0, 8);
+      if (p.splits > 1) mbarWait(a2Full, 0, 10);
+      {
+        // (3xTF32) B2's lo plane (all threads); A2's hi (/ lo) into TMEM
+        // (warps 4-7: lane = row): the MMA reads A from TMEM, so the O1 rows
+        // the ranks stored into this CTA's shared memory are only ever read
+        // by the generic proxy
+        if (X3) {
+          const float4* bv = reinterpret_cast<const float4*>(b2);
+          float4* bl = reinterpret_cast<float4*>(b2lo);
+          for (int j = threadIdx.x; j < nkb2 * p.N2p * 8; j += kThreads) bl[j] = loPart(bv[j]);
+        }
+        if (warp >= 4) {
+          const int row = (warp - 4) * 32 + lane;
+          const uint32_t tl = tmem + (static_cast<uint32_t>((warp - 4) * 32) << 16);
+          for (int kb = 0; kb < nkb2; ++kb) {
+            const float4* ar = reinterpret_cast<const float4*>(a2 + kb * kBM * 128 + row * 128);
+            float hi[kBK], lo[kBK];
+#pragma unroll
+            for (int j = 0; j < kBK / 4; ++j) {
+              const float4 x = ar[j ^ (row & 7)];
+              const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                hi[4 * j + e] = rzTf32(xs[e]);
+                lo[4 * j + e] = toTf32(xs[e] - hi[4 * j + e]);
+              }
+            }
+            tmemStore32(tl + 128 + kb * kBK, hi);
+            if (X3) tmemStore32(tl + 256 + kb * kBK, lo);
+          }
+          tmemStoreWait();
+        }
+        if (X3) fenceProxyAsyncSmem();
+      }
+      tcFenceBefore();
+      __syncthreads();
+      tcFenceAfter();
+      if (warp == 1 && lane == 0) {
+        const uint32_t idesc2 = idescTf32(kBM, p.N2p);
+        for (int kb = 0; kb < nkb2; ++kb) {
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            const uint32_t acc = (kb | kk) != 0;
+            const uint32_t bhi = smem(b2 + kb * p.N2p * 128) + kk * 32;
+            const uint32_t ahi = tmem + 128 + kb * kBK + kk * 8;
+            if constexpr (X3) {
+              const uint32_t alo = tmem + 256 + kb * kBK + kk * 8;
+              const uint32_t blo = smem(b2lo + kb * p.N2p * 128) + kk * 32;
+              mmaTf32Tmem(acc2, alo, descSw128(bhi), idesc2, acc);
+              mmaTf32Tmem(acc2, ahi, descSw128(blo), idesc2, 1);
+              mmaTf32Tmem(acc2, ahi, descSw128(bhi), idesc2, 1);
+            } else {
+              mmaTf32Tmem(acc2, ahi, descSw128(bhi), idesc2, acc);
+            }
+          }
+        }
+        mmaCommit(l2Done);
+      }
+      // layer-2 epilogue: accumulator rows -> shared memory (the A2 region is
+      // free once the MMAs completed) -> bias + ReLU, coalesced row stores
+      // (per-lane row stores cost ~8.7 us)
+      float* o2s = reinterpret_cast<float*>(a2);  // [128][N2p + 4]
+      const int ld2 = p.N2p + 4;
+      if (warp >= 4) {
+        mbarWait(l2Done, 0, 9);
+        tcFenceAfter();
+        const int row = (warp - 4) * 32 + lane;
+        const uint32_t trow = acc2 + (static_cast<uint32_t>((warp - 4) * 32) << 16);
+        for (int c = 0; c < p.N2p; c += 16) {
+          float v[16];
+          tmemLoad16(trow + c, v);
+          tmemLoadWait();
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(o2s + row * ld2 + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+        tcFenceBefore();
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < p.M * p.N2; e += kThreads) {
+        const int r = e / p.N2, c = e - r * p.N2;
+        p.O2[e] = fmaxf(p.bias2[c] + o2s[r * ld2 + c], 0.f);
+      }
+    }
+  }
   if (warp == 2) {
     tcFenceAfter();
     tmemFree<Cfg::kTmemCols>(tmem);
@@ -327,11 +484,11 @@ bool makeMap(CUtensorMap* m, const float* base, int K, int rows, int batch, int6
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, bool X3>
-cudaError_t launchT(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p, int tilesN, int tilesM,
-                    int batch, cudaStream_t s) {
-  using Cfg = TcCfg<BN, X3>;
-  auto kern = tc_gemm_kernel<BN, X3>;
+template <int BN, bool X3, bool L2 = false>
+cudaError_t launchT(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tw2, const TcParams& p,
+                    int tilesN, int tilesM, int batch, cudaStream_t s) {
+  using Cfg = TcCfg<BN, X3, L2>;
+  auto kern = tc_gemm_kernel<BN, X3, L2>;
   // function attributes belong to a device context: set once per device
   // (bit d of `done`), never once per process
   static std::atomic<uint64_t> done{0};
@@ -356,18 +513,18 @@ cudaError_t launchT(const CUtensorMap& ta, const CUtensorMap& tb, const TcParams
   attr[0].val.clusterDim.z = p.splits;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, tw2, p);
 }
 
 template <bool X3>
 cudaError_t dispatchBn(int bn, const CUtensorMap& ta, const CUtensorMap& tb, const TcParams& p, int tilesN,
                        int tilesM, int batch, cudaStream_t s) {
   switch (bn) {
-    case 16: return launchT<16, X3>(ta, tb, p, tilesN, tilesM, batch, s);
-    case 32: return launchT<32, X3>(ta, tb, p, tilesN, tilesM, batch, s);
-    case 64: return launchT<64, X3>(ta, tb, p, tilesN, tilesM, batch, s);
-    case 128: return launchT<128, X3>(ta, tb, p, tilesN, tilesM, batch, s);
-    case 256: return launchT<256, X3>(ta, tb, p, tilesN, tilesM, batch, s);
+    case 16: return launchT<16, X3>(ta, tb, ta, p, tilesN, tilesM, batch, s);
+    case 32: return launchT<32, X3>(ta, tb, ta, p, tilesN, tilesM, batch, s);
+    case 64: return launchT<64, X3>(ta, tb, ta, p, tilesN, tilesM, batch, s);
+    case 128: return launchT<128, X3>(ta, tb, ta, p, tilesN, tilesM, batch, s);
+    case 256: return launchT<256, X3>(ta, tb, ta, p, tilesN, tilesM, batch, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -433,7 +590,7 @@ cudaError_t launchTcGemm(const GemmArgs& a, int math, const TcPlan& pl, cudaStre
   CUtensorMap ta, tb;
   if (!makeMap(&ta, a.A, a.K, a.M, a.sA ? a.batch : 1, a.lda, a.sA, kBM)) return cudaErrorInvalidValue;
   if (!makeMap(&tb, a.B, a.K, a.N, a.sB ? a.batch : 1, a.ldb, a.sB, bn)) return cudaErrorInvalidValue;
-  TcParams p;
+  TcParams p{};
   p.C = a.C;
   p.bias = a.bias;
   p.M = a.M;
@@ -474,6 +631,72 @@ cudaError_t launchTcGemm(const GemmArgs& a, int math, const TcPlan& pl, cudaStre
   }
   return math == kMath3xTf32 ? dispatchBn<true>(bn, ta, tb, p, tilesN, tilesM, a.batch, s)
                              : dispatchBn<false>(bn, ta, tb, p, tilesN, tilesM, a.batch, s);
+}
+
+// ---- two FC layers in one launch (2FCRelu in tensor-core math): layer 1 is
+// the split-K cluster GEMM above (bias + ReLU epilogue, O1 stored); every
+// rank also writes its reduced O1 rows into rank 0's shared memory as layer
+// 2's K-major A operand, and rank 0 then runs layer 2 (M = 128, N = N2, K =
+// N1) on the tensor cores with W2 landed by TMA behind layer 1's epilogue.
+bool tcFc2Supported(const FcChainArgs& a, int math, const char** why) {
+  auto no = [&](const char* w) {
+    if (why) *why = w;
+    return false;
+  };
+  if (math != kMathTf32 && math != kMath3xTf32) return no("fused 2-layer FC: tensor-core math only");
+  if (a.layers != 2) return no("fused 2-layer FC: exactly two layers");
+  const FcLayer &L1 = a.L[0], &L2 = a.L[1];
+  if (a.batch < 1 || a.batch > kBM) return no("fused 2-layer FC: at most 128 rows");
+  if (L1.out < 1 || L1.out > 128 || L1.out % 32) return no("fused 2-layer FC: layer 1 width a multiple of 32, <= 128");
+  if (L2.kred != L1.out) return no("fused 2-layer FC: layer 2 reduces over layer 1's width");
+  if (L2.out < 1 || L2.out > (math == kMath3xTf32 ? 64 : 128)) return no("fused 2-layer FC: layer 2 too wide");
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (a.ldi % 4 || L1.ldw % 4 || L2.ldw % 4 || !al16(a.I) || !al16(L1.W) || !al16(L2.W))
+    return no("fused 2-layer FC: 16-byte operand rows");
+  return true;
+}
+
+cudaError_t launchTcFc2(const FcChainArgs& a, int math, int sms, cudaStream_t s) {
+  if (!tcFc2Supported(a, math, nullptr)) return cudaErrorInvalidValue;
+  const FcLayer &L1 = a.L[0], &L2 = a.L[1];
+  const int bn = L1.out <= 32 ? 32 : L1.out <= 64 ? 64 : 128;
+  TcParams p{};
+  p.C = L1.O;
+  p.bias = L1.bias;
+  p.M = a.batch;
+  p.N = L1.out;
+  p.K = L1.kred;
+  p.ldc = L1.out;
+  p.sC = 0;
+  p.init = kInitBias;
+  p.relu = 1;
+  p.nkb = (L1.kred + kBK - 1) / kBK;
+  p.splits = tcGemmPlan(1, a.batch, L1.out, L1.kred, sms).splits;
+  p.splits = std::min(std::max(1, p.splits), std::min(8, p.nkb));
+  while (p.splits & (p.splits - 1)) --p.splits;
+  p.kbPerSplit = (p.nkb + p.splits - 1) / p.splits;
+  while (p.splits > 1 && (p.splits - 1) * p.kbPerSplit >= p.nkb) {
+    p.splits /= 2;
+    p.kbPerSplit = (p.nkb + p.splits - 1) / p.splits;
+  }
+  p.aBatched = p.bBatched = 0;
+  p.packP = 0;
+  p.batch = 1;
+  p.O2 = L2.O;
+  p.bias2 = L2.bias;
+  p.N2 = L2.out;
+  p.N2p = (L2.out + 15) / 16 * 16;
+  p.K2p = L1.out;
+  CUtensorMap ta, tb, tw;
+  if (!makeMap(&ta, a.I, L1.kred, a.batch, 1, a.ldi, 0, kBM)) return cudaErrorInvalidValue;
+  if (!makeMap(&tb, L1.W, L1.kred, L1.out, 1, L1.ldw, 0, bn)) return cudaErrorInvalidValue;
+  if (!makeMap(&tw, L2.W, L2.kred, L2.out, 1, L2.ldw, 0, p.N2p)) return cudaErrorInvalidValue;
+  const bool x3 = math == kMath3xTf32;
+  switch (bn) {
+    case 32: return x3 ? launchT<32, true, true>(ta, tb, tw, p, 1, 1, 1, s) : launchT<32, false, true>(ta, tb, tw, p, 1, 1, 1, s);
+    case 64: return x3 ? launchT<64, true, true>(ta, tb, tw, p, 1, 1, 1, s) : launchT<64, false, true>(ta, tb, tw, p, 1, 1, 1, s);
+    default: return x3 ? launchT<128, true, true>(ta, tb, tw, p, 1, 1, 1, s) : launchT<128, false, true>(ta, tb, tw, p, 1, 1, 1, s);
+  }
 }
 
 }  // namespace k

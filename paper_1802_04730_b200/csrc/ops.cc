@@ -117,9 +117,12 @@ void decodeTc(const Problem& p, const MappingOptions& o, Mapping& m) {
     }
   }
   m.fused = false;
-  if (p.family == Family::FcChain && !(o.tileSizes.size() > 2 && o.tileSizes[2] == 1)) {
+  const int64_t fcMode = o.tileSizes.size() > 2 ? o.tileSizes[2] : 0;
+  if (p.family == Family::FcChain && fcMode != 1) {
     // the one-kernel chain where every layer fits it (tile_sizes[2] == 1
-    // asks for the per-layer tc_gemm launches instead)
+    // asks for the per-layer tc_gemm launches instead; == 2 for the fused
+    // two-layer split-K kernel, a tunable: 2FCRelu TF32 13.8 vs 11.6 us per
+    // layer, profiles/r02_tcfc2.txt)
     k::FcChainArgs a{};
     a.layers = static_cast<int>(p.fc.layers.size());
     a.ldi = p.fc.ldi;
@@ -128,6 +131,13 @@ void decodeTc(const Problem& p, const MappingOptions& o, Mapping& m) {
       a.L[l].out = p.fc.layers[l].out;
       a.L[l].kred = p.fc.layers[l].kred;
       a.L[l].ldw = p.fc.layers[l].ldw;
+    }
+    if (fcMode == 2) {
+      const char* why = nullptr;
+      if (!k::tcFc2Supported(a, m.math, &why)) invalid(why);
+      m.tcFused = true;
+      m.tcFc2 = true;
+      return;
     }
     if (k::tcFcFusedSupported(a, m.math, nullptr)) {  // (null pointers pass the alignment checks)
       m.tcFused = true;
@@ -301,6 +311,8 @@ std::string Mapping::describe() const {
       return os.str() + (gconvVariant == 1   ? " implicit-GEMM (on-chip im2col)"
                          : gconvVariant == 2 ? " implicit-GEMM (shifted halo)"
                                              : " implicit-GEMM (NHWC staging)");
+    if (family == Family::FcChain && tcFused && tcFc2)
+      return os.str() + " fused 2-layer (split-K cluster; layer 2 in rank 0 from the reduced rows)";
     if (family == Family::FcChain && tcFused) return os.str() + " fused chain (TMEM -> next layer's A in smem)";
     if (tcAuto) os << " planned";
     else os << " bn=" << tc.bn << " splits=" << tc.splits;
@@ -992,7 +1004,8 @@ void launch(const Problem& p, const Mapping& m, void* const* in, void* const* ou
           a.L[l].kred = L.kred;
           a.L[l].ldw = L.ldw;
         }
-        check(k::launchTcFcFused(a, m.math, s), "fused tensor-core FC chain");
+        check(m.tcFc2 ? k::launchTcFc2(a, m.math, smCount(), s) : k::launchTcFcFused(a, m.math, s),
+              "fused tensor-core FC chain");
         return;
       }
       if (!m.fused) {

@@ -84,6 +84,7 @@ struct Mapping {
   k::TcPlan tc;  // tensor-core tile plan (math != FFMA); per-layer plans are derived at launch
   bool tcAuto = true;
   bool tcFused = false;  // FC chains in tensor-core math: the one-kernel chain (tc_fc_fused.cu)
+  bool tcFc2 = false;    // ... or the fused two-layer split-K kernel (tc_gemm.cu, launchTcFc2)
   // Gemm (and unfused FC layers)
   int gemmVariant = 4, gemmThreads = 0;
   // FcChain

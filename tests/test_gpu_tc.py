@@ -134,6 +134,29 @@ def test_tbmm_tc(env, shape, math):
 
 
 @pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("shape", [(128, 1128, 128, 64), (77, 300, 96, 40), (16, 64, 32, 2)])
+def test_fc2_fused_tc(env, math, shape):
+    """The fused two-layer tcgen05 kernel (tile_sizes[2] == 2: layer 1 split-K
+    over a cluster, its reduced rows bulk-copied into rank 0, layer 2 there):
+    both layers within the emulation bound at the paper shape and ragged ones
+    (rows < 128, layer-2 width not a multiple of 16, a short last k-block)."""
+    ee, orc = env
+    B, K, N1, N2 = shape
+    rng = orc.rng(7 + B)
+    I, W1, B1 = rng.f32((B, K)), rng.f32((N1, K)), rng.f32((N1,))
+    W2, B2 = rng.f32((N2, N1)), rng.f32((N2,))
+    opts = {"block_shape": [1, 1, 1], "fusion_strategy": "max", "rng_seed": 0, "shared_memory_budget": 49152,
+            "thread_shape": [256, 1, 1], "tile_sizes": [128, 1, 2], "unroll_copy_shared": False,
+            "unroll_factor": 1, "use_private": False, "use_shared": True}
+    (h1, h2), desc = run(ee, "2FCRelu", [I, W1, B1, W2, B2], [np.zeros((B, N1), np.float32),
+                                                              np.zeros((B, N2), np.float32)], math, opts)
+    assert "fused 2-layer" in desc["kernel"]
+    ee1, eb1 = check_emu(f"fc2 {shape} layer 1", math, K, h1, emu.fc_relu(I, W1, B1, math))
+    ee2, eb2 = check_emu(f"fc2 {shape} layer 2", math, N1, h2, emu.fc_relu(h1, W2, B2, math), opscale(h1, W2))
+    record(f"fc2 fused {shape} layer 2", math, N1, max_rel(orc.fc_relu(h1, W2, B2), h2), None, None, ee2, eb2)
+
+
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
 def test_fc_chains_tc(env, math):
     ee, orc = env
     rng = orc.rng(99)
