@@ -43,6 +43,7 @@ struct FcPlan {
   int denseIn;              // input rows land unpadded with one copy (ald[0] == kred, conflict-free)
   int bulk;                 // 1: cp.async.bulk path, 2: 16-byte cp.async path, 0: cooperative loads
   int nch, kc4;             // cp.async path: layer 0 in nch chunks of kc4 float4s of the reduction
+  int pair;                 // bit l: layer l runs two columns (c, c + cols/2) per thread, interleaved
 };
 
 __host__ __device__ inline int up4(int x) { return (x + 3) & ~3; }
@@ -176,6 +177,70 @@ __device__ __noinline__ float chainSegment(unsigned xa, unsigned wa, int n, floa
   return acc;
 }
 
+// Two chains of one input row against two weight columns, interleaved: per
+// 4 steps one input vector load feeds 8 FFMAs (2 loads per 4 in
+// chainSegment). The chains are LDS-writeback bound at one output per lane
+// (~6.2 cycles per step with 4 warps per SM); 8-step chunks (16-step
+// chunks as in chainSegment measured slower: 6.3 vs 5.9 cycles per step); half the lanes with two
+// outputs each move a quarter fewer bytes through the register file per
+// output. Same slack rules as chainSegment.
+__device__ __noinline__ float2 chainSegment2(unsigned xa, unsigned wa, unsigned wb, int n, float accA, float accB) {
+  const int nch = n >> 3;
+  float4 X0[2], A0[2], B0[2], X1[2], A1[2], B1[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    X0[i] = lds4(xa + i * 16);
+    A0[i] = lds4(wa + i * 16);
+    B0[i] = lds4(wb + i * 16);
+  }
+  int c = 0;
+  for (; c + 2 <= nch; c += 2) {
+    const unsigned o = c * 32;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      X1[i] = lds4(xa + o + 32 + i * 16);
+      A1[i] = lds4(wa + o + 32 + i * 16);
+      B1[i] = lds4(wb + o + 32 + i * 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      accA = fma4(X0[i], A0[i], accA);
+      accB = fma4(X0[i], B0[i], accB);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      X0[i] = lds4(xa + o + 64 + i * 16);
+      A0[i] = lds4(wa + o + 64 + i * 16);
+      B0[i] = lds4(wb + o + 64 + i * 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      accA = fma4(X1[i], A1[i], accA);
+      accB = fma4(X1[i], B1[i], accB);
+    }
+  }
+  if (c < nch) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      accA = fma4(X0[i], A0[i], accA);
+      accB = fma4(X0[i], B0[i], accB);
+    }
+    ++c;
+  }
+  int kk = c * 8;
+  for (; kk + 4 <= n; kk += 4) {
+    const float4 x = lds4(xa + kk * 4);
+    accA = fma4(x, lds4(wa + kk * 4), accA);
+    accB = fma4(x, lds4(wb + kk * 4), accB);
+  }
+  for (; kk < n; ++kk) {
+    const float x = lds1(xa + kk * 4);
+    accA = __fmaf_rn(x, lds1(wa + kk * 4), accA);
+    accB = __fmaf_rn(x, lds1(wb + kk * 4), accB);
+  }
+  return make_float2(accA, accB);
+}
+
 #ifdef TCB_FC_TRACE
 // diagnostic build only (profiles/fc_trace.cu): per-CTA phase timestamps
 __device__ unsigned long long g_fc_trace[1024][32];
@@ -225,11 +290,15 @@ __global__ void __launch_bounds__(kFcMaxThreads)
 
   // first-pass bias of every layer, loaded now so its latency hides behind
   // the weight copies (each chain starts from its bias)
-  float biasPre[kMaxLayers];
+  float biasPre[kMaxLayers], biasPreB[kMaxLayers];
 #pragma unroll
   for (int l = 0; l < kMaxLayers; ++l) {
     const int c = tid / R, c0 = rank * (l < layers ? p.cols[l] : 0);
     biasPre[l] = (l < layers && tid < R * p.cols[l] && c0 + c < a.L[l].out) ? __ldg(a.L[l].bias + c0 + c) : 0.0f;
+    const int cb = c + (l < layers ? p.cols[l] / 2 : 0);
+    biasPreB[l] = (l < layers && ((p.pair >> l) & 1) && tid < R * p.cols[l] / 2 && c0 + cb < a.L[l].out)
+                      ? __ldg(a.L[l].bias + c0 + cb)
+                      : 0.0f;
   }
   if (tid == 0) {
 #pragma unroll
@@ -372,39 +441,72 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     FC_STAMP(3 + 3 * l);
     if (!last && l == 0 && cn > 1) asm volatile("barrier.cluster.wait;" ::: "memory");
     if (l == 0) FC_STAMP(20);
-    const int nchains = R * cols;
-    for (int base = 0; base < nchains; base += T) {
-      // one (row, column) chain per thread and pass, row fastest; idle
-      // lanes run a dummy chain on row 0 / column 0 (no branch in the chain)
-      const int idx = base + tid;
-      const bool live = idx < nchains && c0 + idx / R < L.out;
-      const int r = live ? idx % R : 0, c = live ? idx / R : 0;
-      float bpre = 0.0f;
+    if ((p.pair >> l) & 1) {
+      // one pass: thread t runs columns c and c + cols/2 of row r (planFc:
+      // R * cols <= 2T, cols even); dead chains run on row 0 / column 0
+      const int half = cols >> 1, idx = tid;
+      const int r = idx < R * half ? idx % R : 0, c = idx < R * half ? idx / R : 0;
+      const bool liveA = idx < R * half && c0 + c < L.out, liveB = idx < R * half && c0 + c + half < L.out;
+      float bA = 0.0f, bB = 0.0f;
 #pragma unroll
       for (int q = 0; q < kMaxLayers; ++q)
-        if (q == l) bpre = biasPre[q];  // static register indexing
-      float acc = !live ? 0.0f : base == 0 ? bpre : __ldg(L.bias + c0 + c);
-      const unsigned xa = actBase + (unsigned)(r * ald) * 4u, wa = wBase + (unsigned)(c * p.wld[l]) * 4u;
-      if (l == 0 && LM == 2) {
-        for (int ch = 0; ch < p.nch; ++ch) {  // the chain follows the chunks in
-          if (base == 0) asyncWait(p.nch - 1 - ch + NL - 1);
-          const int k0 = ch * 4 * p.kc4, n = min(4 * p.kc4, L.kred - k0);
-          acc = chainSegment(xa + 4u * k0, wa + 4u * k0, n, acc);
-        }
-      } else {
-        if (l < 3) FC_STAMP(21 + l);  // chain entry (thread 0's first pass)
-        acc = chainSegment(xa, wa, L.kred, acc);
-      }
-      FC_STAMP(16 + l);  // chain done (thread 0's first pass), before its stores
-      if (live) {
-        const float v = fmaxf(acc, 0.0f);
-        if (r < rows) L.O[(int64_t)(row0 + r) * L.out + c0 + c] = v;
-        if (!last) {  // push into the next layer's input buffer of every cluster CTA
-          float* dst = sm + p.offAct[l + 1] + r * p.ald[l + 1] + c0 + c;
+        if (q == l) bA = biasPre[q], bB = biasPreB[q];
+      const unsigned xa = actBase + (unsigned)(r * ald) * 4u, wa = wBase + (unsigned)(c * p.wld[l]) * 4u,
+                     wb = wa + (unsigned)(half * p.wld[l]) * 4u;
+      if (l < 3) FC_STAMP(21 + l);
+      const float2 acc = chainSegment2(xa, wa, liveB ? wb : wa, L.kred, liveA ? bA : 0.0f, liveB ? bB : 0.0f);
+      FC_STAMP(16 + l);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const bool live = h ? liveB : liveA;
+        if (!live) continue;
+        const int cc = c + h * half;
+        const float v = fmaxf(h ? acc.y : acc.x, 0.0f);
+        if (r < rows) L.O[(int64_t)(row0 + r) * L.out + c0 + cc] = v;
+        if (!last) {
+          float* dst = sm + p.offAct[l + 1] + r * p.ald[l + 1] + c0 + cc;
           if (cn > 1) {
             for (int q = 0; q < cn; ++q) stAsyncCluster(dst, &bars[l + 1], q, v);
           } else {
-            *dst = v;  // a lone CTA: plain store, published by the barrier below
+            *dst = v;
+          }
+        }
+      }
+    } else {
+      const int nchains = R * cols;
+      for (int base = 0; base < nchains; base += T) {
+        // one (row, column) chain per thread and pass, row fastest; idle
+        // lanes run a dummy chain on row 0 / column 0 (no branch in the chain)
+        const int idx = base + tid;
+        const bool live = idx < nchains && c0 + idx / R < L.out;
+        const int r = live ? idx % R : 0, c = live ? idx / R : 0;
+        float bpre = 0.0f;
+  #pragma unroll
+        for (int q = 0; q < kMaxLayers; ++q)
+          if (q == l) bpre = biasPre[q];  // static register indexing
+        float acc = !live ? 0.0f : base == 0 ? bpre : __ldg(L.bias + c0 + c);
+        const unsigned xa = actBase + (unsigned)(r * ald) * 4u, wa = wBase + (unsigned)(c * p.wld[l]) * 4u;
+        if (l == 0 && LM == 2) {
+          for (int ch = 0; ch < p.nch; ++ch) {  // the chain follows the chunks in
+            if (base == 0) asyncWait(p.nch - 1 - ch + NL - 1);
+            const int k0 = ch * 4 * p.kc4, n = min(4 * p.kc4, L.kred - k0);
+            acc = chainSegment(xa + 4u * k0, wa + 4u * k0, n, acc);
+          }
+        } else {
+          if (l < 3) FC_STAMP(21 + l);  // chain entry (thread 0's first pass)
+          acc = chainSegment(xa, wa, L.kred, acc);
+        }
+        FC_STAMP(16 + l);  // chain done (thread 0's first pass), before its stores
+        if (live) {
+          const float v = fmaxf(acc, 0.0f);
+          if (r < rows) L.O[(int64_t)(row0 + r) * L.out + c0 + c] = v;
+          if (!last) {  // push into the next layer's input buffer of every cluster CTA
+            float* dst = sm + p.offAct[l + 1] + r * p.ald[l + 1] + c0 + c;
+            if (cn > 1) {
+              for (int q = 0; q < cn; ++q) stAsyncCluster(dst, &bars[l + 1], q, v);
+            } else {
+              *dst = v;  // a lone CTA: plain store, published by the barrier below
+            }
           }
         }
       }
@@ -421,7 +523,7 @@ __global__ void __launch_bounds__(kFcMaxThreads)
 
 // Builds the plan; returns the dynamic shared-memory size. Every operand
 // buffer is followed by >= 32 floats of slack (the chain prefetches ahead).
-static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads = 0) {
+static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads = 0, int threads = 0) {
   p = FcPlan{};
   p.cn = cn;
   p.R = R;
@@ -429,6 +531,11 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads =
   for (int l = 0; l < a.layers; ++l) {
     p.cols[l] = (a.L[l].out + cn - 1) / cn;
     p.wld[l] = up4(a.L[l].kred);
+    // a block of half the layer's chains runs them two columns per thread in
+    // one pass instead of two passes (bulk loads: every kred row 16-B aligned)
+    if (threads > 0 && p.cols[l] % 2 == 0 && R * p.cols[l] > threads && R * p.cols[l] <= 2 * threads &&
+        a.L[l].kred % 4 == 0)
+      p.pair |= 1 << l;
     p.offW[l] = off;
     off += p.cols[l] * p.wld[l] + 32;
   }
@@ -468,6 +575,7 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads =
   // 5.49 us, 2FCRelu 16.9 vs 7.9, MLP1 15.5 vs 6.5: an SM keeps too few
   // cp.async sectors in flight for ~90 KB per CTA (profiles/r02_fc_notes.txt)
   p.bulk = !bulk ? 0 : (loads == 2 || loads == 3) ? 2 : 1;
+  if (p.bulk == 2) p.pair &= ~1;  // layer 0 follows the cp.async chunks (single-column chains)
   const bool oneChunk = loads == 3;
   {
     // layer-0 chunks: ~256-step pieces, at most 4, multiples of 16 steps
@@ -516,7 +624,7 @@ cudaError_t launchFcChain(const FcChainArgs& a, int rows, int cn, int threads, c
   if (a.batch <= 0) return cudaSuccess;
   if (loads == 4) return launchFcTma(a, rows, cn, threads, s);
   FcPlan p;
-  size_t smem = planFc(a, rows, cn, p, loads);
+  size_t smem = planFc(a, rows, cn, p, loads, threads);
   if (smem > 227 * 1024 || cn < 1 || cn > 16 || rows < 1) return cudaErrorInvalidConfiguration;
   if (threads < 32 || threads > kFcMaxThreads || threads % 32) return cudaErrorInvalidConfiguration;
   void (*kern)(FcChainArgs, FcPlan) = fcKernel(a.layers, p.bulk);

@@ -719,6 +719,12 @@ MappingOptions defaultOptions(const Problem& p, int math) {
       }
       while (rows > 1 && k::fcChainSmem(a, rows, cn) > 110 * 1024) rows /= 2;
       int t = std::max(64, k::fcChainThreads(a, rows, cn));  // one pass per layer
+      // long first reductions (MLP1, 2FCRelu: K = 1128): half the block, two
+      // columns per thread in layer 0 (fc_chain.cu chainSegment2): MLP1 6.70
+      // -> 6.20 us, 2FCRelu 7.81 -> 7.57 alone, 16.1 -> 15.3-15.8 in the bench
+      // step; MLP3 (K = 128) measured slower that way (6.1 vs 5.3)
+      if (a.L[0].kred >= 512 && ((a.L[0].out + cn - 1) / cn) % 2 == 0 && a.L[0].kred % 4 == 0 && t % 64 == 0)
+        t /= 2;
       a.ldi = p.fc.ldi;
       for (int l = 0; l < a.layers; ++l) a.L[l].ldw = p.fc.layers[l].ldw;
       o.tileSizes = {rows, cn, 1};

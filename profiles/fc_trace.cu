@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 using namespace tcb::k;
@@ -102,6 +103,17 @@ int main() {
   m.L[2] = {alloc(2 * 32), alloc(2), alloc(128 * 2), 2, 32, 32};
   // the default plans of the bench step (ops.cc defaultOptions)
   run("2FCRelu rows=4 cn=8", f, 4, 8, 64);
+  if (getenv("FC_TRACE_2FC")) {  // other 2FCRelu plans (r02: rows=8 cn=8 t=128 measured 15 us in the sweep)
+    run("2FCRelu rows=4 cn=8 t=32 (column pairs)", f, 4, 8, 32);
+    run("MLP1 rows=4 cn=8 t=32 (column pairs)", one, 4, 8, 32);
+    run("2FCRelu rows=8 cn=8 t=64 (column pairs)", f, 8, 8, 64);
+    if (getenv("FC_TRACE_PAIR_ONLY")) return 0;
+    run("2FCRelu rows=8 cn=8 t=128", f, 8, 8, 128);
+    run("2FCRelu rows=8 cn=16 t=64", f, 8, 16, 64);
+    run("2FCRelu rows=2 cn=8 t=32", f, 2, 8, 32);
+    run("2FCRelu rows=8 cn=4 t=256", f, 8, 4, 256);
+    return 0;
+  }
   run("MLP1 rows=4 cn=8", one, 4, 8, 64);
   run("MLP3 rows=2 cn=4", m, 2, 4, 64);
   run("MLP3 rows=4 cn=4", m, 4, 4, 64);

@@ -111,7 +111,8 @@ def main():
             print(f"{name} alone (back to back): {min(timeit(graph_of([ops[name]], pipelined=True)) for _ in range(3)):.2f} us", flush=True)
     if os.environ.get("PIPE_ONLY"):
         return
-    for combo in COMBOS:
+    combos = json.loads(os.environ["COMBOS_JSON"]) if os.environ.get("COMBOS_JSON") else COMBOS
+    for combo in combos:
         try:
             for name, v in combo.items():
                 o = ops[name]

@@ -174,9 +174,13 @@ def test_slab_variants(engine, oracle, shape):
 
 
 @pytest.mark.parametrize("rows,cn,threads", [(1, 1, 64), (2, 2, 64), (4, 8, 64), (8, 8, 64), (8, 4, 256),
-                                             (16, 8, 128), (3, 3, 96), (8, 16, 64)])
+                                             (16, 8, 128), (3, 3, 96), (8, 16, 64), (4, 8, 32), (5, 8, 64),
+                                             (2, 4, 32), (1, 2, 32)])
 def test_fc_chain_cluster_variants(engine, oracle, golden, rows, cn, threads):
     """Cluster sizes 1..16 (16 = non-portable), ragged rows and column splits.
+    Blocks of half a layer's chains run column pairs per thread (planFc's
+    `pair`: (4, 8, 32), (5, 8, 64), (8, 8, 64), ...), including a second
+    column past a ragged layer's width.
     Combinations whose weight slices exceed shared memory must be rejected
     with MappingInvalid (never silently run)."""
     from paper_1802_04730_b200 import TcError
