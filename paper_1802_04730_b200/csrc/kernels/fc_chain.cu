@@ -43,7 +43,7 @@ struct FcPlan {
   int denseIn;              // input rows land unpadded with one copy (ald[0] == kred, conflict-free)
   int bulk;                 // 1: cp.async.bulk path, 2: 16-byte cp.async path, 0: cooperative loads
   int nch, kc4;             // cp.async path: layer 0 in nch chunks of kc4 float4s of the reduction
-  int pair;                 // bit l: layer l runs two columns (c, c + cols/2) per thread, interleaved
+  int pair;                 // 1: layer 0 runs two columns (c, c + cols/2) per thread, interleaved
 };
 
 __host__ __device__ inline int up4(int x) { return (x + 3) & ~3; }
@@ -290,16 +290,16 @@ __global__ void __launch_bounds__(kFcMaxThreads)
 
   // first-pass bias of every layer, loaded now so its latency hides behind
   // the weight copies (each chain starts from its bias)
-  float biasPre[kMaxLayers], biasPreB[kMaxLayers];
+  float biasPre[kMaxLayers];
 #pragma unroll
   for (int l = 0; l < kMaxLayers; ++l) {
     const int c = tid / R, c0 = rank * (l < layers ? p.cols[l] : 0);
     biasPre[l] = (l < layers && tid < R * p.cols[l] && c0 + c < a.L[l].out) ? __ldg(a.L[l].bias + c0 + c) : 0.0f;
-    const int cb = c + (l < layers ? p.cols[l] / 2 : 0);
-    biasPreB[l] = (l < layers && ((p.pair >> l) & 1) && tid < R * p.cols[l] / 2 && c0 + cb < a.L[l].out)
-                      ? __ldg(a.L[l].bias + c0 + cb)
-                      : 0.0f;
   }
+  // layer 0's second column (column pairs, planFc `pair`)
+  const float biasPreB = (NL <= 2 && (p.pair & 1) && tid < R * (p.cols[0] / 2) && rank * p.cols[0] + tid / R + p.cols[0] / 2 < a.L[0].out)
+                             ? __ldg(a.L[0].bias + rank * p.cols[0] + tid / R + p.cols[0] / 2)
+                             : 0.0f;
   if (tid == 0) {
 #pragma unroll
     for (int b = 0; b < 2 * layers; ++b) mbarInit(&bars[b], 1);
@@ -441,16 +441,15 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     FC_STAMP(3 + 3 * l);
     if (!last && l == 0 && cn > 1) asm volatile("barrier.cluster.wait;" ::: "memory");
     if (l == 0) FC_STAMP(20);
-    if ((p.pair >> l) & 1) {
+    // (column pairs only in 1- and 2-layer chains: the extra code path cost
+    // the 3-layer kernel register spills)
+    if (NL <= 2 && l == 0 && (p.pair & 1)) {
       // one pass: thread t runs columns c and c + cols/2 of row r (planFc:
       // R * cols <= 2T, cols even); dead chains run on row 0 / column 0
       const int half = cols >> 1, idx = tid;
       const int r = idx < R * half ? idx % R : 0, c = idx < R * half ? idx / R : 0;
       const bool liveA = idx < R * half && c0 + c < L.out, liveB = idx < R * half && c0 + c + half < L.out;
-      float bA = 0.0f, bB = 0.0f;
-#pragma unroll
-      for (int q = 0; q < kMaxLayers; ++q)
-        if (q == l) bA = biasPre[q], bB = biasPreB[q];
+      const float bA = biasPre[0], bB = biasPreB;  // (layer 0 only)
       const unsigned xa = actBase + (unsigned)(r * ald) * 4u, wa = wBase + (unsigned)(c * p.wld[l]) * 4u,
                      wb = wa + (unsigned)(half * p.wld[l]) * 4u;
       if (l < 3) FC_STAMP(21 + l);
@@ -533,9 +532,9 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads =
     p.wld[l] = up4(a.L[l].kred);
     // a block of half the layer's chains runs them two columns per thread in
     // one pass instead of two passes (bulk loads: every kred row 16-B aligned)
-    if (threads > 0 && p.cols[l] % 2 == 0 && R * p.cols[l] > threads && R * p.cols[l] <= 2 * threads &&
+    if (l == 0 && a.layers <= 2 && threads > 0 && p.cols[l] % 2 == 0 && R * p.cols[l] > threads && R * p.cols[l] <= 2 * threads &&
         a.L[l].kred % 4 == 0)
-      p.pair |= 1 << l;
+      p.pair = 1;
     p.offW[l] = off;
     off += p.cols[l] * p.wld[l] + 32;
   }
@@ -575,7 +574,7 @@ static size_t planFc(const FcChainArgs& a, int R, int cn, FcPlan& p, int loads =
   // 5.49 us, 2FCRelu 16.9 vs 7.9, MLP1 15.5 vs 6.5: an SM keeps too few
   // cp.async sectors in flight for ~90 KB per CTA (profiles/r02_fc_notes.txt)
   p.bulk = !bulk ? 0 : (loads == 2 || loads == 3) ? 2 : 1;
-  if (p.bulk == 2) p.pair &= ~1;  // layer 0 follows the cp.async chunks (single-column chains)
+  if (p.bulk == 2) p.pair = 0;  // layer 0 follows the cp.async chunks (single-column chains)
   const bool oneChunk = loads == 3;
   {
     // layer-0 chunks: ~256-step pieces, at most 4, multiples of 16 steps
