@@ -288,6 +288,48 @@ __global__ void __launch_bounds__(kFcMaxThreads)
   // bars[l]: layer l's input activations landed; bars[layers + l]: layer l's weight slice landed
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + p.offBar);
 
+  if (tid == 0) {
+#pragma unroll
+    for (int b = 0; b < 2 * layers; ++b) mbarInit(&bars[b], 1);
+    // the pushed activations of every later layer: R rows x all columns
+    // (armed before any peer can push: see the cluster arrive below)
+    if (cn > 1)
+#pragma unroll
+      for (int l = 1; l < layers; ++l) mbarExpectTx(&bars[l], (unsigned)(R * a.L[l - 1].out * 4));
+    FC_STAMP(1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    FC_STAMP(5);
+    if (LM == 1) {
+      // bulk loads: thread 0 arms and issues every copy before anything else
+      // touches the parameters (each first read of a parameter line is a
+      // ~270-cycle constant-cache miss on the way to the first copy)
+      const unsigned rowBytes = (unsigned)a.L[0].kred * 4u;
+      mbarExpectTx(&bars[0], rowBytes * rows);
+      if (p.denseIn) {  // the CTA's input rows are one contiguous block
+        bulkCopy(sm + p.offAct[0], a.I + (int64_t)row0 * a.ldi, rowBytes * rows, &bars[0]);
+      } else {
+        for (int r = 0; r < rows; ++r)
+          bulkCopy(sm + p.offAct[0] + r * p.ald[0], a.I + (int64_t)(row0 + r) * a.ldi, rowBytes, &bars[0]);
+      }
+      FC_STAMP(24);
+#pragma unroll
+      for (int l = 0; l < layers; ++l) {
+        const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
+        mbarExpectTx(&bars[layers + l], (unsigned)(a.L[l].kred * 4 * nc));
+        if (nc == 0) continue;
+        const float* src = a.L[l].W + (int64_t)c0 * a.L[l].ldw;
+        if (l < 4) FC_STAMP(25 + l);
+        if (a.L[l].ldw == a.L[l].kred) {  // the slice is one contiguous block
+          bulkCopy(sm + p.offW[l], src, (unsigned)(nc * a.L[l].kred * 4), &bars[layers + l]);
+        } else {
+          for (int q = 0; q < nc; ++q)
+            bulkCopy(sm + p.offW[l] + q * p.wld[l], src + (int64_t)q * a.L[l].ldw, a.L[l].kred * 4,
+                     &bars[layers + l]);
+        }
+      }
+      FC_STAMP(12);
+    }
+  }
   // first-pass bias of every layer, loaded now so its latency hides behind
   // the weight copies (each chain starts from its bias)
   float biasPre[kMaxLayers];
@@ -300,18 +342,6 @@ __global__ void __launch_bounds__(kFcMaxThreads)
   const float biasPreB = (NL <= 2 && (p.pair & 1) && tid < R * (p.cols[0] / 2) && rank * p.cols[0] + tid / R + p.cols[0] / 2 < a.L[0].out)
                              ? __ldg(a.L[0].bias + rank * p.cols[0] + tid / R + p.cols[0] / 2)
                              : 0.0f;
-  if (tid == 0) {
-#pragma unroll
-    for (int b = 0; b < 2 * layers; ++b) mbarInit(&bars[b], 1);
-    // the pushed activations of every later layer: R rows x all columns
-    // (armed before any peer can push: see the cluster arrive below)
-    if (cn > 1)
-#pragma unroll
-      for (int l = 1; l < layers; ++l) mbarExpectTx(&bars[l], (unsigned)(R * a.L[l - 1].out * 4));
-    FC_STAMP(1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    FC_STAMP(5);
-  }
   __syncthreads();  // inits visible inside the CTA
   FC_STAMP(8);
   // Peers push layer outputs into this CTA's activation buffers and complete
@@ -321,49 +351,12 @@ __global__ void __launch_bounds__(kFcMaxThreads)
   if (cn > 1) asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
   FC_STAMP(11);
 
-  // ---- every global load of the kernel is issued up front. A bulk copy
-  // costs the issuing thread ~200 cycles, so the copies are dealt round-robin
-  // to lane 0 of every warp (copy j -> warp j % warps) and issue in parallel.
+  // ---- every global load of the kernel is issued up front (bulk copies:
+  // by thread 0 right after the barrier inits, above; dealing them
+  // round-robin to the warps' lane 0 bought nothing once a CTA is one or two
+  // warps and the paper chains need three copies)
   if (LM == 1) {
-    const int warp = tid >> 5, nw = (T + 31) >> 5, lane = tid & 31;
-    const unsigned rowBytes = (unsigned)a.L[0].kred * 4u;
-    if (tid == 0) {
-      mbarExpectTx(&bars[0], rowBytes * rows);
-#pragma unroll
-      for (int l = 0; l < layers; ++l) {
-        const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
-        mbarExpectTx(&bars[layers + l], (unsigned)(a.L[l].kred * 4 * nc));
-      }
-    }
-    __syncthreads();  // expectations armed before any copy can complete
-    FC_STAMP(12);
-    if (lane == 0) {
-      int j = 0;  // global copy index
-      if (p.denseIn) {  // the CTA's input rows are one contiguous block
-        if (j++ % nw == warp) bulkCopy(sm + p.offAct[0], a.I + (int64_t)row0 * a.ldi, rowBytes * rows, &bars[0]);
-      } else {
-        for (int r = 0; r < rows; ++r)
-          if (j++ % nw == warp)
-            bulkCopy(sm + p.offAct[0] + r * p.ald[0], a.I + (int64_t)(row0 + r) * a.ldi, rowBytes, &bars[0]);
-      }
-      FC_STAMP(24);
-#pragma unroll
-      for (int l = 0; l < layers; ++l) {
-        const int c0 = rank * p.cols[l], nc = max(0, min(p.cols[l], a.L[l].out - c0));
-        if (nc == 0) continue;
-        const float* src = a.L[l].W + (int64_t)c0 * a.L[l].ldw;
-        if (l < 4) FC_STAMP(25 + l);
-        if (a.L[l].ldw == a.L[l].kred) {  // the slice is one contiguous block
-          if (j++ % nw == warp) bulkCopy(sm + p.offW[l], src, (unsigned)(nc * a.L[l].kred * 4), &bars[layers + l]);
-        } else {
-          for (int q = 0; q < nc; ++q)
-            if (j++ % nw == warp)
-              bulkCopy(sm + p.offW[l] + q * p.wld[l], src + (int64_t)q * a.L[l].ldw, a.L[l].kred * 4,
-                       &bars[layers + l]);
-        }
-      }
-    }
-    // input rows past the batch end are zero
+    // (the copies were issued by thread 0 above) input rows past the batch end are zero
     for (int e = tid; e < (R - rows) * p.ald[0]; e += T) sm[p.offAct[0] + rows * p.ald[0] + e] = 0.0f;
     if (rows < R) __syncthreads();
   } else if (LM == 2) {
