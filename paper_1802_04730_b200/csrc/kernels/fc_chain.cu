@@ -342,6 +342,7 @@ __global__ void __launch_bounds__(kFcMaxThreads)
   const float biasPreB = (NL <= 2 && (p.pair & 1) && tid < R * (p.cols[0] / 2) && rank * p.cols[0] + tid / R + p.cols[0] / 2 < a.L[0].out)
                              ? __ldg(a.L[0].bias + rank * p.cols[0] + tid / R + p.cols[0] / 2)
                              : 0.0f;
+  __syncwarp();      // lane 0 rejoins its warp (compute-sanitizer synccheck: no divergent barrier)
   __syncthreads();  // inits visible inside the CTA
   FC_STAMP(8);
   // Peers push layer outputs into this CTA's activation buffers and complete
@@ -507,6 +508,16 @@ __global__ void __launch_bounds__(kFcMaxThreads)
     if (!last && cn == 1) __syncthreads();
   }
   if (cn > 1 && layers == 1) asm volatile("barrier.cluster.wait;" ::: "memory");  // pair the arrive
+  if (LM == 1 || cn > 1) {
+    // every wait on the barriers is behind us: invalidate them, so the shared
+    // memory they occupied is plain memory again for the next kernel on this
+    // SM (compute-sanitizer synccheck otherwise tracks the stale objects)
+    __syncthreads();
+    if (tid == 0)
+#pragma unroll
+      for (int b = 0; b < 2 * layers; ++b)
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smemAddr(&bars[b])) : "memory");
+  }
   FC_STAMP(15);
   FC_GSTAMP(14);
 }

@@ -315,6 +315,12 @@ __global__ void __launch_bounds__(kFcMaxThreads, 1)
     if (!last && cn == 1) __syncthreads();
   }
   if (cn > 1 && NL == 1) asm volatile("barrier.cluster.wait;" ::: "memory");  // pair the arrive
+  // every wait is behind us: invalidate the barriers (their shared memory is
+  // plain memory again for the next kernel; compute-sanitizer synccheck)
+  __syncthreads();
+  if (tid == 0)
+    for (int b = 0; b < p.nchunk + 1 + 2 * (NL - 1); ++b)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(&bars[b]))) : "memory");
 }
 
 // ------------------------------------------------------------------ host

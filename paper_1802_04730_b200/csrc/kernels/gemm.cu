@@ -240,6 +240,12 @@ __device__ __forceinline__ void bulkG2S(void* dst, const void* src, unsigned byt
       "l"(src), "r"(bytes), "r"(smemU32(bar))
       : "memory");
 }
+// Ends an mbarrier's life once every wait on it is behind us, so its shared
+// memory is plain memory again for the next kernel on the SM
+// (compute-sanitizer synccheck tracks stale barrier objects across kernels).
+__device__ __forceinline__ void barInval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smemU32(bar)) : "memory");
+}
 __device__ __forceinline__ void barWait(uint64_t* bar, unsigned parity) {
   const unsigned addr = smemU32(bar);
   for (unsigned spin = 0;; ++spin) {
@@ -364,6 +370,9 @@ __global__ void __launch_bounds__(512) gemm_nt_batched(const GemmArgs a, const i
       issue(j + S, s);
     }
   }
+  __syncthreads();  // every wait on the ring is behind us
+  if (tid == 0)
+    for (int s = 0; s < S; ++s) barInval(&bars[s]);
 }
 
 // "Slab" GEMM for many small batches (TBMM: 500 x (26x72 · 72x26)). One CTA
@@ -625,6 +634,10 @@ __global__ void __launch_bounds__(256) gemm_nt_slab_rt(const GemmArgs a, const i
       }
     }
   }
+  if (BULK) {  // the fill's barrier: every wait is behind us
+    __syncthreads();
+    if (tid == 0) barInval(&bars[0]);
+  }
   SLAB_STAMP(8);
 #pragma unroll
   for (int i = 0; i < RM; ++i) {
@@ -708,6 +721,8 @@ __global__ void __launch_bounds__(256) gemm_nt_warpbatch(const GemmArgs a, const
   if (dense) {
     __syncwarp();  // lane 0's barrier init before the others poll it
     barWait(bar, 0);
+    __syncwarp();
+    if (lane == 0) barInval(bar);
   } else {
     cp_async_wait<0>();
     __syncwarp();

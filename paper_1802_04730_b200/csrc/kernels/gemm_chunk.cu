@@ -290,6 +290,9 @@ __global__ void __launch_bounds__(256) gemm_nt_wpair(const GemmArgs a, const int
   if (live) {
     WP_STAMP(5, 0ull);
   }
+  if (S > 1) __syncthreads();  // the batch's waits on its barrier are behind us
+  else __syncwarp();
+  if (live && dense && s == 0 && lane == 0) mbarInval(bar);
 }
 
 template <int RM, int S>

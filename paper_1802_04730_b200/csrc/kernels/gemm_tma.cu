@@ -196,7 +196,15 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN) + 32)
         C[(int64_t)m * a.ldc + n] = v;
       }
     }
+  // every wait and arrival on the ring is behind us (the producer warp has
+  // left; peers stop arriving at the cluster barrier): end the barriers
   if (CN > 1) clusterSync();
+  else asm volatile("bar.sync 1, %0;" ::"r"(CT) : "memory");
+  if (tid == 0)
+    for (int s = 0; s < S; ++s) {
+      mbarInval(&full[s]);
+      mbarInval(&empty[s]);
+    }
 }
 
 // ------------------------------------------------------------------ host

@@ -45,6 +45,12 @@ __device__ __forceinline__ uint32_t smem(const void* p) {
 __device__ __forceinline__ void mbarInit(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem(bar)), "r"(count));
 }
+// Ends an mbarrier's life once no wait or arrival on it is pending, so its
+// shared memory is plain memory again for the next kernel on the SM
+// (compute-sanitizer synccheck tracks stale barrier objects across kernels).
+__device__ __forceinline__ void mbarInval(uint64_t* bar) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem(bar)) : "memory");
+}
 __device__ __forceinline__ void fenceBarrierInit() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
