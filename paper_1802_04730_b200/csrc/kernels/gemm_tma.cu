@@ -208,49 +208,9 @@ __global__ void __launch_bounds__((TM / RM) * (TN / RN) + 32)
 }
 
 // ------------------------------------------------------------------ host
-// 3-D map {K, rows, batch} of a row-major fp32 operand, box {32, boxRows, 1},
-// 128-byte swizzle. Encoded maps are cached by (pointer, geometry): graph
-// capture and repeated host calls re-use them (cuTensorMapEncodeTiled costs
-// host time on every synchronised call otherwise).
-struct MapKey {
-  const void* p;
-  int64_t K, rows, batch, ld, sb;
-  int box, dev;
-  bool operator==(const MapKey& o) const {
-    return p == o.p && K == o.K && rows == o.rows && batch == o.batch && ld == o.ld && sb == o.sb && box == o.box &&
-           dev == o.dev;
-  }
-};
-std::mutex g_mapMu;
-std::vector<std::pair<MapKey, CUtensorMap>> g_maps;  // most recent last, <= 128
-
+// operand maps: sm100::cachedMapF32Sw128 (cached by pointer and geometry)
 bool mapOf(CUtensorMap* m, const float* base, int K, int rows, int batch, int64_t ld, int64_t sBatch, int boxRows) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  MapKey key{base, K, rows, batch, ld, sBatch, boxRows, dev};
-  {
-    std::lock_guard<std::mutex> g(g_mapMu);
-    for (size_t i = g_maps.size(); i-- > 0;)
-      if (g_maps[i].first == key) {
-        *m = g_maps[i].second;
-        return true;
-      }
-  }
-  EncodeFn enc = encodeFn();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(batch)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 4,
-                           static_cast<cuuint64_t>(batch > 1 ? sBatch : ld * rows) * 4};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(kTK), static_cast<cuuint32_t>(boxRows), 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  if (enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
-  std::lock_guard<std::mutex> g(g_mapMu);
-  if (g_maps.size() >= 128) g_maps.erase(g_maps.begin());
-  g_maps.push_back({key, *m});
-  return true;
+  return cachedMapF32Sw128(m, base, K, rows, batch, ld, sBatch, kTK, boxRows);
 }
 
 template <int TM, int TN, int RM, int RN, int S, int CN = 1>

@@ -37,6 +37,56 @@ inline EncodeFn encodeFn() {
   return fn;
 }
 
+// host: 3-D map {K, rows, batch} of a row-major fp32 operand, box {boxK,
+// boxRows, 1}, 128-byte swizzle, cached by (pointer, geometry, device):
+// graph capture and repeated host calls re-use the encoded map
+// (cuTensorMapEncodeTiled costs host time on every synchronised call
+// otherwise). Shared by the TMA-fed FFMA GEMM and the tcgen05 GEMM.
+inline bool cachedMapF32Sw128(CUtensorMap* m, const float* base, int K, int rows, int batch, int64_t ld,
+                              int64_t sBatch, int boxK, int boxRows) {
+  struct Key {
+    const void* p;
+    int64_t K, rows, batch, ld, sb;
+    int boxK, boxRows, dev;
+    bool operator==(const Key& o) const {
+      return p == o.p && K == o.K && rows == o.rows && batch == o.batch && ld == o.ld && sb == o.sb &&
+             boxK == o.boxK && boxRows == o.boxRows && dev == o.dev;
+    }
+  };
+  static std::mutex mu;
+  static Key keys[128];
+  static CUtensorMap maps[128];
+  static int n = 0, next = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const Key key{base, K, rows, batch, ld, sBatch, boxK, boxRows, dev};
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (int i = 0; i < n; ++i)
+      if (keys[i] == key) {
+        *m = maps[i];
+        return true;
+      }
+  }
+  EncodeFn enc = encodeFn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(batch)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 4,
+                           static_cast<cuuint64_t>(batch > 1 ? sBatch : ld * rows) * 4};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(boxK), static_cast<cuuint32_t>(boxRows), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  std::lock_guard<std::mutex> g(mu);
+  keys[next] = key;  // a ring of the 128 most recent geometries
+  maps[next] = *m;
+  next = (next + 1) % 128;
+  if (n < 128) ++n;
+  return true;
+}
+
 __device__ __forceinline__ uint32_t smem(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -472,16 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // 3-D map {K, rows, batch} of a row-major fp32 operand; box {32, boxRows, 1}
 bool makeMap(CUtensorMap* m, const float* base, int K, int rows, int batch, int64_t ld, int64_t sBatch,
              int boxRows) {
-  sm100::EncodeFn enc = sm100::encodeFn();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(batch)};
-  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 4,
-                           static_cast<cuuint64_t>(batch > 1 ? sBatch : ld * rows) * 4};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(boxRows), 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return cachedMapF32Sw128(m, base, K, rows, batch, ld, sBatch, kBK, boxRows);  // (sm100.cuh: cached per geometry)
 }
 
 template <int BN, bool X3, bool L2 = false>
