@@ -46,6 +46,8 @@ struct FusedPlan {
   int bBytes[kFcMaxL];                      // one plane of each weight region
   int tcol[kFcMaxL];                        // TMEM column of each layer's accumulator
   int total;                                // bytes of the TMA landing (hi planes)
+  int tmaOut[kFcMaxL];                      // 1: layer l's return leaves by TMA tensor stores from its
+                                            // swizzled tile in the A hi plane (the next layer's A)
   const float* bias[kFcMaxL];
   float* O[kFcMaxL];
 };
@@ -92,6 +94,8 @@ template <int NL, bool X3>
 __global__ void __launch_bounds__(kThreadsFc, 1)
     tc_fc_fused_kernel(const __grid_constant__ CUtensorMap tIn, const __grid_constant__ CUtensorMap tW0,
                        const __grid_constant__ CUtensorMap tW1, const __grid_constant__ CUtensorMap tW2,
+                       const __grid_constant__ CUtensorMap tO0, const __grid_constant__ CUtensorMap tO1,
+                       const __grid_constant__ CUtensorMap tO2,
                        const __grid_constant__ FusedPlan p) {
   extern __shared__ uint8_t smraw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -174,6 +178,10 @@ __global__ void __launch_bounds__(kThreadsFc, 1)
       if (electSync()) mmaCommit(mmaDone);
       __syncwarp();
     }
+    if (l > 0 && p.tmaOut[l - 1]) {  // layer l-1's tile stays in place until its stores have read it
+      if (tid == 0) tmaStoreWaitRead();
+      __syncthreads();
+    }
     mbarWait(mmaDone, l & 1, 1);
     TCFC_STAMP(3 + 2 * l);
     tcFenceAfter();
@@ -197,7 +205,11 @@ __global__ void __launch_bounds__(kThreadsFc, 1)
           op[q] = n < p.N[l] ? fmaxf(v[j + q] + bl[n], 0.0f) : 0.0f;
         }
         const int n = c0 + j;
-        if (grow < p.batch && n < p.N[l]) {
+        if (p.tmaOut[l]) {
+          // the return leaves by TMA from the swizzled tile (below); for the
+          // last layer the dead A plane holds it
+          if (last || n >= p.K[l + 1]) *reinterpret_cast<float4*>(aHi + swOff(row, n)) = o;
+        } else if (grow < p.batch && n < p.N[l]) {
           float* dst = p.O[l] + (int64_t)grow * p.N[l] + n;
           if (n + 4 <= p.N[l] && (p.N[l] & 3) == 0) {
             *reinterpret_cast<float4*>(dst) = o;
@@ -223,7 +235,15 @@ __global__ void __launch_bounds__(kThreadsFc, 1)
     tcFenceBefore();
     __syncthreads();
     TCFC_STAMP(4 + 2 * l);
+    if (p.tmaOut[l] && tid == 0) {
+      // coalesced by the TMA engine: lane-per-row stores put 32 separate
+      // 16-byte L2 writes in every warp store (~1.4 us of layer 1's epilogue)
+      const CUtensorMap* to[3] = {&tO0, &tO1, &tO2};
+      for (int c = 0; c * 32 < p.N[l]; ++c) tmaStore3d(to[l], aHi + c * kRowsTc * 128, c * 32, row0, 0);
+      tmaStoreCommit();
+    }
   }
+  if (tid == 0) tmaStoreWaitAll();  // (no-op without TMA stores) the tiles are read before the CTA exits
   if (warp == 0) {
     tcFenceAfter();
     tmemFree<kCols>(tmem);
@@ -276,6 +296,11 @@ int planFused(const FcChainArgs& a, bool x3, FusedPlan& p) {
     p.O[l] = a.L[l].O;
   }
   p.aBytes = aMax;
+  // TMA-stored returns: 16-byte rows, the whole padded tile inside the A plane,
+  // and (not last) the next layer's A covering every column of it
+  for (int l = 0; l < a.layers; ++l)
+    p.tmaOut[l] = p.N[l] % 4 == 0 && (reinterpret_cast<uintptr_t>(p.O[l]) & 15) == 0 &&
+                  (p.N[l] + 31) / 32 * kRowsTc * 128 <= aMax;
   off = aMax * (x3 ? 2 : 1);
   p.total = p.K[0] / 32 * kRowsTc * 128;
   for (int l = 0; l < a.layers; ++l) {
@@ -298,10 +323,14 @@ cudaError_t launchFusedT(const FcChainArgs& a, cudaStream_t s) {
   if (!mapFc(&tIn, a.I, a.L[0].kred, a.batch, a.ldi, kRowsTc)) return cudaErrorInvalidValue;
   for (int l = 0; l < NL; ++l)
     if (!mapFc(&tw[l], a.L[l].W, a.L[l].kred, a.L[l].out, a.L[l].ldw, up16(a.L[l].out))) return cudaErrorInvalidValue;
+  CUtensorMap to[3]{};
+  for (int l = 0; l < NL; ++l)  // {N, rows} returns, box {32, 128}: the epilogue's swizzled tile
+    if (p.tmaOut[l] && !mapFc(&to[l], a.L[l].O, a.L[l].out, a.batch, a.L[l].out, kRowsTc)) p.tmaOut[l] = 0;
   auto kern = tc_fc_fused_kernel<NL, X3>;
   cudaError_t e = ensureFuncAttrs(reinterpret_cast<const void*>(kern), smemBytes);
   if (e != cudaSuccess) return e;
-  kern<<<(a.batch + kRowsTc - 1) / kRowsTc, kThreadsFc, smemBytes, s>>>(tIn, tw[0], tw[1], tw[2], p);
+  kern<<<(a.batch + kRowsTc - 1) / kRowsTc, kThreadsFc, smemBytes, s>>>(tIn, tw[0], tw[1], tw[2], to[0], to[1],
+                                                                        to[2], p);
   return cudaGetLastError();
 }
 
