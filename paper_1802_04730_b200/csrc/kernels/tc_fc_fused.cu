@@ -75,7 +75,7 @@ __device__ __forceinline__ void splitPlane(float* hi, float* lo, int bytes, int 
 
 #ifdef TCB_TCFC_TRACE
 // diagnostic build only (profiles/tcfc_trace.cu): globaltimer stamps of CTA 0
-__device__ unsigned long long g_tcfc_trace[8];
+__device__ unsigned long long g_tcfc_trace[32];
 #define TCFC_STAMP(ev)                                              \
   do {                                                              \
     unsigned long long t_;                                          \
@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(kThreadsFc, 1)
       }
       if (electSync()) mmaCommit(mmaDone);
       __syncwarp();
+      if (l < 3) TCFC_STAMP(20 + l);  // (trace build) this layer's MMAs issued
     }
     if (l > 0 && p.tmaOut[l - 1]) {  // layer l-1's tile stays in place until its stores have read it
       if (tid == 0) tmaStoreWaitRead();

@@ -40,12 +40,13 @@ int main() {
     cudaError_t err = cudaDeviceSynchronize();
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    unsigned long long tr[8];
+    unsigned long long tr[32];
     cudaMemcpyFromSymbol(tr, g_tcfc_trace, sizeof(tr));
     printf("%s: event %.2f us (%s / %s)\n", math == kMathTf32 ? "tf32" : "3xtf32", ms * 1e3, cudaGetErrorString(le),
            cudaGetErrorString(err));
     const char* nm[8] = {"entry", "landed", "split", "L1 mma", "L1 epi", "L2 mma", "L2 epi", "L3 mma"};
     for (int i = 1; i < 8; ++i) printf("  %-8s +%.2f us\n", nm[i], (tr[i] - tr[0]) * 1e-3);
+    for (int i = 20; i < 23; ++i) printf("  L%d MMAs issued +%.2f us\n", i - 19, (tr[i] - tr[0]) * 1e-3);
   }
   return 0;
 }
