@@ -231,13 +231,15 @@ class OpInstance:
 
 DOM_NOTES = {
     "2FCRelu": "Latency bound, not byte bound: every output is one sequential FFMA chain of 1128 + 128 dependent "
-               "steps (chain_floor_us at 4 cycles a step); it runs ~6.3 cycles a step because two CTAs share an "
-               "SM and their LDS.128 operand reads saturate its shared-memory pipe (one CTA per SM: ~5.0, "
-               "profiles/r02_chain_probe2.txt), after a ~1.5 us load prologue (DESIGN.md section 8).",
-    "tbmm": "500 batches of 26x26 outputs, 72-step chains: one wave of CTAs (slab kernel, 9 rows per warp); its "
-            "8.84 MB land in ~2-2.5 us (cold-read floor ~3.1 us with launch) and the exact chains need ~1.5-2 us "
-            "of SM time at the measured 0.5-0.6 warp-FFMA per cycle per SMSP, overlapped only chunk by chunk "
-            "(DESIGN.md sections 5 and 12).",
+               "steps (chain_floor_us at 4 cycles a step); layer 1 runs two weight columns per thread at ~5.9 "
+               "cycles a step (LDS.128 operand writeback of two CTAs per SM; one CTA per SM: ~5.0, "
+               "profiles/r02_chain_probe2.txt) after ~1.1 us of prologue (copies issued by thread 0 first, "
+               "landed ~2100 cycles after entry, profiles/r02_fc_early/; DESIGN.md section 8).",
+    "tbmm": "500 batches of 26x26 outputs, 72-step chains, one wave of CTAs (slab kernel, 9 rows per warp). Phase "
+            "trace (profiles/r02_slab_ws/trace_slab_c9_c4_c7.txt): its 8.84 MB are in by ~2.0 us (~4.6 TB/s; the "
+            "cp.async issue itself stalls until then), then three 24-step chunks at ~0.9 us each, bound by the "
+            "shared-memory pipe (a broadcast LDS.128 costs 2 wavefronts), stores done ~5.2 us (DESIGN.md "
+            "sections 5 and 12).",
     "MLP3": "Three short dependent layers (128, 64, 32 steps): latency bound, see chain_floor_us.",
 }
 
