@@ -72,8 +72,11 @@ struct TcCfg {
   static constexpr int kABytes = kBM * kBK * 4;
   static constexpr int kBBytes = BN * kBK * 4;
   // a stage: the landed fp32 A and B k-blocks (+ B's lo half for 3xTF32;
-  // A's hi and lo halves go to TMEM, the MMA's A operand there)
-  static constexpr int kStage = kABytes + kBBytes + (X3 ? kBBytes : 0);
+  // A's hi and lo halves go to TMEM, the MMA's A operand there). With B no
+  // wider than A, B's lo half overwrites the landed A once it is in TMEM
+  // (kLoInA): 32 KB stages, a 6-deep ring at BN = 128 instead of 4
+  static constexpr bool kLoInA = X3 && BN <= kBM;
+  static constexpr int kStage = kABytes + kBBytes + (X3 && !kLoInA ? kBBytes : 0);
   static constexpr int kPartLd = BN + 4;  // partial tile row stride (floats)
   static constexpr int kPartBytes = kBM * kPartLd * 4;
   static constexpr int kBudget = 200 * 1024;
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   auto aBig = [&](int s) { return sm + s * Cfg::kStage; };
   auto bBig = [&](int s) { return sm + s * Cfg::kStage + Cfg::kABytes; };
-  auto bLo = [&](int s) { return sm + s * Cfg::kStage + Cfg::kABytes + Cfg::kBBytes; };
+  auto bLo = [&](int s) { return Cfg::kLoInA ? aBig(s) : sm + s * Cfg::kStage + Cfg::kABytes + Cfg::kBBytes; };
   // 3xTF32: TMEM columns of stage s's A operand, hi at +0, lo at +kBK
   auto aCol = [&](int s) { return static_cast<uint32_t>(Cfg::kAccCols + s * 2 * kBK); };
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + Cfg::kRing);
@@ -231,6 +234,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmemStore32(tl, hi);
           tmemStore32(tl + kBK, lo);
         }
+        // B's lo half lands where A was: every conversion thread has its A row
+        // in registers first
+        if constexpr (Cfg::kLoInA) asm volatile("bar.sync 1, 128;" ::: "memory");
         // B: hi is the landed tile itself (the MMA reads rzTf32 of it); lo to
         // the stage's second buffer
         const float4* bv = reinterpret_cast<const float4*>(bBig(s));
