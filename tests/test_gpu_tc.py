@@ -195,6 +195,31 @@ def test_fc_chains_tc(env, math):
         assert e <= tol(math, K, opscale(inp, W))
 
 
+@pytest.mark.parametrize("math", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("B,K1,N1,N2,N3", [(77, 128, 64, 32, 2), (200, 64, 96, 64, 8), (130, 32, 64, 32, 36)])
+def test_fc_fused_tc_ragged(env, math, B, K1, N1, N2, N3):
+    """The one-kernel tcgen05 FC chain at ragged shapes: batches that leave a
+    partial 128-row CTA, layer widths whose TMA-stored returns end inside a
+    32-column box (clipped by the tensor map) and a last layer narrower than
+    a 16-byte row (lane stores)."""
+    ee, orc = env
+    rng = orc.rng(B + N1 + N3)
+    O1 = rng.f32((B, K1))
+    M2, C2, M3, C3b, M4, C4 = (rng.f32((N1, K1)), rng.f32((N1,)), rng.f32((N2, N1)), rng.f32((N2,)),
+                               rng.f32((N3, N2)), rng.f32((N3,)))
+    (q1, q2, q3, q4), desc = run(ee, "MLP3", [O1, M2, C2, M3, C3b, M4, C4],
+                                 [O1, np.zeros((B, N1), np.float32), np.zeros((B, N2), np.float32),
+                                  np.zeros((B, N3), np.float32)], math)
+    assert "fused chain" in desc["kernel"]
+    assert np.array_equal(q1, O1)
+    for got, (inp, W, b, K) in zip((q2, q3, q4), ((O1, M2, C2, K1), (q2, M3, C3b, N1), (q3, M4, C4, N2))):
+        ee_, eb = check_emu(f"fused chain {B}x{K1} layer K={K}", math, K, got, emu.fc_relu(inp, W, b, math),
+                            opscale(inp, W))
+        e = max_rel(orc.fc_relu(inp, W, b), got)
+        record(f"fused chain {B}x{K1} layer K={K}", math, K, e, None, None, ee_, eb)
+        assert e <= tol(math, K, opscale(inp, W))
+
+
 def test_tc_explicit_plan_and_errors(env):
     from paper_1802_04730_b200 import TcError, options_baseline
     ee, orc = env
